@@ -1,0 +1,481 @@
+#!/usr/bin/env python
+"""bench.py -- BASELINE.json's metric on a B200: effective HBM GB/s of the fused kernels.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
+                    [--kernel suite|axpydot|bicgk|atax|gesummv|gemver] [--no-e2e]
+
+A "step" is one pass of the hot path over the suite: the five fused sequences
+at BASELINE.json's bench sizes (AXPYDOT n=2^27; BiCGK, ATAX, GEMVER n=32768;
+GESUMMV n=24576), fp64, seeded synthetic inputs generated on the device.
+`value` = (sum of the sequences' minimum-traffic bytes) / (device
+time of the step), inputs resident in HBM; every input is >= 4 GiB >> L2
+(126 MB), so no L2 flush is needed between iterations.
+
+Extra objects on the JSON line: `per_kernel` (achieved GB/s of each sequence),
+`roofline` (the slowest-by-share sequence against MEASURED_PEAKS.json),
+`e2e` (the same suite through the reference-facing C symbols with PINNED HOST
+buffers, copies inside the timed region), `cpu_baseline` (the reference's own
+generated C on this box's cores, bounded sample), `clocks`, `gpu_launches`.
+
+N > 1 (torchrun): rows are sharded over ranks (paper_1205_1098_b200.sharded),
+one NCCL all-reduce per kernel, total problem size fixed -> "scaling": "strong".
+
+`--impl reference` times the reference's CPU implementation (oracle/_ref, the
+generated C compiled in the build container; else the oracle port) on the
+host cores, same metric; rank 0 only.
+"""
+from __future__ import annotations
+
+import argparse
+import ctypes
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+from pathlib import Path
+
+REPO = Path(__file__).resolve().parent
+sys.path.insert(0, str(REPO))
+
+SUITE = ("axpydot", "bicgk", "atax", "gesummv", "gemver")
+BENCH = {"axpydot": (1 << 27, 1), "bicgk": (32768, 32768), "atax": (32768, 32768),
+         "gesummv": (24576, 24576), "gemver": (32768, 32768)}
+# bounded CPU sample: out of last-level cache, a few seconds on 8 cores
+CPU_SAMPLE = {"axpydot": (1 << 26, 1), "bicgk": (16384, 16384), "atax": (16384, 16384),
+              "gesummv": (12288, 12288), "gemver": (16384, 16384)}
+
+
+def bytes_min(kernel: str, M: int, N: int) -> float:
+    """SURVEY.md section 8d (same table as bto_bytes_min in the library)."""
+    m, n = float(M), float(N)
+    return {"axpydot": 32 * m, "bicgk": 8 * m * n + 16 * m + 16 * n,
+            "atax": 8 * m * n + 16 * n, "gesummv": 16 * m * n + 8 * n + 8 * m,
+            "gemver": 24 * m * n + 32 * m + 40 * n}[kernel]
+
+
+def measured_peak() -> tuple[float, str]:
+    path = REPO / "MEASURED_PEAKS.json"
+    if path.exists():
+        try:
+            return float(json.loads(path.read_text())["hbm_gbs"]), "measured (MEASURED_PEAKS.json)"
+        except Exception:
+            pass
+    return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+# ---------------------------------------------------------------------------
+# clocks during the timed region
+
+class ClockSampler:
+    BAD = {0x8: "hw_slowdown", 0x40: "hw_thermal_slowdown", 0x20: "sw_thermal_slowdown"}
+    NOTE = {0x4: "sw_power_cap", 0x80: "hw_power_brake", 0x1: "gpu_idle",
+            0x2: "app_clocks", 0x100: "display", 0x10: "sync_boost"}
+
+    def __init__(self, index: int = 0, period: float = 0.05):
+        self.index, self.period = index, period
+        self.samples: list[int] = []
+        self.reasons: set[str] = set()
+        self.max_mhz = None
+        self._stop = threading.Event()
+        self._thread = None
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        except Exception:
+            self.nv = None
+
+    def _loop(self):
+        nv = self.nv
+        while not self._stop.is_set():
+            try:
+                self.samples.append(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
+                mask = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for bit, name in {**self.BAD, **self.NOTE}.items():
+                    if mask & bit and name != "gpu_idle":
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            self._stop.wait(self.period)
+
+    def __enter__(self):
+        if self.nv is not None:
+            self._thread = threading.Thread(target=self._loop, daemon=True)
+            self._thread.start()
+        return self
+
+    def __exit__(self, *exc):
+        self._stop.set()
+        if self._thread:
+            self._thread.join()
+
+    def summary(self) -> dict:
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": ["unavailable"]}
+        return {"sm_mhz": int(statistics.median(self.samples)), "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons)}
+
+
+# ---------------------------------------------------------------------------
+# CPU arm: the reference's generated C (oracle/_ref) or the oracle port
+
+def cpu_baseline(steps: int = 2, warmup: int = 1, kernels=SUITE) -> dict:
+    import numpy as np
+    sys.path.insert(0, str(REPO / "tests"))
+    import oracle_lib as O
+
+    cores_avail = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") \
+        else (os.cpu_count() or 1)
+    use_ref = O.ref_available()
+    if use_ref:
+        ladder = O.ref_thread_ladder("bicgk")
+        threads = max(t for t in ladder if t <= max(1, cores_avail))
+        kind = "reference"
+    else:
+        O.ensure_built()
+        threads = max(1, cores_avail)
+        kind = "port"
+    rng = np.random.default_rng(0)
+    per = {}
+    tot_bytes = tot_sec = 0.0
+    for name in kernels:
+        M, N = CPU_SAMPLE[name]
+        ext = {"M": M} if name == "axpydot" else {"M": M, "N": N}
+        inputs = {}
+        for pname, cls in O.PARAMS[name]:
+            if cls == "s":
+                inputs[pname] = float(rng.uniform(-1, 1))
+            elif cls == "a":
+                if pname in ("A", "B"):
+                    shape = (M, N)
+                elif name == "axpydot":
+                    shape = (M,)
+                else:
+                    rowvec = {"bicgk": ("r",), "gemver": ("u1", "u2", "y")}.get(name, ())
+                    shape = (M,) if pname in rowvec else (N,)
+                arr = np.empty(shape)
+                arr.ravel()[:] = rng.random(arr.size) * 2 - 1
+                inputs[pname] = arr
+        run, _ = O.bind_ref(name, inputs, ext, f"t{threads}") if use_ref else \
+            O.bind_oracle(name, inputs, ext, threads)
+        for _ in range(warmup):
+            run()
+        times = []
+        for _ in range(steps):
+            t0 = time.perf_counter()
+            run()
+            times.append(time.perf_counter() - t0)
+        sec = statistics.mean(times)
+        b = bytes_min(name, M, N)
+        per[name] = {"gbs": b / sec / 1e9, "ms": sec * 1e3, "extents": [M, N]}
+        tot_bytes += b
+        tot_sec += sec
+        del inputs
+    return {"value": tot_bytes / tot_sec / 1e9, "unit": "GB/s", "cores": threads,
+            "kind": kind, "ms_per_step": tot_sec * 1e3, "per_kernel": per,
+            "sample": "same five sequences at out-of-LLC sizes: AXPYDOT n=2^26, BiCGK/ATAX/"
+                      "GEMVER n=16384, GESUMMV n=12288; the C "
+                      "function alone on preallocated buffers; mean of %d reps after %d warm-up" % (steps, warmup)}
+
+
+def run_reference_arm(args) -> int:
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    base = cpu_baseline(steps=max(1, args.steps), warmup=max(1, min(args.warmup, 3)))
+    line = {
+        "impl": "reference", "metric": "effective HBM GB/s (min bytes/time), fused suite",
+        "value": base["value"], "unit": "GB/s", "n_gpus": args.gpus, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": base["ms_per_step"], "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": "suite5 (AXPYDOT, BiCGK, ATAX, GESUMMV, GEMVER), bounded CPU sample",
+                   "sample": base["sample"]},
+        "cpu_baseline": {k: base[k] for k in ("value", "unit", "cores", "kind", "sample")},
+        "per_kernel": base["per_kernel"],
+        "e2e": {"value": base["value"], "unit": "GB/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+        "gpu_launches": 0,
+    }
+    print(json.dumps(line))
+    return 0
+
+
+# ---------------------------------------------------------------------------
+# GPU arm
+
+class Suite:
+    """Device buffers + launch closures for the five sequences on one rank."""
+
+    def __init__(self, torch, rank: int, world: int, kernels):
+        from paper_1205_1098_b200 import _native
+        from paper_1205_1098_b200.sharded import GpuShardOps, ShardedRunner, TorchComm, row_block
+        self.torch, self.rank, self.world = torch, rank, world
+        self.native = _native
+        self.ops = GpuShardOps()
+        comm = TorchComm() if world > 1 else None
+        self.runner = ShardedRunner(self.ops, comm, rank, world)
+        self.kernels = kernels
+        dev = torch.device("cuda", torch.cuda.current_device())
+        gen = torch.Generator(device=dev).manual_seed(1234 + rank)
+
+        def rnd(*shape):
+            return torch.rand(*shape, dtype=torch.float64, device=dev, generator=gen) * 2 - 1
+
+        n = 32768
+        lo, hi = row_block(n, rank, world)
+        self.rows = hi - lo
+        self.n = n
+        need_mat = any(k in kernels for k in ("bicgk", "atax", "gemver", "gesummv"))
+        if need_mat:
+            self.A = rnd(self.rows, n)
+            self.Bm = rnd(self.rows, n)            # GEMVER output; GESUMMV's 2nd input lives here
+        self.vecN = [rnd(n) for _ in range(4)]     # p/x, v1, v2, z
+        self.vecM = [rnd(self.rows) for _ in range(4)]   # r/y, u1, u2
+        self.q = torch.empty(self.rows, dtype=torch.float64, device=dev)
+        self.s = torch.empty(n, dtype=torch.float64, device=dev)
+        self.x = torch.empty(n, dtype=torch.float64, device=dev)
+        self.colsum = torch.empty(n, dtype=torch.float64, device=dev)
+        self.w = torch.empty(self.rows, dtype=torch.float64, device=dev)
+        # GESUMMV n = 24576 : views into the big buffers
+        g = 24576
+        glo, ghi = row_block(g, rank, world)
+        self.grows, self.g = ghi - glo, g
+        if "gesummv" in kernels:
+            self.GA = self.A.view(-1)[: self.grows * g].view(self.grows, g)
+            self.GB = self.Bm.view(-1)[: self.grows * g].view(self.grows, g)
+            self.gy = torch.empty(self.grows, dtype=torch.float64, device=dev)
+        # AXPYDOT n = 2^27 sliced over ranks
+        a = 1 << 27
+        alo, ahi = row_block(a, rank, world)
+        self.an = ahi - alo
+        if "axpydot" in kernels:
+            self.aw, self.av, self.au = rnd(self.an), rnd(self.an), rnd(self.an)
+            self.az = torch.empty(self.an, dtype=torch.float64, device=dev)
+            self.abeta = torch.empty(1, dtype=torch.float64, device=dev)
+
+    def launch(self, name: str):
+        r = self.runner
+        if name == "axpydot":
+            r.axpydot(self.aw, self.av, self.au, 0.37, self.az, self.abeta)
+        elif name == "bicgk":
+            r.bicgk(self.A, self.vecN[0], self.vecM[0], self.q, self.s)
+        elif name == "atax":
+            r.atax(self.A, self.vecN[0], self.s)
+        elif name == "gesummv":
+            r.gesummv(0.61, -0.27, self.GA, self.GB, self.vecN[0][: self.g], self.gy)
+        elif name == "gemver":
+            if self.world > 1:
+                r.gemver(self.A, self.vecM[1], self.vecN[1], self.vecM[2], self.vecN[2], 0.83,
+                         -0.41, self.vecM[0], self.vecN[3], self.Bm, self.x, self.w, self.colsum)
+            else:
+                self.ops.gemver(self.A, self.vecM[1], self.vecN[1], self.vecM[2], self.vecN[2],
+                                0.83, -0.41, self.vecM[0], self.vecN[3], self.Bm, self.x, self.w)
+
+
+def e2e_host(torch, kernels, steps: int, warmup: int) -> dict:
+    """The suite through the reference's C symbols with pinned HOST buffers:
+    host->device copies of every input and device->host copies of every output
+    are inside the timed region (the call returns when outputs are on the host)."""
+    from paper_1205_1098_b200 import _native
+    lib = _native.load()
+
+    def pinned(count):
+        return torch.empty(count, dtype=torch.float64, pin_memory=True)
+
+    n, g, a = 32768, 24576, 1 << 27
+    big_in = pinned(n * n)
+    chunk = 1 << 26                      # fill through the GPU: host RNG is slow
+    for off in range(0, n * n, chunk):
+        big_in[off:off + chunk].copy_(
+            torch.rand(chunk, dtype=torch.float64, device="cuda") * 2 - 1)
+    big_out = pinned(n * n)
+    vec = [pinned(n).uniform_(-1, 1) for _ in range(8)]
+    outv = [pinned(n) for _ in range(3)]
+    scalar = pinned(1)
+    P = lambda t: ctypes.c_void_p(t.data_ptr())
+    h2d = d2h = 0.0
+    calls = []
+    if "axpydot" in kernels:
+        q = a
+        w_, v_, u_ = big_in[:q], big_in[q:2 * q], big_in[2 * q:3 * q]
+        calls.append(lambda: lib.axpydot(P(w_), P(v_), P(u_), 0.37, P(big_out[:q]), P(scalar), q))
+        h2d += 24.0 * q
+        d2h += 8.0 * q + 8
+    if "bicgk" in kernels:
+        calls.append(lambda: lib.bicgk(P(big_in), P(vec[0]), P(vec[1]), P(outv[0]), P(outv[1]), n, n))
+        h2d += 8.0 * n * n + 16 * n
+        d2h += 16.0 * n
+    if "atax" in kernels:
+        calls.append(lambda: lib.atax(P(big_in), P(vec[0]), P(outv[0]), n, n))
+        h2d += 8.0 * n * n + 8 * n
+        d2h += 8.0 * n
+    if "gesummv" in kernels:
+        A_, B_ = big_in[: g * g], big_in[g * g: 2 * g * g] if 2 * g * g <= n * n else big_in[: g * g]
+        calls.append(lambda: lib.gesummv(0.61, -0.27, P(A_), P(B_), P(vec[0]), P(outv[0]), g, g))
+        h2d += 16.0 * g * g + 8 * g
+        d2h += 8.0 * g
+    if "gemver" in kernels:
+        calls.append(lambda: lib.gemver(P(big_in), P(vec[1]), P(vec[2]), P(vec[3]), P(vec[4]),
+                                        0.83, -0.41, P(vec[5]), P(vec[6]), P(big_out),
+                                        P(outv[1]), P(outv[2]), n, n))
+        h2d += 8.0 * n * n + 48 * n
+        d2h += 8.0 * n * n + 16 * n
+
+    def step():
+        for call in calls:
+            call()
+            _native.check()
+
+    for _ in range(warmup):
+        step()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        step()
+    torch.cuda.synchronize()
+    sec = (time.perf_counter() - t0) / steps
+    total = sum(bytes_min(k, *BENCH[k]) for k in kernels)
+    return {"value": total / sec / 1e9, "unit": "GB/s", "ms_per_step": sec * 1e3,
+            "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+            "api": "C symbols of include/bto_b200.h section 1 with pinned host pointers"}
+
+
+def run_gpu_arm(args) -> int:
+    import torch
+    import torch.distributed as dist
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if not torch.cuda.is_available():
+        print(json.dumps({"error": "no CUDA device; this bench has no CPU fallback"}))
+        return 2
+    torch.cuda.set_device(local_rank)
+    if world > 1:
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    kernels = SUITE if args.kernel == "suite" else (args.kernel,)
+
+    from paper_1205_1098_b200 import _native
+    _native.load()
+    suite = Suite(torch, rank, world, kernels)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    for _ in range(max(3, args.warmup)):
+        for k in kernels:
+            suite.launch(k)
+    barrier()
+
+    ev = [[(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+           for _ in kernels] for _ in range(args.steps)]
+    first, last = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    launches0 = _native.kernel_launches()
+    with ClockSampler(local_rank) as clocks:
+        barrier()
+        first.record()
+        for s in range(args.steps):
+            for i, k in enumerate(kernels):
+                ev[s][i][0].record()
+                suite.launch(k)
+                ev[s][i][1].record()
+        last.record()
+        barrier()
+    launches = _native.kernel_launches() - launches0
+    total_ms = first.elapsed_time(last)
+    per_ms = {k: statistics.mean(ev[s][i][0].elapsed_time(ev[s][i][1]) for s in range(args.steps))
+              for i, k in enumerate(kernels)}
+    per_min = {k: min(ev[s][i][0].elapsed_time(ev[s][i][1]) for s in range(args.steps))
+               for i, k in enumerate(kernels)}
+    if world > 1:
+        t = torch.tensor([total_ms] + [per_ms[k] for k in kernels], dtype=torch.float64,
+                         device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        vals = t.tolist()
+        total_ms = vals[0]
+        per_ms = dict(zip(kernels, vals[1:]))
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return 0
+
+    ms_per_step = total_ms / args.steps
+    total_bytes = sum(bytes_min(k, *BENCH[k]) for k in kernels)
+    value = total_bytes / (ms_per_step * 1e-3) / 1e9
+    peak, peak_src = measured_peak()
+    per_kernel = {}
+    for k in kernels:
+        gbs = bytes_min(k, *BENCH[k]) / (per_ms[k] * 1e-3) / 1e9
+        per_kernel[k] = {"gbs": round(gbs, 1), "ms": round(per_ms[k], 4),
+                         "ms_min": round(per_min[k], 4),
+                         "frac_of_peak": round(gbs / (peak * world), 4),
+                         "bytes_min": bytes_min(k, *BENCH[k]), "extents": list(BENCH[k])}
+    dominant = max(kernels, key=lambda k: per_ms[k])
+    dom = per_kernel[dominant]
+    line = {
+        "metric": "effective HBM GB/s (min bytes/time), fused suite",
+        "value": round(value, 1), "unit": "GB/s", "n_gpus": world, "steps": args.steps,
+        "warmup": max(3, args.warmup), "ms_per_step": round(ms_per_step, 4),
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+        "dtype": "f64", "data": "synthetic",
+        "config": {
+            "workload": "suite5: AXPYDOT n=2^27, BiCGK n=32768, ATAX n=32768, GESUMMV n=24576, "
+                        "GEMVER n=32768" if args.kernel == "suite" else
+                        f"{args.kernel} at BASELINE bench size {BENCH[args.kernel]}",
+            "parallelism": f"row-shard x{world}" if world > 1 else "single GPU",
+            "l2": "every input >= 4 GiB >> 126 MB L2; no flush between iterations",
+            "timing": "CUDA events on the launch stream, max over ranks",
+        },
+        "per_kernel": per_kernel,
+        "roofline": {"bound": "hbm", "kernel": dominant, "achieved": dom["gbs"],
+                     "peak": peak * world, "unit": "GB/s",
+                     "frac": round(dom["gbs"] / (peak * world), 4),
+                     "traffic": None, "peak_source": peak_src,
+                     "algorithmic_bytes": dom["bytes_min"]},
+        "clocks": clocks.summary(),
+        "gpu_launches": launches,
+    }
+    line["suite_frac_of_peak"] = round(value / (peak * world), 4)
+    if world == 1 and not args.no_e2e:
+        try:
+            line["e2e"] = e2e_host(torch, kernels, steps=max(1, min(args.steps, 3)), warmup=1)
+        except Exception as exc:  # e.g. not enough pinned host memory
+            line["e2e"] = {"value": None, "error": f"{type(exc).__name__}: {exc}"}
+    if world == 1 and not args.no_cpu:
+        try:
+            base = cpu_baseline(steps=2, warmup=1, kernels=kernels)
+            line["cpu_baseline"] = {k: base[k] for k in ("value", "unit", "cores", "kind", "sample")}
+            line["cpu_baseline"]["per_kernel"] = {k: round(v["gbs"], 2)
+                                                  for k, v in base["per_kernel"].items()}
+        except Exception as exc:
+            line["cpu_baseline"] = {"value": None, "error": f"{type(exc).__name__}: {exc}"}
+    print(json.dumps(line))
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def main() -> int:
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=("b200", "reference"), default="b200")
+    ap.add_argument("--kernel", choices=("suite",) + SUITE, default="suite")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference_arm(args)
+    return run_gpu_arm(args)
+
+
+if __name__ == "__main__":
+    raise SystemExit(main())

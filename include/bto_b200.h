@@ -1,0 +1,157 @@
+/* bto_b200.h -- C ABI of libbto_b200.so, the B200 (sm_100a) drop-in for the
+ * reference's generated-C kernels.
+ *
+ * Boundary being replaced.  The reference (matfuse) prints one C function per
+ * kernel spec and calls it through ctypes:
+ *   - signature rule ........ cemit.py:225-241 (kernel_params): inputs in
+ *     declaration order (array -> const double*, scalar -> double by value),
+ *     outputs in declaration order (double*; a scalar output is double*),
+ *     then the extents in sorted order (M[, N]) as long; returns void;
+ *   - symbol name ........... spec.name.lower()            (cemit.py:261)
+ *   - caller ................ runtime.run_kernel            (runtime.py:99-150)
+ *     which dlopens the library, looks the symbol up by kernel name and
+ *     passes numpy (HOST) buffers; outputs arrive NaN-filled and must be
+ *     fully overwritten (runtime.py:108,130);
+ *   - layout ................ fp64, matrices dense row-major, i*N + j
+ *     (cemit.py:54-72).
+ *
+ * Section 1 exports exactly those symbols, so the reference's own
+ * `run_kernel(Path("libbto_b200.so"), kernel, graph, inputs, extents)` works
+ * unchanged.  Every pointer argument may be a host pointer (pageable or
+ * pinned) or a device pointer; the library asks the driver which.  If any
+ * argument is host memory the call stages it through device memory and
+ * returns when the outputs are back on the host; if all are device pointers
+ * the kernels are enqueued on the library stream (bto_set_stream, default the
+ * legacy default stream) and the call returns immediately.
+ *
+ * The functions return void like the reference's, so failures are reported
+ * through bto_last_error(); nothing here falls back to the CPU.
+ */
+#ifndef BTO_B200_H
+#define BTO_B200_H
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define BTO_B200_ABI_VERSION 1
+
+/* ---- error channel (thread-local; cleared at the start of every call) ---- */
+enum {
+    BTO_OK = 0,
+    BTO_ERR_CUDA = 1,         /* a CUDA runtime call or launch failed         */
+    BTO_ERR_INVALID = 2,      /* negative extent, null pointer, bad argument  */
+    BTO_ERR_NO_DEVICE = 3,    /* no sm_100 device visible                     */
+    BTO_ERR_ALLOC = 4         /* workspace / staging allocation failed        */
+};
+int         bto_last_error(void);
+const char *bto_last_error_string(void);
+void        bto_clear_error(void);
+
+/* ---- 1. drop-in symbols: the reference's generated-C signatures ----------
+ * Hot path (BASELINE.json north_star); replaces the functions cemit.py
+ * prints for kernels/{axpydot,bicgk,atax,gesummv,gemver}.bto.              */
+void axpydot(const double *w, const double *v, const double *u, double alpha,
+             double *z, double *beta, long M);
+void bicgk(const double *A, const double *p, const double *r,
+           double *q, double *s, long M, long N);
+void atax(const double *A, const double *x, double *y, long M, long N);
+void gesummv(double alpha, double beta, const double *A, const double *B,
+             const double *x, double *y, long M, long N);
+void gemver(const double *A, const double *u1, const double *v1,
+            const double *u2, const double *v2, double alpha, double beta,
+            const double *y, const double *z,
+            double *B, double *x, double *w, long M, long N);
+/* Rest of the reference corpus (corpus.py:18-21 + BATAX), same primitives.  */
+void vadd(const double *w, const double *y, const double *z, double *x, long M);
+void waxpby(double alpha, const double *x, double beta, const double *y,
+            double *w, long M);
+void dgemv(double alpha, const double *A, const double *x, double beta,
+           const double *y, double *z, long M, long N);
+void dgemvt(double alpha, double beta, const double *A, const double *y,
+            const double *z, double *x, double *w, long M, long N);
+void batax(const double *x, double beta, const double *A, double *y,
+           long M, long N);
+
+/* ---- 2. asynchronous variants: DEVICE pointers only, explicit stream ------
+ * Same argument order plus a cudaStream_t (as void*).  Return BTO_OK or an
+ * error code (also left in bto_last_error).  These are what the timing loop
+ * (the replacement for cost.py:163-208 / cemit.py:294-359) and the sharded
+ * runtime call.                                                             */
+typedef void *bto_stream_t;
+
+int bto_axpydot_async(const double *w, const double *v, const double *u,
+                      double alpha, double *z, double *beta, long M,
+                      bto_stream_t stream);
+int bto_bicgk_async(const double *A, const double *p, const double *r,
+                    double *q, double *s, long M, long N, bto_stream_t stream);
+int bto_atax_async(const double *A, const double *x, double *y,
+                   long M, long N, bto_stream_t stream);
+int bto_gesummv_async(double alpha, double beta, const double *A,
+                      const double *B, const double *x, double *y,
+                      long M, long N, bto_stream_t stream);
+int bto_gemver_async(const double *A, const double *u1, const double *v1,
+                     const double *u2, const double *v2, double alpha,
+                     double beta, const double *y, const double *z,
+                     double *B, double *x, double *w, long M, long N,
+                     bto_stream_t stream);
+int bto_vadd_async(const double *w, const double *y, const double *z,
+                   double *x, long M, bto_stream_t stream);
+int bto_waxpby_async(double alpha, const double *x, double beta,
+                     const double *y, double *w, long M, bto_stream_t stream);
+int bto_dgemv_async(double alpha, const double *A, const double *x,
+                    double beta, const double *y, double *z,
+                    long M, long N, bto_stream_t stream);
+int bto_dgemvt_async(double alpha, double beta, const double *A,
+                     const double *y, const double *z, double *x, double *w,
+                     long M, long N, bto_stream_t stream);
+int bto_batax_async(const double *x, double beta, const double *A, double *y,
+                    long M, long N, bto_stream_t stream);
+
+/* ---- 3. row-sharded pieces (multi-GPU runtime) ------
+ * A rank owning rows [M*g/G, M*(g+1)/G) calls the *_async entry points above
+ * on its shard for AXPYDOT/BiCGK/ATAX/GESUMMV and all-reduces the column-
+ * indexed result.  GEMVER and DGEMVT have a true grid-wide dependency (x needs
+ * every row), so they are split at the exchange point:
+ *   pass1: B = A + u1 v1' + u2 v2' (rows of the shard), colsum = B' y
+ *          (A == B and u1 == NULL selects DGEMVT: colsum = A' y, nothing stored)
+ *   -- all-reduce colsum over ranks --
+ *   xupdate: x = colsum*beta + z
+ *   pass2: w = alpha * B x  (rows of the shard)                              */
+int bto_gemver_pass1_async(const double *A, const double *u1, const double *v1,
+                           const double *u2, const double *v2, const double *y,
+                           double *B, double *colsum, long M, long N,
+                           bto_stream_t stream);
+int bto_gemver_xupdate_async(const double *colsum, double beta, const double *z,
+                             double *x, long N, bto_stream_t stream);
+int bto_gemver_pass2_async(const double *B, const double *x, double alpha,
+                           double *w, long M, long N, bto_stream_t stream);
+
+/* ---- 4. runtime control and introspection --------------------------------- */
+int   bto_abi_version(void);
+int   bto_set_stream(bto_stream_t stream);      /* stream for section-1 calls */
+/* Tunables of the launch heuristics (what the GPU variant search explores):
+ * "mv_rows" (8|16|32 rows per unit), "mv_vec" (1|2 double2 per thread per row),
+ * "grid_per_sm" (0 = occupancy), "vec_unroll" (1|2|4), ...  Unknown key or an
+ * unsupported value returns BTO_ERR_INVALID.  bto_get_tuning returns -1 for
+ * an unknown key.                                                           */
+int   bto_set_tuning(const char *key, long value);
+long  bto_get_tuning(const char *key);
+/* Kernels launched by this library since load (bench.py's gpu_launches).    */
+long  bto_kernel_launches(void);
+/* Minimum HBM traffic of one call in bytes (SURVEY.md section 8d formulas);
+ * negative for an unknown kernel name.  N is ignored for vector kernels.    */
+double bto_bytes_min(const char *kernel, long M, long N);
+/* Device facts the cost model needs: SM count, max resident threads per SM,
+ * L2 bytes, total global memory bytes.  Returns BTO_OK or an error.         */
+int   bto_device_info(int *sm_count, int *max_threads_per_sm,
+                      long *l2_bytes, long *global_bytes);
+/* Bytes currently held in the partial-sum workspace and the host staging
+ * arena (both cached between calls); bto_release_workspace frees them.      */
+long  bto_workspace_bytes(void);
+int   bto_release_workspace(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* BTO_B200_H */

@@ -1,0 +1,1005 @@
+// api.cu -- the C ABI of libbto_b200.so (declared in include/bto_b200.h).
+//
+// Host side of the drop-in boundary: argument checking, host/device pointer
+// staging (the part of runtime.run_kernel, runtime.py:99-150, that moves
+// buffers), the cached partial-sum workspace (replaces the per-call
+// malloc/free of cemit.py:183-202), launch planning, and the kernel sequences
+// for the ten corpus kernels.  No CPU fallback: without a device every entry
+// point fails with BTO_ERR_NO_DEVICE / BTO_ERR_CUDA.
+#include <atomic>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <mutex>
+#include <vector>
+
+#include "bto_b200.h"
+#include "mv_kernels.cuh"
+#include "vec_kernels.cuh"
+
+namespace {
+
+using namespace bto;
+
+// ---------------------------------------------------------------------------
+// error channel
+
+thread_local int g_err = BTO_OK;
+thread_local char g_errmsg[512] = "";
+std::atomic<long> g_launches{0};
+
+int fail(int code, const char *fmt, ...)
+{
+    g_err = code;
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(g_errmsg, sizeof(g_errmsg), fmt, ap);
+    va_end(ap);
+    return code;
+}
+
+#define CUDA_TRY(expr)                                                         \
+    do {                                                                       \
+        cudaError_t e_ = (expr);                                               \
+        if (e_ != cudaSuccess)                                                 \
+            return fail(BTO_ERR_CUDA, "%s failed: %s", #expr,                  \
+                        cudaGetErrorString(e_));                               \
+    } while (0)
+
+#define BTO_TRY(expr)                                                          \
+    do {                                                                       \
+        int rc_ = (expr);                                                      \
+        if (rc_ != BTO_OK) return rc_;                                         \
+    } while (0)
+
+// ---------------------------------------------------------------------------
+// per-device context
+
+struct Tuning {
+    long mv_rows = 8;        // rows per unit (8 | 16)
+    long mv_vec = 2;         // double2 per thread per row (1 | 2)
+    long grid_per_sm = 0;    // CTAs per SM for the matrix kernels, 0 = occupancy
+    long vec_unroll = 4;     // independent double2 triples in flight (1 | 2 | 4)
+    long vec_grid_per_sm = 0;
+};
+
+struct DeviceCtx {
+    bool ready = false;
+    int device = -1;
+    int sm_count = 0;
+    int max_threads_per_sm = 0;
+    long l2_bytes = 0;
+    long global_bytes = 0;
+    char *ws = nullptr;            // partial sums
+    size_t ws_bytes = 0;
+    unsigned int *tickets = nullptr;
+    char *arena = nullptr;         // device staging for host arguments
+    size_t arena_bytes = 0;
+    cudaStream_t stream = nullptr; // stream of the section-1 entry points
+    std::map<const void *, int> occupancy;
+};
+
+std::mutex g_mu;
+DeviceCtx g_ctx[64];
+Tuning g_tuning;
+
+int get_ctx(DeviceCtx **out)
+{
+    int ndev = 0;
+    cudaError_t e = cudaGetDeviceCount(&ndev);
+    if (e != cudaSuccess || ndev == 0) {
+        return fail(BTO_ERR_NO_DEVICE, "no CUDA device: %s",
+                    e == cudaSuccess ? "device count is 0" : cudaGetErrorString(e));
+    }
+    int dev = 0;
+    CUDA_TRY(cudaGetDevice(&dev));
+    if (dev < 0 || dev >= 64) return fail(BTO_ERR_INVALID, "device index %d", dev);
+    DeviceCtx &c = g_ctx[dev];
+    if (!c.ready) {
+        cudaDeviceProp prop;
+        CUDA_TRY(cudaGetDeviceProperties(&prop, dev));
+        if (prop.major < 10) {
+            return fail(BTO_ERR_NO_DEVICE,
+                        "device %d is sm_%d%d; this library is built for sm_100a only",
+                        dev, prop.major, prop.minor);
+        }
+        c.device = dev;
+        c.sm_count = prop.multiProcessorCount;
+        c.max_threads_per_sm = prop.maxThreadsPerMultiProcessor;
+        c.l2_bytes = prop.l2CacheSize;
+        c.global_bytes = (long)prop.totalGlobalMem;
+        CUDA_TRY(cudaMalloc(&c.tickets, 64 * sizeof(unsigned int)));
+        CUDA_TRY(cudaMemset(c.tickets, 0, 64 * sizeof(unsigned int)));
+        c.ready = true;
+    }
+    *out = &c;
+    return BTO_OK;
+}
+
+int grow(char **buf, size_t *have, size_t want, const char *what)
+{
+    if (want <= *have) return BTO_OK;
+    // nothing of ours may still be running on the old buffer
+    CUDA_TRY(cudaDeviceSynchronize());
+    if (*buf) CUDA_TRY(cudaFree(*buf));
+    *buf = nullptr;
+    *have = 0;
+    size_t bytes = want + want / 8 + (1u << 20);
+    cudaError_t e = cudaMalloc(buf, bytes);
+    if (e != cudaSuccess) {
+        bytes = want;
+        e = cudaMalloc(buf, bytes);
+    }
+    if (e != cudaSuccess) {
+        return fail(BTO_ERR_ALLOC, "cannot allocate %zu bytes of %s: %s", want, what,
+                    cudaGetErrorString(e));
+    }
+    *have = bytes;
+    return BTO_OK;
+}
+
+// bump allocator over the workspace; sizes first, pointers after ensure()
+struct WsLayout {
+    size_t total = 0;
+    size_t take(size_t doubles)
+    {
+        const size_t off = total;
+        total += ((doubles * sizeof(double) + 255) / 256) * 256;
+        return off;
+    }
+};
+
+template <typename K>
+int occupancy_of(DeviceCtx &c, K kernel, int *occ)
+{
+    const void *key = reinterpret_cast<const void *>(kernel);
+    auto it = c.occupancy.find(key);
+    if (it == c.occupancy.end()) {
+        int n = 0;
+        CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, kernel, kThreads, 0));
+        if (n < 1) n = 1;
+        it = c.occupancy.emplace(key, n).first;
+    }
+    *occ = it->second;
+    return BTO_OK;
+}
+
+int check_launch(const char *what)
+{
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) {
+        return fail(BTO_ERR_CUDA, "launch of %s failed: %s", what, cudaGetErrorString(e));
+    }
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    return BTO_OK;
+}
+
+bool aligned16(const void *p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+// ---------------------------------------------------------------------------
+// vector kernels
+
+using VecKernel = void (*)(const VecArgs);
+
+template <int OP>
+VecKernel vec_kernel_ptr(int unroll, bool aligned)
+{
+    if (!aligned) return vec_kernel<OP, 1, false>;
+    switch (unroll) {
+        case 1: return vec_kernel<OP, 1, true>;
+        case 2: return vec_kernel<OP, 2, true>;
+        default: return vec_kernel<OP, 4, true>;
+    }
+}
+
+template <int OP>
+int launch_vec(DeviceCtx &c, VecArgs g, cudaStream_t stream)
+{
+    if (g.n < 1) return fail(BTO_ERR_INVALID, "extent M=%ld must be >= 1", g.n);
+    const bool aligned = aligned16(g.a) && aligned16(g.b) && aligned16(g.out) &&
+                         (OP == kWaxpby || aligned16(g.c));
+    VecKernel fn = vec_kernel_ptr<OP>((int)g_tuning.vec_unroll, aligned);
+    int occ = 1;
+    BTO_TRY(occupancy_of(c, fn, &occ));
+    const long per_sm = g_tuning.vec_grid_per_sm > 0 ? g_tuning.vec_grid_per_sm : occ;
+    long grid = (long)c.sm_count * per_sm;
+    const long work = ((aligned ? (g.n + 1) / 2 : g.n) + kThreads - 1) / kThreads;
+    if (grid > work) grid = work;
+    if (grid < 1) grid = 1;
+    if (OP == kAxpydot) {
+        WsLayout lay;
+        const size_t off = lay.take((size_t)grid);
+        BTO_TRY(grow(&c.ws, &c.ws_bytes, lay.total, "workspace"));
+        g.partials = reinterpret_cast<double *>(c.ws + off);
+        g.ticket = c.tickets;
+    }
+    fn<<<(unsigned)grid, kThreads, 0, stream>>>(g);
+    return check_launch("vec_kernel");
+}
+
+// ---------------------------------------------------------------------------
+// matrix kernels
+
+using MvKernel = void (*)(const MvArgs);
+
+struct MvPlan {
+    int R = 8, V = 1;
+    bool aligned = true;
+    long strip_width = 512;
+    int nstrips = 1;
+    long units_per_strip = 1, total_units = 1;
+    long grid = 1;
+    long slots = 1;        // max CTAs sharing one strip
+    MvKernel fn = nullptr;
+};
+
+template <int FLAGS>
+MvKernel mv_kernel_ptr(int R, int V, bool aligned)
+{
+    if (!aligned) return mv_tile_kernel<FLAGS, 8, 1, false>;
+    if constexpr ((FLAGS & kFlagN2) == 0) {   // two matrices: keep the tile small
+        if (R == 16 && V == 1) return mv_tile_kernel<FLAGS, 16, 1, true>;
+        if (R == 8 && V == 2) return mv_tile_kernel<FLAGS, 8, 2, true>;
+    }
+    return mv_tile_kernel<FLAGS, 8, 1, true>;
+}
+
+template <int FLAGS>
+int plan_mv(DeviceCtx &c, long M, long N, bool aligned, MvPlan *p)
+{
+    int R = (int)g_tuning.mv_rows, V = (int)g_tuning.mv_vec;
+    if (!aligned || (FLAGS & kFlagN2)) { R = 8; V = 1; }
+    if (!((R == 8 && V == 1) || (R == 16 && V == 1) || (R == 8 && V == 2))) { R = 8; V = 1; }
+    p->R = R;
+    p->V = V;
+    p->aligned = aligned;
+    p->fn = mv_kernel_ptr<FLAGS>(R, V, aligned);
+    p->strip_width = (long)kThreads * 2 * V;
+    p->nstrips = (int)((N + p->strip_width - 1) / p->strip_width);
+    p->units_per_strip = (M + R - 1) / R;
+    p->total_units = p->units_per_strip * p->nstrips;
+    int occ = 1;
+    BTO_TRY(occupancy_of(c, p->fn, &occ));
+    const long per_sm = g_tuning.grid_per_sm > 0 ? g_tuning.grid_per_sm : occ;
+    long grid = (long)c.sm_count * per_sm;
+    if (grid > p->total_units) grid = p->total_units;
+    if (grid < 1) grid = 1;
+    p->grid = grid;
+    long slots = 1;
+    for (int s = 0; s < p->nstrips; ++s) {
+        const long first = split_owner(p->total_units, grid, (long)s * p->units_per_strip);
+        const long last = split_owner(p->total_units, grid,
+                                      (long)(s + 1) * p->units_per_strip - 1);
+        if (last - first + 1 > slots) slots = last - first + 1;
+    }
+    p->slots = slots;
+    return BTO_OK;
+}
+
+void fill_geometry(const MvPlan &p, MvArgs *a, long M, long N)
+{
+    a->M = M;
+    a->N = N;
+    a->units_per_strip = p.units_per_strip;
+    a->total_units = p.total_units;
+    a->nstrips = p.nstrips;
+}
+
+int launch_mv(const MvPlan &p, const MvArgs &a, cudaStream_t stream)
+{
+    p.fn<<<(unsigned)p.grid, kThreads, 0, stream>>>(a);
+    return check_launch("mv_tile_kernel");
+}
+
+int launch_finalize(const MvPlan &p, FinArgs f, long M, long N, cudaStream_t stream)
+{
+    f.M = M;
+    f.N = N;
+    f.units_per_strip = p.units_per_strip;
+    f.total_units = p.total_units;
+    f.grid = p.grid;
+    f.strip_width = p.strip_width;
+    f.nstrips = p.nstrips;
+    const long cb = f.cmode != kColNone ? (N + kThreads - 1) / kThreads : 0;
+    const long rb = f.rmode != kRowNone ? (M + kThreads - 1) / kThreads : 0;
+    f.col_blocks = (int)cb;
+    finalize_kernel<<<(unsigned)(cb + rb), kThreads, 0, stream>>>(f);
+    return check_launch("finalize_kernel");
+}
+
+int check_mn(long M, long N)
+{
+    if (M < 1 || N < 1) {
+        return fail(BTO_ERR_INVALID, "extents M=%ld N=%ld must be >= 1", M, N);
+    }
+    return BTO_OK;
+}
+
+bool mat_aligned(long N, const void *a, const void *b = nullptr, const void *c = nullptr)
+{
+    return (N % 2 == 0) && aligned16(a) && aligned16(b) && aligned16(c);
+}
+
+// One streaming pass producing row dots and/or column sums, then the join.
+// prepare() plans the launch and books its partial buffers in the sequence's
+// workspace layout; run() launches after the workspace has been sized once,
+// so no pointer handed out earlier in the sequence can move.
+template <int FLAGS>
+struct Pass {
+    MvPlan plan;
+    size_t off_row = 0, off_row2 = 0, off_col = 0;
+    long M = 0, N = 0;
+
+    int prepare(DeviceCtx &c, long m, long n, bool aligned, WsLayout *lay)
+    {
+        M = m;
+        N = n;
+        BTO_TRY(plan_mv<FLAGS>(c, M, N, aligned, &plan));
+        if (FLAGS & kFlagN) off_row = lay->take((size_t)plan.nstrips * M);
+        if (FLAGS & kFlagN2) off_row2 = lay->take((size_t)plan.nstrips * M);
+        if (FLAGS & kFlagT) off_col = lay->take((size_t)plan.slots * N);
+        return BTO_OK;
+    }
+
+    // Row results go to f.rowout through f.rmode, column results to f.colout
+    // through f.cmode.
+    int run(DeviceCtx &c, MvArgs a, FinArgs f, cudaStream_t stream) const
+    {
+        fill_geometry(plan, &a, M, N);
+        a.rowpart = reinterpret_cast<double *>(c.ws + off_row);
+        a.rowpart2 = reinterpret_cast<double *>(c.ws + off_row2);
+        a.colpart = reinterpret_cast<double *>(c.ws + off_col);
+        BTO_TRY(launch_mv(plan, a, stream));
+        f.rowpart = a.rowpart;
+        f.rowpart2 = a.rowpart2;
+        f.colpart = a.colpart;
+        if (!(FLAGS & kFlagN)) f.rmode = kRowNone;
+        if (!(FLAGS & kFlagT)) f.cmode = kColNone;
+        return launch_finalize(plan, f, M, N, stream);
+    }
+};
+
+int size_ws(DeviceCtx &c, const WsLayout &lay)
+{
+    return grow(&c.ws, &c.ws_bytes, lay.total, "workspace");
+}
+
+// ---------------------------------------------------------------------------
+// kernel sequences (device pointers, asynchronous)
+
+int seq_axpydot(DeviceCtx &c, const double *w, const double *v, const double *u,
+                double alpha, double *z, double *beta, long M, cudaStream_t st)
+{
+    VecArgs g{};
+    g.a = w; g.b = v; g.c = u; g.alpha = alpha; g.out = z; g.dot = beta; g.n = M;
+    return launch_vec<kAxpydot>(c, g, st);
+}
+
+int seq_vadd(DeviceCtx &c, const double *w, const double *y, const double *z,
+             double *x, long M, cudaStream_t st)
+{
+    VecArgs g{};
+    g.a = w; g.b = y; g.c = z; g.out = x; g.n = M;
+    return launch_vec<kVadd>(c, g, st);
+}
+
+int seq_waxpby(DeviceCtx &c, double alpha, const double *x, double beta,
+               const double *y, double *w, long M, cudaStream_t st)
+{
+    VecArgs g{};
+    g.a = x; g.b = y; g.alpha = alpha; g.beta = beta; g.out = w; g.n = M;
+    return launch_vec<kWaxpby>(c, g, st);
+}
+
+int seq_bicgk(DeviceCtx &c, const double *A, const double *p, const double *r,
+              double *q, double *s, long M, long N, cudaStream_t st)
+{
+    BTO_TRY(check_mn(M, N));
+    WsLayout lay;
+    Pass<kFlagN | kFlagT> pass;
+    BTO_TRY(pass.prepare(c, M, N, mat_aligned(N, A), &lay));
+    BTO_TRY(size_ws(c, lay));
+    MvArgs a{};
+    a.A = A; a.colw = p; a.roww = r;
+    FinArgs f{};
+    f.cmode = kColPlain; f.colout = s;
+    f.rmode = kRowPlain; f.rowout = q;
+    return pass.run(c, a, f, st);
+}
+
+// y = [beta *] A'(A x): pass 1 contracts t = A x into a workspace vector (it
+// never reaches the caller), pass 2 streams A again for A' t.
+int seq_atax(DeviceCtx &c, const double *A, const double *x, double *y, long M,
+             long N, bool scaled, double beta, cudaStream_t st)
+{
+    BTO_TRY(check_mn(M, N));
+    const bool al = mat_aligned(N, A);
+    WsLayout lay;
+    const size_t off_t = lay.take((size_t)M);
+    Pass<kFlagN> dots;
+    Pass<kFlagT> sums;
+    BTO_TRY(dots.prepare(c, M, N, al, &lay));
+    BTO_TRY(sums.prepare(c, M, N, al, &lay));
+    BTO_TRY(size_ws(c, lay));
+    double *t = reinterpret_cast<double *>(c.ws + off_t);
+    {
+        MvArgs a{};
+        a.A = A; a.colw = x;
+        FinArgs f{};
+        f.rmode = kRowPlain; f.rowout = t;
+        BTO_TRY(dots.run(c, a, f, st));
+    }
+    MvArgs a{};
+    a.A = A; a.roww = t;
+    FinArgs f{};
+    f.cmode = scaled ? kColScale : kColPlain; f.cscale = beta; f.colout = y;
+    return sums.run(c, a, f, st);
+}
+
+int seq_gesummv(DeviceCtx &c, double alpha, double beta, const double *A,
+                const double *B, const double *x, double *y, long M, long N,
+                cudaStream_t st)
+{
+    BTO_TRY(check_mn(M, N));
+    WsLayout lay;
+    Pass<kFlagN | kFlagN2> pass;
+    BTO_TRY(pass.prepare(c, M, N, mat_aligned(N, A, B), &lay));
+    BTO_TRY(size_ws(c, lay));
+    MvArgs a{};
+    a.A = A; a.A2 = B; a.colw = x;
+    FinArgs f{};
+    f.rmode = kRowGesummv; f.ralpha = alpha; f.rbeta = beta; f.rowout = y;
+    return pass.run(c, a, f, st);
+}
+
+int seq_dgemv(DeviceCtx &c, double alpha, const double *A, const double *x,
+              double beta, const double *y, double *z, long M, long N,
+              cudaStream_t st)
+{
+    BTO_TRY(check_mn(M, N));
+    WsLayout lay;
+    Pass<kFlagN> pass;
+    BTO_TRY(pass.prepare(c, M, N, mat_aligned(N, A), &lay));
+    BTO_TRY(size_ws(c, lay));
+    MvArgs a{};
+    a.A = A; a.colw = x;
+    FinArgs f{};
+    f.rmode = kRowDgemv; f.ralpha = alpha; f.rbeta = beta; f.rowy = y; f.rowout = z;
+    return pass.run(c, a, f, st);
+}
+
+// GEMVER / DGEMVT pass 1: colsum = B' y with B = A + u1 v1' + u2 v2' stored
+// (u1 == nullptr: DGEMVT, colsum = A' y, nothing stored).  f.cmode decides
+// what lands in f.colout (the sum itself, or x = sum*beta + z).
+int seq_pass1(DeviceCtx &c, const double *A, const double *u1, const double *v1,
+              const double *u2, const double *v2, const double *y, double *B,
+              FinArgs f, long M, long N, cudaStream_t st)
+{
+    WsLayout lay;
+    MvArgs a{};
+    a.A = A; a.roww = y;
+    if (u1 == nullptr) {
+        Pass<kFlagT> pass;
+        BTO_TRY(pass.prepare(c, M, N, mat_aligned(N, A), &lay));
+        BTO_TRY(size_ws(c, lay));
+        return pass.run(c, a, f, st);
+    }
+    a.u1 = u1; a.v1 = v1; a.u2 = u2; a.v2 = v2; a.Bout = B;
+    Pass<kFlagT | kFlagRank2> pass;
+    BTO_TRY(pass.prepare(c, M, N, mat_aligned(N, A, B), &lay));
+    BTO_TRY(size_ws(c, lay));
+    return pass.run(c, a, f, st);
+}
+
+int seq_pass2(DeviceCtx &c, const double *B, const double *x, double alpha,
+              double *w, long M, long N, cudaStream_t st)
+{
+    WsLayout lay;
+    Pass<kFlagN> pass;
+    BTO_TRY(pass.prepare(c, M, N, mat_aligned(N, B), &lay));
+    BTO_TRY(size_ws(c, lay));
+    MvArgs a{};
+    a.A = B; a.colw = x;
+    FinArgs f{};
+    f.rmode = kRowScale; f.ralpha = alpha; f.rowout = w;
+    return pass.run(c, a, f, st);
+}
+
+// The two passes run back to back on one stream and no workspace pointer
+// outlives its pass (x and colsum are caller buffers), so each pass may size
+// the workspace for itself.
+int seq_gemver(DeviceCtx &c, const double *A, const double *u1, const double *v1,
+               const double *u2, const double *v2, double alpha, double beta,
+               const double *y, const double *z, double *B, double *x, double *w,
+               long M, long N, cudaStream_t st)
+{
+    BTO_TRY(check_mn(M, N));
+    if (u1 == nullptr || v1 == nullptr || u2 == nullptr || v2 == nullptr) {
+        return fail(BTO_ERR_INVALID, "gemver: null rank-2 vector");
+    }
+    FinArgs f{};
+    f.cmode = kColAxpz; f.cscale = beta; f.colz = z; f.colout = x;
+    BTO_TRY(seq_pass1(c, A, u1, v1, u2, v2, y, B, f, M, N, st));
+    return seq_pass2(c, B, x, alpha, w, M, N, st);
+}
+
+int seq_dgemvt(DeviceCtx &c, double alpha, double beta, const double *A,
+               const double *y, const double *z, double *x, double *w, long M,
+               long N, cudaStream_t st)
+{
+    BTO_TRY(check_mn(M, N));
+    FinArgs f{};
+    f.cmode = kColAxpz; f.cscale = beta; f.colz = z; f.colout = x;
+    BTO_TRY(seq_pass1(c, A, nullptr, nullptr, nullptr, nullptr, y, nullptr, f, M, N, st));
+    return seq_pass2(c, A, x, alpha, w, M, N, st);
+}
+
+// ---------------------------------------------------------------------------
+// host/device argument staging for the section-1 entry points
+
+class Call {
+public:
+    Call() : lock_(g_mu)
+    {
+        g_err = BTO_OK;
+        g_errmsg[0] = 0;
+        rc_ = get_ctx(&ctx_);
+    }
+    bool ok() const { return rc_ == BTO_OK; }
+    DeviceCtx &ctx() { return *ctx_; }
+    cudaStream_t stream() const { return ctx_->stream; }
+    void status(int rc) { if (rc_ == BTO_OK) rc_ = rc; }
+
+    void in(const double **slot, long count) { add(const_cast<double **>(slot), count, false); }
+    void out(double **slot, long count) { add(slot, count, true); }
+
+    // classify, allocate staging, copy inputs host -> device
+    void prepare()
+    {
+        if (!ok()) return;
+        size_t need = 0;
+        for (Arg &a : args_) {
+            if (*a.slot == nullptr || a.count < 1) {
+                status(fail(BTO_ERR_INVALID, "null pointer or empty array argument"));
+                return;
+            }
+            cudaPointerAttributes attr;
+            cudaError_t e = cudaPointerGetAttributes(&attr, *a.slot);
+            if (e != cudaSuccess) {
+                cudaGetLastError();
+                attr.type = cudaMemoryTypeUnregistered;
+            }
+            a.on_host = !(attr.type == cudaMemoryTypeDevice ||
+                          attr.type == cudaMemoryTypeManaged);
+            if (a.on_host) {
+                a.offset = need;
+                need += ((size_t)a.count * sizeof(double) + 255) / 256 * 256;
+                any_host_ = true;
+            }
+        }
+        if (!any_host_) return;
+        status(grow(&ctx_->arena, &ctx_->arena_bytes, need, "staging arena"));
+        if (!ok()) return;
+        for (Arg &a : args_) {
+            if (!a.on_host) continue;
+            a.host = *a.slot;
+            *a.slot = reinterpret_cast<double *>(ctx_->arena + a.offset);
+            if (!a.is_out) {
+                cudaError_t e = cudaMemcpyAsync(*a.slot, a.host, (size_t)a.count * sizeof(double),
+                                                cudaMemcpyHostToDevice, stream());
+                if (e != cudaSuccess) {
+                    status(fail(BTO_ERR_CUDA, "host->device copy failed: %s",
+                                cudaGetErrorString(e)));
+                    return;
+                }
+            }
+        }
+    }
+
+    // copy outputs device -> host and wait (only when something was staged)
+    void finish()
+    {
+        if (!any_host_) return;
+        if (ok()) {
+            for (Arg &a : args_) {
+                if (!a.on_host || !a.is_out) continue;
+                cudaError_t e = cudaMemcpyAsync(a.host, *a.slot, (size_t)a.count * sizeof(double),
+                                                cudaMemcpyDeviceToHost, stream());
+                if (e != cudaSuccess) {
+                    status(fail(BTO_ERR_CUDA, "device->host copy failed: %s",
+                                cudaGetErrorString(e)));
+                    break;
+                }
+            }
+        }
+        cudaError_t e = cudaStreamSynchronize(stream());
+        if (e != cudaSuccess && ok()) {
+            status(fail(BTO_ERR_CUDA, "kernel sequence failed: %s", cudaGetErrorString(e)));
+        }
+    }
+
+private:
+    struct Arg {
+        double **slot;
+        long count;
+        bool is_out;
+        bool on_host = false;
+        size_t offset = 0;
+        double *host = nullptr;
+    };
+    void add(double **slot, long count, bool is_out)
+    {
+        Arg a;
+        a.slot = slot;
+        a.count = count;
+        a.is_out = is_out;
+        args_.push_back(a);
+    }
+    std::lock_guard<std::mutex> lock_;
+    DeviceCtx *ctx_ = nullptr;
+    int rc_ = BTO_OK;
+    bool any_host_ = false;
+    std::vector<Arg> args_;
+};
+
+// async entry points share this prologue
+struct AsyncCall {
+    AsyncCall() : lock(g_mu)
+    {
+        g_err = BTO_OK;
+        g_errmsg[0] = 0;
+        rc = get_ctx(&ctx);
+    }
+    std::lock_guard<std::mutex> lock;
+    DeviceCtx *ctx = nullptr;
+    int rc = BTO_OK;
+};
+
+bool extents_ok(Call &c, long M, long N)
+{
+    if (!c.ok()) return false;
+    if (M < 1 || N < 1) {
+        c.status(fail(BTO_ERR_INVALID, "extents M=%ld N=%ld must be >= 1", M, N));
+        return false;
+    }
+    return true;
+}
+
+}  // namespace
+
+// ===========================================================================
+// exported symbols
+
+extern "C" {
+
+int bto_last_error(void) { return g_err; }
+const char *bto_last_error_string(void) { return g_errmsg; }
+void bto_clear_error(void) { g_err = BTO_OK; g_errmsg[0] = 0; }
+int bto_abi_version(void) { return BTO_B200_ABI_VERSION; }
+long bto_kernel_launches(void) { return g_launches.load(); }
+
+// ---- section 1: the reference's signatures ---------------------------------
+
+void axpydot(const double *w, const double *v, const double *u, double alpha,
+             double *z, double *beta, long M)
+{
+    Call c;
+    if (!extents_ok(c, M, 1)) return;
+    c.in(&w, M); c.in(&v, M); c.in(&u, M); c.out(&z, M); c.out(&beta, 1);
+    c.prepare();
+    if (c.ok()) c.status(seq_axpydot(c.ctx(), w, v, u, alpha, z, beta, M, c.stream()));
+    c.finish();
+}
+
+void vadd(const double *w, const double *y, const double *z, double *x, long M)
+{
+    Call c;
+    if (!extents_ok(c, M, 1)) return;
+    c.in(&w, M); c.in(&y, M); c.in(&z, M); c.out(&x, M);
+    c.prepare();
+    if (c.ok()) c.status(seq_vadd(c.ctx(), w, y, z, x, M, c.stream()));
+    c.finish();
+}
+
+void waxpby(double alpha, const double *x, double beta, const double *y,
+            double *w, long M)
+{
+    Call c;
+    if (!extents_ok(c, M, 1)) return;
+    c.in(&x, M); c.in(&y, M); c.out(&w, M);
+    c.prepare();
+    if (c.ok()) c.status(seq_waxpby(c.ctx(), alpha, x, beta, y, w, M, c.stream()));
+    c.finish();
+}
+
+void bicgk(const double *A, const double *p, const double *r, double *q,
+           double *s, long M, long N)
+{
+    Call c;
+    if (!extents_ok(c, M, N)) return;
+    c.in(&A, M * N); c.in(&p, N); c.in(&r, M); c.out(&q, M); c.out(&s, N);
+    c.prepare();
+    if (c.ok()) c.status(seq_bicgk(c.ctx(), A, p, r, q, s, M, N, c.stream()));
+    c.finish();
+}
+
+void atax(const double *A, const double *x, double *y, long M, long N)
+{
+    Call c;
+    if (!extents_ok(c, M, N)) return;
+    c.in(&A, M * N); c.in(&x, N); c.out(&y, N);
+    c.prepare();
+    if (c.ok()) c.status(seq_atax(c.ctx(), A, x, y, M, N, false, 1.0, c.stream()));
+    c.finish();
+}
+
+void batax(const double *x, double beta, const double *A, double *y, long M, long N)
+{
+    Call c;
+    if (!extents_ok(c, M, N)) return;
+    c.in(&x, N); c.in(&A, M * N); c.out(&y, N);
+    c.prepare();
+    if (c.ok()) c.status(seq_atax(c.ctx(), A, x, y, M, N, true, beta, c.stream()));
+    c.finish();
+}
+
+void gesummv(double alpha, double beta, const double *A, const double *B,
+             const double *x, double *y, long M, long N)
+{
+    Call c;
+    if (!extents_ok(c, M, N)) return;
+    c.in(&A, M * N); c.in(&B, M * N); c.in(&x, N); c.out(&y, M);
+    c.prepare();
+    if (c.ok()) c.status(seq_gesummv(c.ctx(), alpha, beta, A, B, x, y, M, N, c.stream()));
+    c.finish();
+}
+
+void dgemv(double alpha, const double *A, const double *x, double beta,
+           const double *y, double *z, long M, long N)
+{
+    Call c;
+    if (!extents_ok(c, M, N)) return;
+    c.in(&A, M * N); c.in(&x, N); c.in(&y, M); c.out(&z, M);
+    c.prepare();
+    if (c.ok()) c.status(seq_dgemv(c.ctx(), alpha, A, x, beta, y, z, M, N, c.stream()));
+    c.finish();
+}
+
+void gemver(const double *A, const double *u1, const double *v1, const double *u2,
+            const double *v2, double alpha, double beta, const double *y,
+            const double *z, double *B, double *x, double *w, long M, long N)
+{
+    Call c;
+    if (!extents_ok(c, M, N)) return;
+    c.in(&A, M * N); c.in(&u1, M); c.in(&v1, N); c.in(&u2, M); c.in(&v2, N);
+    c.in(&y, M); c.in(&z, N); c.out(&B, M * N); c.out(&x, N); c.out(&w, M);
+    c.prepare();
+    if (c.ok()) {
+        c.status(seq_gemver(c.ctx(), A, u1, v1, u2, v2, alpha, beta, y, z, B, x, w,
+                            M, N, c.stream()));
+    }
+    c.finish();
+}
+
+void dgemvt(double alpha, double beta, const double *A, const double *y,
+            const double *z, double *x, double *w, long M, long N)
+{
+    Call c;
+    if (!extents_ok(c, M, N)) return;
+    c.in(&A, M * N); c.in(&y, M); c.in(&z, N); c.out(&x, N); c.out(&w, M);
+    c.prepare();
+    if (c.ok()) c.status(seq_dgemvt(c.ctx(), alpha, beta, A, y, z, x, w, M, N, c.stream()));
+    c.finish();
+}
+
+// ---- section 2: asynchronous, device pointers --------------------------------
+
+#define ASYNC_PROLOGUE()                                                        \
+    AsyncCall ac;                                                               \
+    if (ac.rc != BTO_OK) return ac.rc;                                          \
+    cudaStream_t st = static_cast<cudaStream_t>(stream)
+
+int bto_axpydot_async(const double *w, const double *v, const double *u,
+                      double alpha, double *z, double *beta, long M,
+                      bto_stream_t stream)
+{
+    ASYNC_PROLOGUE();
+    return seq_axpydot(*ac.ctx, w, v, u, alpha, z, beta, M, st);
+}
+
+int bto_vadd_async(const double *w, const double *y, const double *z, double *x,
+                   long M, bto_stream_t stream)
+{
+    ASYNC_PROLOGUE();
+    return seq_vadd(*ac.ctx, w, y, z, x, M, st);
+}
+
+int bto_waxpby_async(double alpha, const double *x, double beta, const double *y,
+                     double *w, long M, bto_stream_t stream)
+{
+    ASYNC_PROLOGUE();
+    return seq_waxpby(*ac.ctx, alpha, x, beta, y, w, M, st);
+}
+
+int bto_bicgk_async(const double *A, const double *p, const double *r, double *q,
+                    double *s, long M, long N, bto_stream_t stream)
+{
+    ASYNC_PROLOGUE();
+    return seq_bicgk(*ac.ctx, A, p, r, q, s, M, N, st);
+}
+
+int bto_atax_async(const double *A, const double *x, double *y, long M, long N,
+                   bto_stream_t stream)
+{
+    ASYNC_PROLOGUE();
+    return seq_atax(*ac.ctx, A, x, y, M, N, false, 1.0, st);
+}
+
+int bto_batax_async(const double *x, double beta, const double *A, double *y,
+                    long M, long N, bto_stream_t stream)
+{
+    ASYNC_PROLOGUE();
+    return seq_atax(*ac.ctx, A, x, y, M, N, true, beta, st);
+}
+
+int bto_gesummv_async(double alpha, double beta, const double *A, const double *B,
+                      const double *x, double *y, long M, long N,
+                      bto_stream_t stream)
+{
+    ASYNC_PROLOGUE();
+    return seq_gesummv(*ac.ctx, alpha, beta, A, B, x, y, M, N, st);
+}
+
+int bto_dgemv_async(double alpha, const double *A, const double *x, double beta,
+                    const double *y, double *z, long M, long N, bto_stream_t stream)
+{
+    ASYNC_PROLOGUE();
+    return seq_dgemv(*ac.ctx, alpha, A, x, beta, y, z, M, N, st);
+}
+
+int bto_gemver_async(const double *A, const double *u1, const double *v1,
+                     const double *u2, const double *v2, double alpha, double beta,
+                     const double *y, const double *z, double *B, double *x,
+                     double *w, long M, long N, bto_stream_t stream)
+{
+    ASYNC_PROLOGUE();
+    return seq_gemver(*ac.ctx, A, u1, v1, u2, v2, alpha, beta, y, z, B, x, w, M, N, st);
+}
+
+int bto_dgemvt_async(double alpha, double beta, const double *A, const double *y,
+                     const double *z, double *x, double *w, long M, long N,
+                     bto_stream_t stream)
+{
+    ASYNC_PROLOGUE();
+    return seq_dgemvt(*ac.ctx, alpha, beta, A, y, z, x, w, M, N, st);
+}
+
+// ---- section 3: row-sharded pieces ---------------------------------------------
+
+int bto_gemver_pass1_async(const double *A, const double *u1, const double *v1,
+                           const double *u2, const double *v2, const double *y,
+                           double *B, double *colsum, long M, long N,
+                           bto_stream_t stream)
+{
+    ASYNC_PROLOGUE();
+    BTO_TRY(check_mn(M, N));
+    FinArgs f{};
+    f.cmode = kColPlain; f.colout = colsum;
+    return seq_pass1(*ac.ctx, A, u1, v1, u2, v2, y, B, f, M, N, st);
+}
+
+int bto_gemver_xupdate_async(const double *colsum, double beta, const double *z,
+                             double *x, long N, bto_stream_t stream)
+{
+    ASYNC_PROLOGUE();
+    if (N < 1) return fail(BTO_ERR_INVALID, "extent N=%ld must be >= 1", N);
+    axpz_kernel<<<(unsigned)((N + kThreads - 1) / kThreads), kThreads, 0, st>>>(
+        colsum, beta, z, x, N);
+    return check_launch("axpz_kernel");
+}
+
+int bto_gemver_pass2_async(const double *B, const double *x, double alpha,
+                           double *w, long M, long N, bto_stream_t stream)
+{
+    ASYNC_PROLOGUE();
+    BTO_TRY(check_mn(M, N));
+    return seq_pass2(*ac.ctx, B, x, alpha, w, M, N, st);
+}
+
+// ---- section 4: control ----------------------------------------------------------
+
+int bto_set_stream(bto_stream_t stream)
+{
+    AsyncCall ac;
+    if (ac.rc != BTO_OK) return ac.rc;
+    ac.ctx->stream = static_cast<cudaStream_t>(stream);
+    return BTO_OK;
+}
+
+static long *tuning_slot(const char *key)
+{
+    if (!key) return nullptr;
+    if (!strcmp(key, "mv_rows")) return &g_tuning.mv_rows;
+    if (!strcmp(key, "mv_vec")) return &g_tuning.mv_vec;
+    if (!strcmp(key, "grid_per_sm")) return &g_tuning.grid_per_sm;
+    if (!strcmp(key, "vec_unroll")) return &g_tuning.vec_unroll;
+    if (!strcmp(key, "vec_grid_per_sm")) return &g_tuning.vec_grid_per_sm;
+    return nullptr;
+}
+
+int bto_set_tuning(const char *key, long value)
+{
+    std::lock_guard<std::mutex> lock(g_mu);
+    long *slot = tuning_slot(key);
+    if (!slot) return fail(BTO_ERR_INVALID, "unknown tuning key %s", key ? key : "(null)");
+    bool ok = value >= 0;
+    if (slot == &g_tuning.mv_rows) ok = value == 8 || value == 16;
+    if (slot == &g_tuning.mv_vec) ok = value == 1 || value == 2;
+    if (slot == &g_tuning.vec_unroll) ok = value == 1 || value == 2 || value == 4;
+    if (slot == &g_tuning.grid_per_sm || slot == &g_tuning.vec_grid_per_sm) ok = value >= 0 && value <= 64;
+    if (!ok) return fail(BTO_ERR_INVALID, "tuning %s=%ld is not supported", key, value);
+    *slot = value;
+    return BTO_OK;
+}
+
+long bto_get_tuning(const char *key)
+{
+    std::lock_guard<std::mutex> lock(g_mu);
+    long *slot = tuning_slot(key);
+    return slot ? *slot : -1;
+}
+
+double bto_bytes_min(const char *kernel, long M, long N)
+{
+    if (!kernel) return -1.0;
+    const double m = (double)M, n = (double)N;
+    if (!strcmp(kernel, "axpydot")) return 32.0 * m;
+    if (!strcmp(kernel, "vadd")) return 32.0 * m;
+    if (!strcmp(kernel, "waxpby")) return 24.0 * m;
+    if (!strcmp(kernel, "bicgk")) return 8.0 * m * n + 16.0 * m + 16.0 * n;
+    if (!strcmp(kernel, "atax")) return 8.0 * m * n + 16.0 * n;
+    if (!strcmp(kernel, "batax")) return 8.0 * m * n + 16.0 * n;
+    if (!strcmp(kernel, "gesummv")) return 16.0 * m * n + 8.0 * n + 8.0 * m;
+    if (!strcmp(kernel, "dgemv")) return 8.0 * m * n + 8.0 * n + 16.0 * m;
+    // read A, write B, re-read B; u1,u2,y (M) v1,v2,z (N) in; x out + re-read; w out
+    if (!strcmp(kernel, "gemver")) return 24.0 * m * n + 32.0 * m + 40.0 * n;
+    // A twice; y (M), z (N) in; x out + re-read (N); w out (M)
+    if (!strcmp(kernel, "dgemvt")) return 16.0 * m * n + 16.0 * m + 24.0 * n;
+    return -1.0;
+}
+
+int bto_device_info(int *sm_count, int *max_threads_per_sm, long *l2_bytes,
+                    long *global_bytes)
+{
+    AsyncCall ac;
+    if (ac.rc != BTO_OK) return ac.rc;
+    if (sm_count) *sm_count = ac.ctx->sm_count;
+    if (max_threads_per_sm) *max_threads_per_sm = ac.ctx->max_threads_per_sm;
+    if (l2_bytes) *l2_bytes = ac.ctx->l2_bytes;
+    if (global_bytes) *global_bytes = ac.ctx->global_bytes;
+    return BTO_OK;
+}
+
+long bto_workspace_bytes(void)
+{
+    std::lock_guard<std::mutex> lock(g_mu);
+    long total = 0;
+    for (DeviceCtx &c : g_ctx) total += (long)(c.ws_bytes + c.arena_bytes);
+    return total;
+}
+
+int bto_release_workspace(void)
+{
+    AsyncCall ac;
+    if (ac.rc != BTO_OK) return ac.rc;
+    CUDA_TRY(cudaDeviceSynchronize());
+    DeviceCtx &c = *ac.ctx;
+    if (c.ws) CUDA_TRY(cudaFree(c.ws));
+    if (c.arena) CUDA_TRY(cudaFree(c.arena));
+    c.ws = nullptr; c.ws_bytes = 0;
+    c.arena = nullptr; c.arena_bytes = 0;
+    return BTO_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,129 @@
+// common.cuh -- device helpers shared by the fused BLAS-1/BLAS-2 kernels (sm_100a).
+//
+// Everything here is HBM-bound fp64 streaming work: 128-bit coalesced loads
+// that bypass L1 (each matrix element is used once), warp-shuffle reductions
+// with a FIXED combination order (the reference guarantees bit-stable results
+// at a fixed thread count, cemit.py:8-10; we guarantee it at a fixed launch
+// geometry), and rounded-separately arithmetic where the reference's C rounds
+// separately (cemit.py:112-136 prints one binary op per statement and gcc on
+// baseline x86-64 does not contract them into FMAs).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace bto {
+
+constexpr int kThreads = 256;            // every kernel here uses 256-thread CTAs
+constexpr int kWarps = kThreads / 32;
+constexpr unsigned kFullMask = 0xffffffffu;
+
+// ---- streaming global loads / stores ---------------------------------------
+// .nc + L1::no_allocate: read-once data must not evict the small vectors
+// (weights, x) that do get re-used from L1.
+__device__ __forceinline__ double2 ld_stream2(const double *p)   // 16 B aligned
+{
+    double2 v;
+    asm("ld.global.nc.L1::no_allocate.v2.f64 {%0, %1}, [%2];"
+        : "=d"(v.x), "=d"(v.y) : "l"(p));
+    return v;
+}
+
+__device__ __forceinline__ double ld_stream1(const double *p)
+{
+    double v;
+    asm("ld.global.nc.L1::no_allocate.f64 %0, [%1];" : "=d"(v) : "l"(p));
+    return v;
+}
+
+// evict-first stores for write-once outputs (z, B)
+__device__ __forceinline__ void st_stream2(double *p, double2 v)   // 16 B aligned
+{
+    asm volatile("st.global.cs.v2.f64 [%0], {%1, %2};"
+                 :: "l"(p), "d"(v.x), "d"(v.y) : "memory");
+}
+
+__device__ __forceinline__ void st_stream1(double *p, double v)
+{
+    asm volatile("st.global.cs.f64 [%0], %1;" :: "l"(p), "d"(v) : "memory");
+}
+
+// loads that must observe data written earlier in the same grid by other CTAs
+__device__ __forceinline__ double ld_cg(const double *p)
+{
+    double v;
+    asm volatile("ld.global.cg.f64 %0, [%1];" : "=d"(v) : "l"(p) : "memory");
+    return v;
+}
+
+// ---- reductions with a fixed order ------------------------------------------
+__device__ __forceinline__ double warp_sum(double v)
+{
+#pragma unroll
+    for (int off = 16; off >= 1; off >>= 1) {
+        v += __shfl_xor_sync(kFullMask, v, off);
+    }
+    return v;
+}
+
+// Sum over the CTA; result valid in thread 0.  scratch: kWarps doubles.
+__device__ __forceinline__ double block_sum(double v, double *scratch)
+{
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    v = warp_sum(v);
+    if (lane == 0) scratch[warp] = v;
+    __syncthreads();
+    double total = 0.0;
+    if (warp == 0) {
+        double part = lane < kWarps ? scratch[lane] : 0.0;
+#pragma unroll
+        for (int off = kWarps / 2; off >= 1; off >>= 1) {
+            part += __shfl_xor_sync(kFullMask, part, off);
+        }
+        total = part;
+    }
+    __syncthreads();
+    return total;
+}
+
+// Transposing warp reduction: every lane holds R per-row partial sums v[0..R);
+// afterwards v[0] of lane l is the warp-wide sum of row (l / (32/R)).
+// 31 shuffles for R = 32 instead of 32*5: the halving butterfly sends the half
+// of the rows a lane does not keep to its partner.
+template <int R>
+__device__ __forceinline__ void warp_transpose_sum(double (&v)[R], int lane)
+{
+    static_assert(R == 8 || R == 16 || R == 32, "R must be 8, 16 or 32");
+#pragma unroll
+    for (int s = 0; s < 5; ++s) {
+        const int off = 16 >> s;
+        const int alive = R >> s;
+        if (alive > 1) {
+            const bool upper = (lane & off) != 0;
+            const int half = alive >> 1;
+#pragma unroll
+            for (int k = 0; k < half; ++k) {
+                const double give = upper ? v[k] : v[k + half];
+                const double keep = upper ? v[k + half] : v[k];
+                v[k] = keep + __shfl_xor_sync(kFullMask, give, off);
+            }
+        } else {
+            v[0] += __shfl_xor_sync(kFullMask, v[0], off);
+        }
+    }
+}
+
+// ---- static work split shared by kernels and their finalisers ---------------
+// U units are dealt to G CTAs as contiguous ranges [U*k/G, U*(k+1)/G), the
+// reference's own block formula (cemit.py:195-196) one level down.
+__host__ __device__ __forceinline__ long split_begin(long U, long G, long k)
+{
+    return (U * k) / G;
+}
+
+// the CTA whose range contains unit u (the largest k with split_begin(k) <= u)
+__host__ __device__ __forceinline__ long split_owner(long U, long G, long u)
+{
+    return ((u + 1) * G - 1) / U;
+}
+
+}  // namespace bto

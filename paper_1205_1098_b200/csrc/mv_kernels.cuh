@@ -1,0 +1,359 @@
+// mv_kernels.cuh -- the matrix-streaming engine behind BiCGK, ATAX, GESUMMV,
+// GEMVER (and DGEMV / DGEMVT / BATAX).
+//
+// One templated kernel streams a row-major fp64 matrix once and evaluates, on
+// the tile it holds in registers, any combination of
+//   N-product   rowdot[i] += A[i,j] * colw[j]      (q = A p, A x, B x)
+//   N2-product  the same on a second matrix         (GESUMMV's B x)
+//   T-product   colsum[j] += A[i,j] * roww[i]       (s = A' r, B' y)
+//   rank-2      B[i,j] = (A[i,j] + u1[i] v1[j]) + u2[i] v2[j], stored once,
+//               the T-product then runs on B        (GEMVER pass 1)
+// which is what "fusing the loops" of the reference's organisms means here
+// ({_i{_j 1 2}} for BiCGK, {_i{_j 1 3} ..} for GESUMMV,
+// {_i{_j 1 2 3 4 5}} for GEMVER).
+//
+// Decomposition.  The matrix is cut into column strips of SW = 512*V columns;
+// a strip is cut into units of R rows.  A thread owns 2*V columns of the strip
+// (one or two double2 per row -> every warp load is 512 contiguous bytes) and
+// walks DOWN the strip, so
+//   * column sums stay in 2*V registers for as long as the CTA stays in the
+//     strip and are flushed once per (CTA, strip) into `colpart`;
+//   * the column weights colw[j] are loaded once per strip (no re-read of x);
+//   * row dots are reduced per unit: warp_transpose_sum across the lanes,
+//     shared memory across the 8 warps, one partial per (strip, row) into
+//     `rowpart`.
+// Units are numbered strip-major and dealt to the G resident CTAs as equal
+// contiguous ranges (split_begin), i.e. the grid is persistent, perfectly
+// balanced, and a CTA touches at most a couple of strips.  A second tiny
+// kernel (finalize_kernel) adds the partials in a fixed order -- the
+// reference's "serial ascending-block join" (cemit.py:204-222).
+//
+// Overheads on top of the algorithmic bytes: rowpart = nstrips*M doubles
+// (N/SW of a vector per row: 1/(64*V) of the matrix), colpart <= slots*N.
+#pragma once
+#include "common.cuh"
+
+namespace bto {
+
+enum : int { kFlagN = 1, kFlagN2 = 2, kFlagT = 4, kFlagRank2 = 8 };
+
+struct MvArgs {
+    const double *A;        // matrix streamed (M x N row-major)
+    const double *A2;       // second matrix (kFlagN2)
+    double *Bout;           // rank-2 result (kFlagRank2)
+    const double *colw;     // [N] weights of the N-products
+    const double *roww;     // [M] weights of the T-product
+    const double *u1, *v1, *u2, *v2;   // rank-2 update vectors
+    double *rowpart;        // [nstrips][M]
+    double *rowpart2;       // [nstrips][M] (kFlagN2)
+    double *colpart;        // [slots][N]
+    long M, N;
+    long units_per_strip;   // ceil(M / R)
+    long total_units;       // nstrips * units_per_strip
+    int nstrips;
+};
+
+template <bool ALIGNED>
+__device__ __forceinline__ double2 mv_load(const double *base, long row, long N,
+                                           long j, bool ok0, bool ok1)
+{
+    const double *p = base + row * N + j;
+    if constexpr (ALIGNED) {
+        return ok0 ? ld_stream2(p) : make_double2(0.0, 0.0);
+    }
+    double2 v;
+    v.x = ok0 ? ld_stream1(p) : 0.0;
+    v.y = ok1 ? ld_stream1(p + 1) : 0.0;
+    return v;
+}
+
+// Per-thread view of the strip the CTA is walking down.
+template <int V>
+struct StripState {
+    long jcol[V];                     // first of the two columns of each double2
+    bool ok0[V], ok1[V];              // column j / j+1 inside the matrix
+    double2 cw[V], cv1[V], cv2[V];    // colw, v1, v2 at those columns
+    double2 csum[V];                  // running column sums (T-product)
+};
+
+// One unit = R rows of the strip.  INTERIOR units (all rows and the whole strip
+// inside the matrix) are predicate-free so every load is issued before the
+// first use; edge units are guarded.
+template <int FLAGS, int R, int V, bool ALIGNED, bool INTERIOR>
+__device__ __forceinline__ void mv_unit(const MvArgs &a, StripState<V> &st, long r0,
+                                        double (&rp)[R],
+                                        double (&rp2)[(FLAGS & kFlagN2) ? R : 1])
+{
+    constexpr bool kN = (FLAGS & kFlagN) != 0;
+    constexpr bool kN2 = (FLAGS & kFlagN2) != 0;
+    constexpr bool kT = (FLAGS & kFlagT) != 0;
+    constexpr bool kRank2 = (FLAGS & kFlagRank2) != 0;
+    constexpr bool kInterior = INTERIOR;
+    const long M = a.M, N = a.N;
+    long (&jcol)[V] = st.jcol;
+    bool (&ok0)[V] = st.ok0;
+    bool (&ok1)[V] = st.ok1;
+    double2 (&cw)[V] = st.cw;
+    double2 (&cv1)[V] = st.cv1;
+    double2 (&cv2)[V] = st.cv2;
+    double2 (&csum)[V] = st.csum;
+    double2 t[R][V], t2[kN2 ? R : 1][V];
+#pragma unroll
+    for (int i = 0; i < R; ++i) {
+        const bool rv = kInterior || (r0 + i < M);
+#pragma unroll
+        for (int v = 0; v < V; ++v) {
+            if constexpr (kInterior && ALIGNED) {
+                t[i][v] = ld_stream2(a.A + (r0 + i) * N + jcol[v]);
+                if constexpr (kN2) t2[i][v] = ld_stream2(a.A2 + (r0 + i) * N + jcol[v]);
+            } else {
+                t[i][v] = mv_load<ALIGNED>(a.A, r0 + i, N, jcol[v],
+                                           rv && ok0[v], rv && ok1[v]);
+                if constexpr (kN2) {
+                    t2[i][v] = mv_load<ALIGNED>(a.A2, r0 + i, N, jcol[v],
+                                                rv && ok0[v], rv && ok1[v]);
+                }
+            }
+        }
+    }
+    double rw[kT ? R : 1], ru1[kRank2 ? R : 1], ru2[kRank2 ? R : 1];
+#pragma unroll
+    for (int i = 0; i < R; ++i) {
+        const bool rv = kInterior || (r0 + i < M);
+        if constexpr (kT) rw[i] = rv ? __ldg(a.roww + r0 + i) : 0.0;
+        if constexpr (kRank2) {
+            ru1[i] = rv ? __ldg(a.u1 + r0 + i) : 0.0;
+            ru2[i] = rv ? __ldg(a.u2 + r0 + i) : 0.0;
+        }
+    }
+#pragma unroll
+    for (int i = 0; i < R; ++i) {
+        const long row = r0 + i;
+        const bool rv = kInterior || (row < M);
+        double dot = 0.0, dot2 = 0.0;
+#pragma unroll
+        for (int v = 0; v < V; ++v) {
+            double2 e = t[i][v];
+            if constexpr (kRank2) {
+                // t0 = u1*v1 ; t1 = A + t0 ; t2 = u2*v2 ; B = t1 + t2
+                e.x = __dadd_rn(__dadd_rn(e.x, __dmul_rn(ru1[i], cv1[v].x)),
+                                __dmul_rn(ru2[i], cv2[v].x));
+                e.y = __dadd_rn(__dadd_rn(e.y, __dmul_rn(ru1[i], cv1[v].y)),
+                                __dmul_rn(ru2[i], cv2[v].y));
+                double *dst = a.Bout + row * N + jcol[v];
+                if constexpr (ALIGNED) {
+                    if (kInterior || (rv && ok0[v])) st_stream2(dst, e);
+                } else {
+                    if (rv && ok0[v]) st_stream1(dst, e.x);
+                    if (rv && ok1[v]) st_stream1(dst + 1, e.y);
+                }
+            }
+            if constexpr (kN) {
+                dot = fma(e.x, cw[v].x, dot);
+                dot = fma(e.y, cw[v].y, dot);
+            }
+            if constexpr (kN2) {
+                dot2 = fma(t2[i][v].x, cw[v].x, dot2);
+                dot2 = fma(t2[i][v].y, cw[v].y, dot2);
+            }
+            if constexpr (kT) {
+                csum[v].x = fma(e.x, rw[i], csum[v].x);
+                csum[v].y = fma(e.y, rw[i], csum[v].y);
+            }
+        }
+        rp[i] = dot;
+        if constexpr (kN2) rp2[i] = dot2;
+    }
+}
+
+template <int FLAGS, int R, int V, bool ALIGNED>
+__global__ void __launch_bounds__(kThreads)
+mv_tile_kernel(const MvArgs a)
+{
+    constexpr bool kN = (FLAGS & kFlagN) != 0;
+    constexpr bool kN2 = (FLAGS & kFlagN2) != 0;
+    constexpr bool kT = (FLAGS & kFlagT) != 0;
+    constexpr bool kRank2 = (FLAGS & kFlagRank2) != 0;
+    static_assert(!kN2 || kN, "the second N-product rides on the first");
+    constexpr int kRowSets = kN2 ? 2 : 1;
+    constexpr int kLanesPerRow = 32 / R;
+    constexpr long kStripWidth = (long)kThreads * 2 * V;
+
+    __shared__ double red[2][kRowSets][kWarps][R];
+
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const long G = gridDim.x, cta = blockIdx.x;
+    const long u_begin = split_begin(a.total_units, G, cta);
+    const long u_end = split_begin(a.total_units, G, cta + 1);
+    const long M = a.M, N = a.N;
+
+    long strip = -1;
+    bool strip_inside = false;
+    StripState<V> st;
+    long (&jcol)[V] = st.jcol;
+    bool (&ok0)[V] = st.ok0;
+    bool (&ok1)[V] = st.ok1;
+    double2 (&cw)[V] = st.cw;
+    double2 (&cv1)[V] = st.cv1;
+    double2 (&cv2)[V] = st.cv2;
+    double2 (&csum)[V] = st.csum;
+    int buf = 0;
+
+    auto flush_colsums = [&]() {
+        // this CTA's slot among the CTAs that share the strip
+        const long first = split_owner(a.total_units, G, strip * a.units_per_strip);
+        double *dst = a.colpart + (cta - first) * N;
+#pragma unroll
+        for (int v = 0; v < V; ++v) {
+            if constexpr (ALIGNED) {
+                if (ok0[v]) *reinterpret_cast<double2 *>(dst + jcol[v]) = csum[v];
+            } else {
+                if (ok0[v]) dst[jcol[v]] = csum[v].x;
+                if (ok1[v]) dst[jcol[v] + 1] = csum[v].y;
+            }
+        }
+    };
+
+    for (long u = u_begin; u < u_end; ++u) {
+        const long c = u / a.units_per_strip;
+        const long r0 = (u - c * a.units_per_strip) * R;
+        if (c != strip) {
+            if (kT && strip >= 0) flush_colsums();
+            strip = c;
+            strip_inside = (c + 1) * kStripWidth <= N;
+#pragma unroll
+            for (int v = 0; v < V; ++v) {
+                const long j = c * kStripWidth + (long)v * (kThreads * 2) + 2 * tid;
+                jcol[v] = j;
+                ok0[v] = j < N;
+                ok1[v] = j + 1 < N;
+                csum[v] = make_double2(0.0, 0.0);
+                if constexpr (kN || kN2) {
+                    cw[v].x = ok0[v] ? __ldg(a.colw + j) : 0.0;
+                    cw[v].y = ok1[v] ? __ldg(a.colw + j + 1) : 0.0;
+                }
+                if constexpr (kRank2) {
+                    cv1[v].x = ok0[v] ? __ldg(a.v1 + j) : 0.0;
+                    cv1[v].y = ok1[v] ? __ldg(a.v1 + j + 1) : 0.0;
+                    cv2[v].x = ok0[v] ? __ldg(a.v2 + j) : 0.0;
+                    cv2[v].y = ok1[v] ? __ldg(a.v2 + j + 1) : 0.0;
+                }
+            }
+        }
+
+        double rp[R], rp2[kN2 ? R : 1];
+        // Interior units (all R rows and the whole strip inside the matrix) take
+        // a predicate-free path so that every load of the unit is issued before
+        // the first use; edge units take the guarded path.
+        if (strip_inside && r0 + R <= M) {
+            mv_unit<FLAGS, R, V, ALIGNED, true>(a, st, r0, rp, rp2);
+        } else {
+            mv_unit<FLAGS, R, V, ALIGNED, false>(a, st, r0, rp, rp2);
+        }
+
+        if constexpr (kN) {
+            // lanes -> one value per row, then the 8 warps through shared memory
+            warp_transpose_sum<R>(rp, lane);
+            if ((lane % kLanesPerRow) == 0) red[buf][0][warp][lane / kLanesPerRow] = rp[0];
+            if constexpr (kN2) {
+                warp_transpose_sum<R>(rp2, lane);
+                if ((lane % kLanesPerRow) == 0)
+                    red[buf][kRowSets - 1][warp][lane / kLanesPerRow] = rp2[0];
+            }
+            __syncthreads();
+            if (tid < R * kRowSets) {
+                const int set = tid / R, i = tid % R;
+                double s = red[buf][set][0][i];
+#pragma unroll
+                for (int w = 1; w < kWarps; ++w) s += red[buf][set][w][i];
+                if (r0 + i < M) {
+                    double *dst = set == 1 ? a.rowpart2 : a.rowpart;
+                    dst[strip * M + r0 + i] = s;
+                }
+            }
+            // red[] is double-buffered: the next unit writes the other half and
+            // its __syncthreads orders this unit's reads before buf is reused.
+            buf ^= 1;
+        }
+    }
+    if (kT && strip >= 0) flush_colsums();
+}
+
+// ---- finaliser: fixed-order join of the partials + the sequence's epilogue ----
+enum ColMode : int { kColNone = 0, kColPlain = 1, kColAxpz = 2, kColScale = 3 };
+enum RowMode : int { kRowNone = 0, kRowPlain = 1, kRowGesummv = 2, kRowScale = 3,
+                     kRowDgemv = 4 };
+
+struct FinArgs {
+    // column side: out[j] = f( sum_k colpart[k][j] )
+    const double *colpart;
+    double *colout;
+    const double *colz;       // kColAxpz: x = sum*cscale + z
+    double cscale;
+    int cmode;
+    long N;
+    long units_per_strip, total_units, grid;   // geometry of the producer launch
+    long strip_width;
+    // row side: out[i] = f( sum_c rowpart[c][i] )
+    const double *rowpart, *rowpart2;
+    double *rowout;
+    const double *rowy;       // kRowDgemv: z = sum*alpha + y*beta
+    double ralpha, rbeta;
+    int rmode;
+    long M;
+    int nstrips;
+    int col_blocks;           // CTAs [0, col_blocks) do columns, the rest rows
+};
+
+__global__ void __launch_bounds__(kThreads)
+finalize_kernel(const FinArgs f)
+{
+    if ((int)blockIdx.x < f.col_blocks) {
+        const long j = (long)blockIdx.x * kThreads + threadIdx.x;
+        if (j >= f.N) return;
+        const long strip = j / f.strip_width;
+        const long first = split_owner(f.total_units, f.grid, strip * f.units_per_strip);
+        const long last = split_owner(f.total_units, f.grid,
+                                      (strip + 1) * f.units_per_strip - 1);
+        double s = f.colpart[j];
+        for (long k = 1; k <= last - first; ++k) s += f.colpart[k * f.N + j];
+        if (f.cmode == kColAxpz) {            // t4 = t3*beta ; x = t4 + z
+            s = __dadd_rn(__dmul_rn(s, f.cscale), f.colz[j]);
+        } else if (f.cmode == kColScale) {    // y = t1*beta
+            s = __dmul_rn(s, f.cscale);
+        }
+        f.colout[j] = s;
+    } else {
+        const long i = (long)(blockIdx.x - f.col_blocks) * kThreads + threadIdx.x;
+        if (i >= f.M) return;
+        double s = f.rowpart[i];
+        for (int c = 1; c < f.nstrips; ++c) s += f.rowpart[(long)c * f.M + i];
+        if (f.rmode == kRowGesummv) {         // t1 = t0*alpha ; t3 = t2*beta ; y = t1 + t3
+            double s2 = f.rowpart2[i];
+            for (int c = 1; c < f.nstrips; ++c) s2 += f.rowpart2[(long)c * f.M + i];
+            s = __dadd_rn(__dmul_rn(s, f.ralpha), __dmul_rn(s2, f.rbeta));
+        } else if (f.rmode == kRowScale) {    // w = t5*alpha
+            s = __dmul_rn(s, f.ralpha);
+        } else if (f.rmode == kRowDgemv) {    // t1 = t0*alpha ; t2 = y*beta ; z = t1 + t2
+            s = __dadd_rn(__dmul_rn(s, f.ralpha), __dmul_rn(f.rowy[i], f.rbeta));
+        }
+        f.rowout[i] = s;
+    }
+}
+
+// x = colsum*beta + z on its own (the sharded GEMVER exchanges colsum first)
+__global__ void __launch_bounds__(kThreads)
+axpz_kernel(const double *colsum, double beta, const double *z, double *x, long n)
+{
+    const long j = (long)blockIdx.x * kThreads + threadIdx.x;
+    if (j < n) x[j] = __dadd_rn(__dmul_rn(colsum[j], beta), z[j]);
+}
+
+__global__ void __launch_bounds__(kThreads)
+fill_kernel(double *dst, double value, long n)
+{
+    const long j = (long)blockIdx.x * kThreads + threadIdx.x;
+    if (j < n) dst[j] = value;
+}
+
+}  // namespace bto

@@ -1,0 +1,168 @@
+"""Row-sharded multi-GPU execution: one process per GPU, one all-reduce per kernel.
+
+The reference parallelises by cutting ONE axis into static blocks
+(`lo = ext*p/t, hi = ext*(p+1)/t`, cemit.py:195-196), giving each block its
+own partial buffer for reductions that cross the cut and joining the
+partials afterwards (lower.py:123-135, cemit.py:204-222).  This module lifts
+that protocol one level: rank g of G owns rows [M*g/G, M*(g+1)/G) of every
+matrix and of every row-indexed vector; column-indexed vectors are
+replicated; the "join" is a sum all-reduce over NCCL/NVLink of the
+column-indexed result:
+
+    AXPYDOT  all vectors sliced           all-reduce 1 fp64   (beta)
+    BiCGK    q stays sharded              all-reduce N fp64   (s)
+    ATAX     --                           all-reduce N fp64   (y)
+    GESUMMV  y stays sharded              none
+    GEMVER   B, w stay sharded            all-reduce N fp64   (B'y) BETWEEN the passes
+
+`local` is the per-shard compute: in production `GpuShardOps` (the C ABI on
+this rank's device); the CPU tests inject a numpy implementation to exercise
+the slicing / exchange logic over gloo.
+"""
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass
+
+__all__ = ["row_block", "ShardSpec", "SHARDING", "ShardedRunner", "GpuShardOps"]
+
+
+def row_block(extent: int, rank: int, world: int) -> tuple[int, int]:
+    """Rows owned by `rank`: the reference's block bounds (cemit.py:195-196)."""
+    return (extent * rank) // world, (extent * (rank + 1)) // world
+
+
+@dataclass(frozen=True)
+class ShardSpec:
+    row_sliced: tuple[str, ...]      # inputs/outputs indexed by the row axis (sliced)
+    replicated: tuple[str, ...]      # column-indexed inputs (every rank holds all)
+    reduced: tuple[str, ...]         # outputs that need the sum all-reduce
+    sharded_out: tuple[str, ...]     # outputs that stay row-sharded
+
+
+SHARDING = {
+    "axpydot": ShardSpec(("w", "v", "u", "z"), (), ("beta",), ("z",)),
+    "bicgk": ShardSpec(("A", "r", "q"), ("p",), ("s",), ("q",)),
+    "atax": ShardSpec(("A",), ("x",), ("y",), ()),
+    "gesummv": ShardSpec(("A", "B", "y"), ("x",), (), ("y",)),
+    "gemver": ShardSpec(("A", "u1", "u2", "y", "B", "w"), ("v1", "v2", "z"),
+                        ("x",), ("B", "w")),
+}
+
+
+def shard_inputs(name: str, inputs: dict, rank: int, world: int, rows: int) -> dict:
+    """Slice full-size inputs down to what `rank` owns (used by tests/bench)."""
+    lo, hi = row_block(rows, rank, world)
+    spec = SHARDING[name]
+    return {k: (v[lo:hi] if k in spec.row_sliced else v) for k, v in inputs.items()}
+
+
+class ShardedRunner:
+    """Runs one kernel on this rank's shard and performs the exchange.
+
+    comm: an object with `all_reduce_sum(tensor_or_array)` (in place);
+    local: shard compute with methods named after the kernels (see GpuShardOps).
+    """
+
+    def __init__(self, local, comm, rank: int, world: int):
+        self.local, self.comm, self.rank, self.world = local, comm, rank, world
+
+    def axpydot(self, w, v, u, alpha, z, beta):
+        self.local.axpydot(w, v, u, alpha, z, beta)
+        if self.world > 1:
+            self.comm.all_reduce_sum(beta)
+
+    def bicgk(self, A, p, r, q, s):
+        self.local.bicgk(A, p, r, q, s)
+        if self.world > 1:
+            self.comm.all_reduce_sum(s)
+
+    def atax(self, A, x, y):
+        # t = A_g x is complete on the rank (rows are whole), y_g = A_g' t
+        self.local.atax(A, x, y)
+        if self.world > 1:
+            self.comm.all_reduce_sum(y)
+
+    def gesummv(self, alpha, beta, A, B, x, y):
+        self.local.gesummv(alpha, beta, A, B, x, y)
+
+    def gemver(self, A, u1, v1, u2, v2, alpha, beta, y, z, B, x, w, colsum):
+        """colsum: N-element scratch for the exchanged B'y partials."""
+        self.local.gemver_pass1(A, u1, v1, u2, v2, y, B, colsum)
+        if self.world > 1:
+            self.comm.all_reduce_sum(colsum)
+        self.local.gemver_xupdate(colsum, beta, z, x)
+        self.local.gemver_pass2(B, x, alpha, w)
+
+
+class TorchComm:
+    """Sum all-reduce through torch.distributed (NCCL on GPUs, gloo in tests)."""
+
+    def __init__(self, group=None):
+        import torch.distributed as dist
+        self.dist, self.group = dist, group
+
+    def all_reduce_sum(self, tensor):
+        self.dist.all_reduce(tensor, op=self.dist.ReduceOp.SUM, group=self.group)
+
+
+class GpuShardOps:
+    """Per-shard compute through the asynchronous C ABI on the current stream.
+
+    All arguments are contiguous float64 CUDA tensors on this rank's device
+    (scalars are Python floats; `beta` of AXPYDOT is a 1-element tensor).
+    """
+
+    def __init__(self, stream=None):
+        from . import _native
+        self._native = _native
+        self.lib = _native.load()
+        self._stream = stream
+
+    def _st(self):
+        import torch
+        stream = self._stream or torch.cuda.current_stream()
+        return ctypes.c_void_p(stream.cuda_stream)
+
+    @staticmethod
+    def _p(t):
+        return ctypes.c_void_p(t.data_ptr())
+
+    def axpydot(self, w, v, u, alpha, z, beta):
+        self._native.check(self.lib.bto_axpydot_async(
+            self._p(w), self._p(v), self._p(u), float(alpha), self._p(z), self._p(beta),
+            w.numel(), self._st()))
+
+    def bicgk(self, A, p, r, q, s):
+        self._native.check(self.lib.bto_bicgk_async(
+            self._p(A), self._p(p), self._p(r), self._p(q), self._p(s),
+            A.shape[0], A.shape[1], self._st()))
+
+    def atax(self, A, x, y):
+        self._native.check(self.lib.bto_atax_async(
+            self._p(A), self._p(x), self._p(y), A.shape[0], A.shape[1], self._st()))
+
+    def gesummv(self, alpha, beta, A, B, x, y):
+        self._native.check(self.lib.bto_gesummv_async(
+            float(alpha), float(beta), self._p(A), self._p(B), self._p(x), self._p(y),
+            A.shape[0], A.shape[1], self._st()))
+
+    def gemver(self, A, u1, v1, u2, v2, alpha, beta, y, z, B, x, w):
+        self._native.check(self.lib.bto_gemver_async(
+            self._p(A), self._p(u1), self._p(v1), self._p(u2), self._p(v2),
+            float(alpha), float(beta), self._p(y), self._p(z), self._p(B), self._p(x),
+            self._p(w), A.shape[0], A.shape[1], self._st()))
+
+    def gemver_pass1(self, A, u1, v1, u2, v2, y, B, colsum):
+        self._native.check(self.lib.bto_gemver_pass1_async(
+            self._p(A), self._p(u1), self._p(v1), self._p(u2), self._p(v2), self._p(y),
+            self._p(B), self._p(colsum), A.shape[0], A.shape[1], self._st()))
+
+    def gemver_xupdate(self, colsum, beta, z, x):
+        self._native.check(self.lib.bto_gemver_xupdate_async(
+            self._p(colsum), float(beta), self._p(z), self._p(x), x.numel(), self._st()))
+
+    def gemver_pass2(self, B, x, alpha, w):
+        self._native.check(self.lib.bto_gemver_pass2_async(
+            self._p(B), self._p(x), float(alpha), self._p(w), B.shape[0], B.shape[1],
+            self._st()))

@@ -1,0 +1,32 @@
+from __future__ import annotations
+
+import sys
+from pathlib import Path
+
+import pytest
+
+REPO = Path(__file__).resolve().parent.parent
+if str(REPO) not in sys.path:
+    sys.path.insert(0, str(REPO))
+if str(REPO / "tests") not in sys.path:
+    sys.path.insert(0, str(REPO / "tests"))
+
+
+def pytest_configure(config):
+    config.addinivalue_line("markers", "gpu: needs a real B200 (run with -m gpu)")
+
+
+@pytest.fixture(scope="session")
+def oracle():
+    import oracle_lib
+    oracle_lib.ensure_built()
+    return oracle_lib
+
+
+@pytest.fixture(scope="session")
+def bto_lib():
+    """The product package with its CUDA library loaded (GPU tests only)."""
+    import paper_1205_1098_b200 as pkg
+    from paper_1205_1098_b200 import _native
+    _native.load()
+    return pkg

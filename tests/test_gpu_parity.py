@@ -1,0 +1,268 @@
+"""Parity of the sm_100a kernels with the reference, through the C ABI.
+
+Every test here needs a B200 (`-m gpu`).  The checker is the CPU oracle
+(oracle/, bit-identical to the reference's generated C -- tests/test_oracle.py)
+and the committed golden outputs of the reference itself.  Gate (BASELINE.json
+north_star): max relative error <= 1e-12 * log2(n) with the reference's metric
+|g - e| / max(|e|, 1) (runtime.py:167-175); outputs that involve no reduction
+(AXPYDOT z, GEMVER B, VADD x, WAXPBY w) must be BIT-IDENTICAL.
+"""
+from __future__ import annotations
+
+import math
+
+import numpy as np
+import pytest
+import torch
+
+import golden_util as G
+import paper_1205_1098_b200 as bto
+from paper_1205_1098_b200 import _native
+
+pytestmark = pytest.mark.gpu
+
+KERNELS = tuple(bto.CORPUS)
+ELEMENTWISE = {"axpydot": ("z",), "gemver": ("B",), "vadd": ("x",), "waxpby": ("w",)}
+
+
+def tol(ext: dict) -> float:
+    return 1e-12 * max(1.0, math.log2(max(ext.values())))
+
+
+def ext_of(name: str, m: int, n: int) -> dict:
+    return {"M": m} if bto.load_graph(name).extent_names == ("M",) else {"M": m, "N": n}
+
+
+def run_host(name, inputs, ext):
+    g = bto.load_graph(name)
+    return bto.run_kernel(bto.library_path(), bto.gpu_kernel(g), g, inputs, ext)
+
+
+def run_device(name, inputs, ext):
+    g = bto.load_graph(name)
+    dev = {k: (torch.from_numpy(np.ascontiguousarray(v)).cuda() if isinstance(v, np.ndarray) else v)
+           for k, v in inputs.items()}
+    out = bto.run_kernel(bto.library_path(), bto.gpu_kernel(g), g, dev, ext)
+    return {k: (v.cpu().numpy() if hasattr(v, "cpu") else v) for k, v in out.items()}
+
+
+def assert_matches(name, got, want, ext, what=""):
+    for out in want:
+        assert not np.any(np.isnan(np.asarray(got[out]))), f"{name}.{out} has unwritten (NaN) elements"
+    err = bto.max_rel_error(got, want)
+    assert err <= tol(ext), f"{name} {ext} {what}: error {err:.3e} > {tol(ext):.3e}"
+    for out in ELEMENTWISE.get(name, ()):
+        assert np.array_equal(np.asarray(got[out]), np.asarray(want[out])), \
+            f"{name}.{out} {ext} {what}: not bit-identical"
+
+
+@pytest.mark.parametrize("name", KERNELS)
+def test_golden_small_cases_host_and_device_pointers(bto_lib, name):
+    graph = bto.load_graph(name)
+    for (m, n, seed) in G.small_cases(name):
+        ext = ext_of(name, m, n)
+        inputs = bto.random_inputs(graph, ext, seed=seed)
+        prefix = f"small/{m}x{n}/s{seed}"
+        for runner in (run_host, run_device):
+            got = runner(name, inputs, ext)
+            for which in ("O2", "O1"):
+                want = G.expected(name, prefix, which)
+                assert G.max_err(got, want) <= tol(ext), (name, ext, seed, which, runner.__name__)
+            for out in ELEMENTWISE.get(name, ()):
+                assert G.bit_equal(got[out], G.expected(name, prefix, "O2")[out]), (name, ext, out)
+
+
+@pytest.mark.parametrize("name", bto.HOT_PATH)
+def test_check_configs_against_reference_outputs(bto_lib, name):
+    """BASELINE.json check sizes and seeds, against the reference's own outputs."""
+    graph = bto.load_graph(name)
+    ext = bto.CHECK_CONFIGS[name]
+    inputs = bto.gen_inputs(graph, ext, seed=bto.SEEDS[name])
+    assert G.sha([inputs[k] for k, _ in graph.spec.inputs]) == G.inputs_sha(name, "check")
+    got = run_device(name, inputs, ext)
+    for which in ("O2", "O1"):
+        err = G.max_err(got, G.expected(name, "check", which))
+        assert err <= tol(ext), f"{name} vs {which}: {err:.3e}"
+    for out in ELEMENTWISE.get(name, ()):
+        assert G.bit_equal(got[out], G.expected(name, "check", "O2")[out]), (name, out)
+
+
+RAGGED = [(1, 1), (1, 513), (513, 1), (3, 1000), (1000, 3), (255, 511), (257, 1026),
+          (1031, 2050), (64, 4096), (4100, 514), (129, 1537)]
+
+
+@pytest.mark.parametrize("name", KERNELS)
+def test_ragged_extents_against_live_oracle(bto_lib, oracle, name):
+    """Edge tiles: extents that are not multiples of the strip width or the
+    unit height, odd N (unaligned rows -> scalar-load path), single row/column."""
+    graph = bto.load_graph(name)
+    for (m, n) in RAGGED:
+        ext = ext_of(name, m, n)
+        inputs = bto.gen_inputs(graph, ext, seed=m * 7 + n)
+        want = oracle.oracle_run(name, inputs, ext, threads=8)
+        assert_matches(name, run_device(name, inputs, ext), want, ext, "device")
+    ext = ext_of(name, 300, 77)
+    inputs = bto.gen_inputs(graph, ext, seed=1)
+    assert_matches(name, run_host(name, inputs, ext),
+                   oracle.oracle_run(name, inputs, ext, threads=8), ext, "host")
+
+
+@pytest.mark.parametrize("rows,vec", [(8, 1), (16, 1), (8, 2)])
+def test_every_tile_variant(bto_lib, oracle, rows, vec):
+    old = (_native.get_tuning("mv_rows"), _native.get_tuning("mv_vec"))
+    try:
+        _native.set_tuning(mv_rows=rows, mv_vec=vec)
+        for name in ("bicgk", "atax", "gesummv", "gemver", "dgemv", "dgemvt", "batax"):
+            graph = bto.load_graph(name)
+            for (m, n) in [(777, 1300), (2048, 1024), (1500, 3000)]:
+                ext = {"M": m, "N": n}
+                inputs = bto.gen_inputs(graph, ext, seed=m + n)
+                want = oracle.oracle_run(name, inputs, ext, threads=8)
+                assert_matches(name, run_device(name, inputs, ext), want, ext, f"R{rows}V{vec}")
+    finally:
+        _native.set_tuning(mv_rows=old[0], mv_vec=old[1])
+
+
+@pytest.mark.parametrize("grid_per_sm", [1, 3, 16])
+def test_grid_size_only_changes_reduction_order(bto_lib, oracle, grid_per_sm):
+    try:
+        _native.set_tuning(grid_per_sm=grid_per_sm, vec_grid_per_sm=grid_per_sm)
+        for name, ext in (("bicgk", {"M": 3000, "N": 2500}), ("axpydot", {"M": 1234567}),
+                          ("gemver", {"M": 1200, "N": 2200})):
+            graph = bto.load_graph(name)
+            inputs = bto.gen_inputs(graph, ext, seed=3)
+            want = oracle.oracle_run(name, inputs, ext, threads=8)
+            assert_matches(name, run_device(name, inputs, ext), want, ext, f"grid{grid_per_sm}")
+    finally:
+        _native.set_tuning(grid_per_sm=0, vec_grid_per_sm=0)
+
+
+def test_unaligned_device_pointers(bto_lib, oracle):
+    """8-byte-aligned (not 16) base pointers must take the scalar-load path."""
+    m, n = 300, 258
+    graph = bto.load_graph("bicgk")
+    inputs = bto.gen_inputs(graph, {"M": m, "N": n}, seed=9)
+    want = oracle.oracle_run("bicgk", inputs, {"M": m, "N": n}, threads=8)
+    pad = torch.empty(m * n + 1, dtype=torch.float64, device="cuda")
+    A = pad[1:].view(m, n)
+    A.copy_(torch.from_numpy(inputs["A"]))
+    assert A.data_ptr() % 16 == 8
+    dev = {"A": A, "p": torch.from_numpy(inputs["p"]).cuda(), "r": torch.from_numpy(inputs["r"]).cuda()}
+    got = bto.run_kernel(bto.library_path(), bto.gpu_kernel(graph), graph, dev, {"M": m, "N": n})
+    assert bto.max_rel_error(got, want) <= tol({"M": m, "N": n})
+    # vector kernel, odd offset
+    g2 = bto.load_graph("axpydot")
+    k = 100001
+    inp = bto.gen_inputs(g2, {"M": k}, seed=2)
+    want = oracle.oracle_run("axpydot", inp, {"M": k}, threads=8)
+    buf = torch.empty(3 * k + 3, dtype=torch.float64, device="cuda")
+    dev = {"alpha": inp["alpha"]}
+    for idx, nm in enumerate(("w", "v", "u")):
+        view = buf[idx * (k + 1) + 1: idx * (k + 1) + 1 + k]
+        view.copy_(torch.from_numpy(inp[nm]))
+        dev[nm] = view
+    got = bto.run_kernel(bto.library_path(), bto.gpu_kernel(g2), g2, dev, {"M": k})
+    assert np.array_equal(got["z"].cpu().numpy(), want["z"])
+    assert bto.max_rel_error(got, want) <= tol({"M": k})
+
+
+def test_results_are_bit_stable_run_to_run(bto_lib):
+    for name in ("axpydot", "bicgk", "gemver"):
+        graph = bto.load_graph(name)
+        ext = ext_of(name, 4096, 3072) if name != "axpydot" else {"M": 1 << 22}
+        inputs = bto.gen_inputs(graph, ext, seed=0)
+        a = run_device(name, inputs, ext)
+        b = run_device(name, inputs, ext)
+        for out in a:
+            assert np.array_equal(np.asarray(a[out]), np.asarray(b[out])), (name, out)
+
+
+def test_bad_extents_are_errors(bto_lib):
+    lib = _native.load()
+    x = torch.zeros(8, dtype=torch.float64, device="cuda")
+    rc = lib.bto_vadd_async(x.data_ptr(), x.data_ptr(), x.data_ptr(), x.data_ptr(), 0, None)
+    assert rc == 2 and lib.bto_last_error() == 2
+    with pytest.raises(_native.BtoError):
+        _native.check(rc)
+
+
+def test_known_answers_on_gpu(bto_lib):
+    # the reference's own KATs (tests/test_codegen.py:46-59)
+    out = run_host("batax", {"A": np.eye(3), "x": np.array([1.0, 2.0, 3.0]), "beta": 2.0},
+                   {"M": 3, "N": 3})
+    np.testing.assert_array_equal(out["y"], [2.0, 4.0, 6.0])
+    y = np.array([3.0, -1.0, 4.0])
+    out = run_host("dgemv", {"A": np.ones((3, 2)), "x": np.ones(2), "alpha": 0.0, "beta": 1.0,
+                             "y": y}, {"M": 3, "N": 2})
+    np.testing.assert_array_equal(out["z"], y)
+
+
+# ---- full BASELINE sizes: size-independent properties (no CPU oracle at 8 GiB) ----
+
+def _rand(shape, seed):
+    gen = torch.Generator(device="cuda").manual_seed(seed)
+    return torch.rand(shape, dtype=torch.float64, device="cuda", generator=gen) * 2 - 1
+
+
+def _run(name, inputs, ext):
+    g = bto.load_graph(name)
+    return bto.run_kernel(bto.library_path(), bto.gpu_kernel(g), g, inputs, ext)
+
+
+def _err(a, b):
+    return float(torch.max(torch.abs(a - b) / torch.clamp(torch.abs(b), min=1.0)))
+
+
+def test_bench_size_cross_kernel_identities(bto_lib):
+    n = 32768
+    ext = {"M": n, "N": n}
+    t = 1e-12 * math.log2(n)
+    A = _rand((n, n), 1)
+    p, r = _rand((n,), 2), _rand((n,), 3)
+    bi = _run("bicgk", {"A": A, "p": p, "r": r}, ext)
+    # independent check of both products (cuBLAS fp64 as a second opinion)
+    assert _err(bi["q"], torch.mv(A, p)) <= t
+    assert _err(bi["s"], torch.mv(A.t(), r)) <= t
+    # ATAX(A, x) == s of BiCGK(A, p=x, r=A x)
+    at = _run("atax", {"A": A, "x": p}, ext)
+    s2 = _run("bicgk", {"A": A, "p": p, "r": bi["q"]}, ext)["s"]
+    assert _err(at["y"], s2) <= t * 4
+    # GEMVER with zero rank-2 vectors: B == A bit for bit, x = beta A'y + z, w = alpha A x
+    zero = torch.zeros(n, dtype=torch.float64, device="cuda")
+    z = _rand((n,), 4)
+    ge = _run("gemver", {"A": A, "u1": zero, "v1": zero, "u2": zero, "v2": zero,
+                         "alpha": 0.5, "beta": -0.25, "y": r, "z": z}, ext)
+    assert torch.equal(ge["B"], A)
+    assert _err(ge["x"], -0.25 * bi["s"] + z) <= t
+    assert _err(ge["w"], 0.5 * torch.mv(A, ge["x"])) <= t * 4
+    # full GEMVER: rows of B against the definition on a sample, x/w via cuBLAS on B
+    u1, v1, u2, v2 = (_rand((n,), s) for s in (5, 6, 7, 8))
+    ge = _run("gemver", {"A": A, "u1": u1, "v1": v1, "u2": u2, "v2": v2,
+                         "alpha": 0.7, "beta": 0.3, "y": r, "z": z}, ext)
+    rows = torch.tensor([0, 1, 4097, n // 2, n - 1], device="cuda")
+    want = (A[rows] + u1[rows, None] * v1[None, :]) + u2[rows, None] * v2[None, :]
+    assert torch.equal(ge["B"][rows], want)
+    assert _err(ge["x"], 0.3 * torch.mv(ge["B"].t(), r) + z) <= t
+    assert _err(ge["w"], 0.7 * torch.mv(ge["B"], ge["x"])) <= t * 4
+    del ge, A, want
+    torch.cuda.empty_cache()
+    # GESUMMV at its own bench size: B = A and beta = alpha  =>  y = 2 alpha A x
+    m = 24576
+    A = _rand((m, m), 9)
+    x = _rand((m,), 10)
+    y = _run("gesummv", {"alpha": 0.375, "beta": 0.375, "A": A, "B": A, "x": x},
+             {"M": m, "N": m})["y"]
+    assert _err(y, 0.75 * torch.mv(A, x)) <= 1e-12 * math.log2(m)
+
+
+def test_bench_size_axpydot_properties(bto_lib):
+    n = 1 << 27
+    w, v, u = _rand((n,), 1), _rand((n,), 2), _rand((n,), 3)
+    out = _run("axpydot", {"w": w, "v": v, "u": u, "alpha": 0.0}, {"M": n})
+    assert torch.equal(out["z"], w)                      # alpha = 0: z is w, bit for bit
+    ref = float(torch.dot(w, u))
+    assert abs(out["beta"] - ref) / max(abs(ref), 1.0) <= 1e-12 * 27
+    out = _run("axpydot", {"w": w, "v": v, "u": u, "alpha": -0.625}, {"M": n})
+    assert torch.equal(out["z"], w - v * (-0.625))       # mul then sub, each rounded once
+    ref = float(torch.dot(out["z"], u))
+    assert abs(out["beta"] - ref) / max(abs(ref), 1.0) <= 1e-12 * 27
