@@ -14,6 +14,7 @@
 #include <mutex>
 #include <vector>
 
+#include "atax_cluster.cuh"
 #include "bto_b200.h"
 #include "mv_kernels.cuh"
 #include "vec_kernels.cuh"
@@ -62,6 +63,12 @@ struct Tuning {
     long grid_per_sm = 0;    // CTAs per SM for the matrix kernels, 0 = occupancy
     long vec_unroll = 4;     // independent double2 triples in flight (1 | 2 | 4)
     long vec_grid_per_sm = 0;
+    long atax_fused = 1;     // 1: single-pass cluster kernel when applicable, 0: two passes
+    long atax_cluster = 0;   // cluster size of the fused ATAX (0 = auto | 1 | 2 | 4 | 8 | 16)
+    long atax_stages = 0;    // TMA ring depth (0 = as many as fit, at most 8)
+    long atax_rows = 0;      // rows per panel (0 = auto)
+    long atax_lookahead = 0; // panels phase 1 runs ahead of phase 2 (0 = auto | 1..3)
+    long debug = 0;          // print launch plans to stderr
 };
 
 struct DeviceCtx {
@@ -78,6 +85,7 @@ struct DeviceCtx {
     size_t arena_bytes = 0;
     cudaStream_t stream = nullptr; // stream of the section-1 entry points
     std::map<const void *, int> occupancy;
+    std::map<const void *, int> max_clusters;
 };
 
 std::mutex g_mu;
@@ -408,12 +416,178 @@ int seq_bicgk(DeviceCtx &c, const double *A, const double *p, const double *r,
     return pass.run(c, a, f, st);
 }
 
+// ---- fused single-pass ATAX (atax_cluster.cuh) -----------------------------------
+
+using AtaxKernel = void (*)(const AtaxArgs);
+
+struct AtaxPlan {
+    AtaxKernel fn = nullptr;     // nullptr: not applicable, use the two-pass sequence
+    int C = 1, KMAX = 1, RG = 1, W = 0, S = 0, L = 1;
+    size_t smem = 0;
+    int nclusters = 0;
+};
+
+template <int C>
+AtaxKernel atax_kernel_ptr(int kmax)
+{
+    switch (kmax) {
+        case 1: return atax_cluster_kernel<C, 1>;
+        case 2: return atax_cluster_kernel<C, 2>;
+        case 4: return atax_cluster_kernel<C, 4>;
+        case 8: return atax_cluster_kernel<C, 8>;
+        case 16: return atax_cluster_kernel<C, 16>;
+    }
+    return nullptr;
+}
+
+AtaxKernel atax_kernel_ptr(int c, int kmax)
+{
+    switch (c) {
+        case 1: return atax_kernel_ptr<1>(kmax);
+        case 2: return atax_kernel_ptr<2>(kmax);
+        case 4: return atax_kernel_ptr<4>(kmax);
+        case 8: return atax_kernel_ptr<8>(kmax);
+        case 16: return atax_kernel_ptr<16>(kmax);
+    }
+    return nullptr;
+}
+
+int fill_launch_config(const AtaxPlan &p, cudaLaunchConfig_t *cfg, cudaLaunchAttribute *attr,
+                       cudaStream_t stream)
+{
+    memset(cfg, 0, sizeof(*cfg));
+    cfg->gridDim = dim3((unsigned)(p.nclusters > 0 ? p.nclusters * p.C : p.C), 1, 1);
+    cfg->blockDim = dim3(kAtaxThreads, 1, 1);
+    cfg->dynamicSmemBytes = p.smem;
+    cfg->stream = stream;
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = (unsigned)p.C;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg->attrs = attr;
+    cfg->numAttrs = p.C > 1 ? 1 : 0;
+    return BTO_OK;
+}
+
+// Picks cluster size, per-thread column count, ring depth and the number of
+// co-resident clusters.  Leaves p->fn == nullptr when the fused kernel does not
+// apply (odd N / unaligned operands / a row too long for 16 CTAs).
+int plan_atax(DeviceCtx &c, const double *A, const double *x, long M, long N, AtaxPlan *p)
+{
+    p->fn = nullptr;
+    if (!g_tuning.atax_fused || (N % 2) || !aligned16(A) || !aligned16(x)) return BTO_OK;
+    int C = (int)g_tuning.atax_cluster;
+    if (C == 0) {
+        // smallest cluster whose per-CTA slice fits 8 double2 per thread (4096 columns)
+        C = 1;
+        while (C < 16 && (N + C - 1) / C > 4096) C *= 2;
+    }
+    long W = (N + C - 1) / C;
+    W += W & 1;
+    int kmax = 1;
+    while ((long)kmax * 2 * kThreads < W) kmax *= 2;
+    if (kmax > 16) return BTO_OK;
+    if ((long)(C - 1) * W >= N && C > 1) return BTO_OK;   // a CTA would own no column
+    AtaxKernel fn = atax_kernel_ptr(C, kmax);
+    if (!fn) return BTO_OK;
+    int rg = (16 / kmax) < kAtaxMaxRows ? (16 / kmax) : kAtaxMaxRows;
+    if (g_tuning.atax_rows > 0 && g_tuning.atax_rows < rg) rg = (int)g_tuning.atax_rows;
+    const size_t stage = (size_t)rg * W * sizeof(double);
+    cudaFuncAttributes fattr;
+    CUDA_TRY(cudaFuncGetAttributes(&fattr, fn));
+    // 227 KiB per CTA on sm_100, minus the kernel's static shared memory
+    const size_t budget = ((227 * 1024 - fattr.sharedSizeBytes) / 1024) * 1024;
+    int S = (int)(budget / stage);
+    if (S > 8) S = 8;
+    if (g_tuning.atax_stages > 0 && g_tuning.atax_stages < S) S = (int)g_tuning.atax_stages;
+    if (S < 3) return BTO_OK;           // lookahead 1 + one panel in flight
+    int L = S >= 5 ? 2 : 1;
+    if (g_tuning.atax_lookahead > 0) L = (int)g_tuning.atax_lookahead;
+    if (L > S - 2) L = S - 2;
+    if (L > 3) L = 3;
+    p->L = L;
+    p->C = C;
+    p->KMAX = kmax;
+    p->RG = rg;
+    p->W = (int)W;
+    p->S = S;
+    p->smem = stage * S;
+    auto it = c.max_clusters.find(reinterpret_cast<const void *>(fn));
+    if (it == c.max_clusters.end()) {
+        CUDA_TRY(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)budget));
+        if (C > 8) {
+            CUDA_TRY(cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+        }
+        int n = 0;
+        if (C > 1) {
+            AtaxPlan probe = *p;
+            probe.nclusters = c.sm_count / C;
+            probe.smem = budget;
+            cudaLaunchConfig_t cfg;
+            cudaLaunchAttribute attr[1];
+            fill_launch_config(probe, &cfg, attr, nullptr);
+            CUDA_TRY(cudaOccupancyMaxActiveClusters(&n, fn, &cfg));
+        } else {
+            n = c.sm_count;
+        }
+        if (n < 1) n = 1;
+        it = c.max_clusters.emplace(reinterpret_cast<const void *>(fn), n).first;
+    }
+    long ncl = it->second;
+    const long groups = (M + rg - 1) / rg;
+    if (ncl > groups) ncl = groups;
+    p->nclusters = (int)ncl;
+    p->fn = fn;
+    return BTO_OK;
+}
+
+int seq_atax_fused(DeviceCtx &c, const AtaxPlan &p, const double *A, const double *x,
+                   double *y, long M, long N, bool scaled, double beta, cudaStream_t st)
+{
+    WsLayout lay;
+    const size_t off = lay.take((size_t)p.nclusters * N);
+    BTO_TRY(size_ws(c, lay));
+    AtaxArgs a{};
+    a.A = A; a.x = x; a.M = M; a.N = N;
+    a.ypart = reinterpret_cast<double *>(c.ws + off);
+    a.W = p.W; a.stages = p.S; a.rows = p.RG; a.lookahead = p.L; a.nclusters = p.nclusters;
+    if (g_tuning.debug) {
+        fprintf(stderr, "[bto] atax fused: C=%d KMAX=%d rows=%d W=%d stages=%d lookahead=%d smem=%zu clusters=%d\n",
+                p.C, p.KMAX, p.RG, p.W, p.S, p.L, p.smem, p.nclusters);
+    }
+    cudaLaunchConfig_t cfg;
+    cudaLaunchAttribute attr[1];
+    fill_launch_config(p, &cfg, attr, st);
+    CUDA_TRY(cudaLaunchKernelEx(&cfg, p.fn, a));
+    BTO_TRY(check_launch("atax_cluster_kernel"));
+    // join the per-cluster partials in ascending cluster order
+    FinArgs f{};
+    f.colpart = a.ypart;
+    f.colout = y;
+    f.cmode = scaled ? kColScale : kColPlain;
+    f.cscale = beta;
+    f.N = N;
+    f.M = M;
+    f.strip_width = N;                 // one "strip": every column has the same contributors
+    f.units_per_strip = p.nclusters;   // owner(0) = 0, owner(U-1) = G-1 when U == G
+    f.total_units = p.nclusters;
+    f.grid = p.nclusters;
+    f.rmode = kRowNone;
+    f.col_blocks = (int)((N + kThreads - 1) / kThreads);
+    finalize_kernel<<<(unsigned)f.col_blocks, kThreads, 0, st>>>(f);
+    return check_launch("finalize_kernel");
+}
+
 // y = [beta *] A'(A x): pass 1 contracts t = A x into a workspace vector (it
 // never reaches the caller), pass 2 streams A again for A' t.
 int seq_atax(DeviceCtx &c, const double *A, const double *x, double *y, long M,
              long N, bool scaled, double beta, cudaStream_t st)
 {
     BTO_TRY(check_mn(M, N));
+    AtaxPlan fused;
+    BTO_TRY(plan_atax(c, A, x, M, N, &fused));
+    if (fused.fn) return seq_atax_fused(c, fused, A, x, y, M, N, scaled, beta, st);
     const bool al = mat_aligned(N, A);
     WsLayout lay;
     const size_t off_t = lay.take((size_t)M);
@@ -925,6 +1099,12 @@ static long *tuning_slot(const char *key)
     if (!strcmp(key, "grid_per_sm")) return &g_tuning.grid_per_sm;
     if (!strcmp(key, "vec_unroll")) return &g_tuning.vec_unroll;
     if (!strcmp(key, "vec_grid_per_sm")) return &g_tuning.vec_grid_per_sm;
+    if (!strcmp(key, "atax_fused")) return &g_tuning.atax_fused;
+    if (!strcmp(key, "atax_cluster")) return &g_tuning.atax_cluster;
+    if (!strcmp(key, "atax_stages")) return &g_tuning.atax_stages;
+    if (!strcmp(key, "atax_rows")) return &g_tuning.atax_rows;
+    if (!strcmp(key, "atax_lookahead")) return &g_tuning.atax_lookahead;
+    if (!strcmp(key, "debug")) return &g_tuning.debug;
     return nullptr;
 }
 
@@ -937,6 +1117,11 @@ int bto_set_tuning(const char *key, long value)
     if (slot == &g_tuning.mv_rows) ok = value == 8 || value == 16;
     if (slot == &g_tuning.mv_vec) ok = value == 1 || value == 2;
     if (slot == &g_tuning.vec_unroll) ok = value == 1 || value == 2 || value == 4;
+    if (slot == &g_tuning.atax_fused) ok = value == 0 || value == 1;
+    if (slot == &g_tuning.atax_cluster) ok = value == 0 || value == 1 || value == 2 || value == 4 || value == 8 || value == 16;
+    if (slot == &g_tuning.atax_stages) ok = value == 0 || (value >= 3 && value <= 8);
+    if (slot == &g_tuning.atax_lookahead) ok = value >= 0 && value <= 3;
+    if (slot == &g_tuning.atax_rows) ok = value >= 0 && value <= 8;
     if (slot == &g_tuning.grid_per_sm || slot == &g_tuning.vec_grid_per_sm) ok = value >= 0 && value <= 64;
     if (!ok) return fail(BTO_ERR_INVALID, "tuning %s=%ld is not supported", key, value);
     *slot = value;
