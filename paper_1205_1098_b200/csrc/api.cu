@@ -58,10 +58,10 @@ int fail(int code, const char *fmt, ...)
 // per-device context
 
 struct Tuning {
-    long mv_rows = 8;        // rows per unit (8 | 16)
-    long mv_vec = 2;         // double2 per thread per row (1 | 2)
-    long grid_per_sm = 0;    // CTAs per SM for the matrix kernels, 0 = occupancy
-    long vec_unroll = 4;     // independent double2 triples in flight (1 | 2 | 4)
+    long mv_rows = 0;        // rows per unit (0 = per-kind default | 8 | 16)
+    long mv_vec = 0;         // double2 per thread per row (0 = per-kind default | 1 | 2)
+    long grid_per_sm = 0;    // CTAs per SM for the matrix kernels (0 = per-kind default)
+    long vec_unroll = 2;     // independent double2 triples in flight (1 | 2 | 4)
     long vec_grid_per_sm = 0;
     long atax_fused = 1;     // 1: single-pass cluster kernel when applicable, 0: two passes
     long atax_cluster = 0;   // cluster size of the fused ATAX (0 = auto | 1 | 2 | 4 | 8 | 16)
@@ -253,10 +253,27 @@ MvKernel mv_kernel_ptr(int R, int V, bool aligned)
     return mv_tile_kernel<FLAGS, 8, 1, true>;
 }
 
+// Launch defaults per pass kind, from the B200 sweep at n = 32768
+// (profiles/r01/sweep_*.json): {rows per unit, double2 per thread, CTAs per SM
+// (0 = what the occupancy calculator allows)}.
+struct MvDefault { int rows, vec, grid_per_sm; };
+
+template <int FLAGS>
+constexpr MvDefault mv_default()
+{
+    if (FLAGS == (kFlagN | kFlagT)) return {16, 1, 0};       // BiCGK
+    if (FLAGS == (kFlagN | kFlagN2)) return {8, 1, 6};       // GESUMMV
+    if (FLAGS == (kFlagT | kFlagRank2)) return {8, 1, 8};    // GEMVER pass 1
+    if (FLAGS == kFlagT) return {16, 1, 6};                  // A' y
+    return {8, 1, 0};                                        // A x
+}
+
 template <int FLAGS>
 int plan_mv(DeviceCtx &c, long M, long N, bool aligned, MvPlan *p)
 {
-    int R = (int)g_tuning.mv_rows, V = (int)g_tuning.mv_vec;
+    constexpr MvDefault dflt = mv_default<FLAGS>();
+    int R = g_tuning.mv_rows ? (int)g_tuning.mv_rows : dflt.rows;
+    int V = g_tuning.mv_vec ? (int)g_tuning.mv_vec : dflt.vec;
     if (!aligned || (FLAGS & kFlagN2)) { R = 8; V = 1; }
     if (!((R == 8 && V == 1) || (R == 16 && V == 1) || (R == 8 && V == 2))) { R = 8; V = 1; }
     p->R = R;
@@ -269,7 +286,8 @@ int plan_mv(DeviceCtx &c, long M, long N, bool aligned, MvPlan *p)
     p->total_units = p->units_per_strip * p->nstrips;
     int occ = 1;
     BTO_TRY(occupancy_of(c, p->fn, &occ));
-    const long per_sm = g_tuning.grid_per_sm > 0 ? g_tuning.grid_per_sm : occ;
+    long per_sm = g_tuning.grid_per_sm > 0 ? g_tuning.grid_per_sm : dflt.grid_per_sm;
+    if (per_sm <= 0) per_sm = occ;
     long grid = (long)c.sm_count * per_sm;
     if (grid > p->total_units) grid = p->total_units;
     if (grid < 1) grid = 1;
@@ -1114,8 +1132,8 @@ int bto_set_tuning(const char *key, long value)
     long *slot = tuning_slot(key);
     if (!slot) return fail(BTO_ERR_INVALID, "unknown tuning key %s", key ? key : "(null)");
     bool ok = value >= 0;
-    if (slot == &g_tuning.mv_rows) ok = value == 8 || value == 16;
-    if (slot == &g_tuning.mv_vec) ok = value == 1 || value == 2;
+    if (slot == &g_tuning.mv_rows) ok = value == 0 || value == 8 || value == 16;
+    if (slot == &g_tuning.mv_vec) ok = value == 0 || value == 1 || value == 2;
     if (slot == &g_tuning.vec_unroll) ok = value == 1 || value == 2 || value == 4;
     if (slot == &g_tuning.atax_fused) ok = value == 0 || value == 1;
     if (slot == &g_tuning.atax_cluster) ok = value == 0 || value == 1 || value == 2 || value == 4 || value == 8 || value == 16;

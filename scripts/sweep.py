@@ -21,15 +21,45 @@ from bench import BENCH, SUITE, Suite, bytes_min, measured_peak  # noqa: E402
 from paper_1205_1098_b200 import _native  # noqa: E402
 
 
+PIECES = ("gemver_pass1", "gemver_pass2", "tonly", "dgemv")
+PIECE_BYTES = {"gemver_pass1": 16.0, "gemver_pass2": 8.0, "tonly": 8.0, "dgemv": 8.0}
+
+
+def launch_piece(suite, name):
+    """Single passes of the matrix engine on the suite's buffers (n = 32768)."""
+    import ctypes
+    lib, n = _native.load(), suite.n
+    P = lambda t: ctypes.c_void_p(t.data_ptr())
+    st = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+    if name == "gemver_pass1":
+        rc = lib.bto_gemver_pass1_async(P(suite.A), P(suite.vecM[1]), P(suite.vecN[1]),
+                                        P(suite.vecM[2]), P(suite.vecN[2]), P(suite.vecM[0]),
+                                        P(suite.Bm), P(suite.colsum), n, n, st)
+    elif name == "tonly":
+        rc = lib.bto_gemver_pass1_async(P(suite.A), None, None, None, None, P(suite.vecM[0]),
+                                        None, P(suite.colsum), n, n, st)
+    elif name == "gemver_pass2":
+        rc = lib.bto_gemver_pass2_async(P(suite.Bm), P(suite.vecN[0]), 0.5, P(suite.w), n, n, st)
+    else:
+        rc = lib.bto_dgemv_async(0.5, P(suite.A), P(suite.vecN[0]), 0.25, P(suite.vecM[0]),
+                                 P(suite.w), n, n, st)
+    _native.check(rc)
+
+
 def time_kernel(suite, name, reps):
+    if name in PIECES:
+        orig = suite.launch
+        launch = lambda _n: launch_piece(suite, name)
+    else:
+        launch = suite.launch
     for _ in range(3):
-        suite.launch(name)
+        launch(name)
     torch.cuda.synchronize()
     evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
            for _ in range(reps)]
     for a, b in evs:
         a.record()
-        suite.launch(name)
+        launch(name)
         b.record()
     torch.cuda.synchronize()
     ms = [a.elapsed_time(b) for a, b in evs]
@@ -46,7 +76,7 @@ def main():
     kernels = tuple(args.kernels.split(","))
     torch.cuda.set_device(0)
     _native.load()
-    suite = Suite(torch, 0, 1, kernels)
+    suite = Suite(torch, 0, 1, tuple(k for k in kernels if k not in PIECES) or ("gemver",))
     peak, _ = measured_peak()
     rows = []
     mv_cfgs = [(8, 1), (16, 1), (8, 2)]
@@ -65,12 +95,13 @@ def main():
             except Exception as exc:
                 print(name, cfg, "FAILED", exc)
                 continue
-            gbs = bytes_min(name, *BENCH[name]) / (med * 1e-3) / 1e9
+            nbytes = PIECE_BYTES[name] * 32768.0 ** 2 if name in PIECES else bytes_min(name, *BENCH[name])
+            gbs = nbytes / (med * 1e-3) / 1e9
             rows.append({"kernel": name, **cfg, "ms_median": med, "ms_min": best,
                          "gbs": gbs, "frac": gbs / peak})
             print(f"{name:8s} {cfg} median {med:8.4f} ms  min {best:8.4f} ms  "
                   f"{gbs:7.1f} GB/s  {100 * gbs / peak:5.1f}%", flush=True)
-        _native.set_tuning(mv_rows=8, mv_vec=2, grid_per_sm=0, vec_unroll=4, vec_grid_per_sm=0)
+        _native.set_tuning(mv_rows=0, mv_vec=0, grid_per_sm=0, vec_unroll=2, vec_grid_per_sm=0)
     Path(args.out).parent.mkdir(exist_ok=True)
     Path(args.out).write_text(json.dumps(rows, indent=1))
 

@@ -59,7 +59,7 @@ def test_bytes_min_formulas():
 
 
 def test_tuning_keys_are_validated():
-    assert _native.get_tuning("mv_rows") in (8, 16)
+    assert _native.get_tuning("mv_rows") in (0, 8, 16)
     assert _native.get_tuning("no_such_key") == -1
     with pytest.raises(_native.BtoError):
         _native.set_tuning(mv_rows=5)

@@ -123,6 +123,47 @@ def test_every_tile_variant(bto_lib, oracle, rows, vec):
         _native.set_tuning(mv_rows=old[0], mv_vec=old[1])
 
 
+ATAX_SHAPES = [(2048, 1024), (8, 2), (1, 4096), (100, 514), (333, 8192), (64, 16390),
+               (1000, 4098), (37, 32768), (5000, 1026)]
+
+
+@pytest.mark.parametrize("cluster", [0, 1, 2, 4, 8, 16])
+def test_fused_atax_every_cluster_size(bto_lib, oracle, cluster):
+    """Single-pass ATAX/BATAX (cluster-resident row panels, TMA ring, st.async
+    exchange): every cluster size, ring depth, panel height and lookahead must
+    give the oracle's result; shapes include slices that leave the last CTA of
+    the cluster short, fewer rows than clusters, and a single row."""
+    try:
+        for (m, n) in ATAX_SHAPES:
+            ext = {"M": m, "N": n}
+            for name in ("atax", "batax"):
+                graph = bto.load_graph(name)
+                inputs = bto.gen_inputs(graph, ext, seed=m + n)
+                want = oracle.oracle_run(name, inputs, ext, threads=8)
+                for stages, rows, look in ((0, 0, 0), (3, 0, 1), (0, 1, 3), (4, 1, 2)):
+                    _native.set_tuning(atax_fused=1, atax_cluster=cluster, atax_stages=stages,
+                                       atax_rows=rows, atax_lookahead=look)
+                    assert_matches(name, run_device(name, inputs, ext), want, ext,
+                                   f"C{cluster} S{stages} R{rows} L{look}")
+    finally:
+        _native.set_tuning(atax_fused=1, atax_cluster=0, atax_stages=0, atax_rows=0,
+                           atax_lookahead=0)
+
+
+def test_two_pass_atax_fallback(bto_lib, oracle):
+    """Odd N (rows not 16-byte aligned) and atax_fused=0 take the two-pass path."""
+    try:
+        for fused, (m, n) in ((1, (301, 1001)), (0, (2048, 1024)), (0, (700, 4100))):
+            _native.set_tuning(atax_fused=fused)
+            ext = {"M": m, "N": n}
+            graph = bto.load_graph("atax")
+            inputs = bto.gen_inputs(graph, ext, seed=5)
+            want = oracle.oracle_run("atax", inputs, ext, threads=8)
+            assert_matches("atax", run_device("atax", inputs, ext), want, ext, f"fused={fused}")
+    finally:
+        _native.set_tuning(atax_fused=1)
+
+
 @pytest.mark.parametrize("grid_per_sm", [1, 3, 16])
 def test_grid_size_only_changes_reduction_order(bto_lib, oracle, grid_per_sm):
     try:
