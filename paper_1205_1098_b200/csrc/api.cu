@@ -61,6 +61,7 @@ struct Tuning {
     long mv_rows = 0;        // rows per unit (0 = per-kind default | 8 | 16)
     long mv_vec = 0;         // double2 per thread per row (0 = per-kind default | 1 | 2)
     long grid_per_sm = 0;    // CTAs per SM for the matrix kernels (0 = per-kind default)
+    long mv_minb = 0;        // __launch_bounds__ min CTAs/SM variant (0 = default | 1 2 3 4 6)
     long vec_unroll = 2;     // independent double2 triples in flight (1 | 2 | 4)
     long vec_grid_per_sm = 0;
     long atax_fused = 1;     // 1: single-pass cluster kernel when applicable, 0: two passes
@@ -242,30 +243,60 @@ struct MvPlan {
     MvKernel fn = nullptr;
 };
 
-template <int FLAGS>
-MvKernel mv_kernel_ptr(int R, int V, bool aligned)
+template <int FLAGS, int R, int V>
+MvKernel mv_kernel_minb(int minb)
 {
-    if (!aligned) return mv_tile_kernel<FLAGS, 8, 1, false>;
-    if constexpr ((FLAGS & kFlagN2) == 0) {   // two matrices: keep the tile small
-        if (R == 16 && V == 1) return mv_tile_kernel<FLAGS, 16, 1, true>;
-        if (R == 8 && V == 2) return mv_tile_kernel<FLAGS, 8, 2, true>;
+    switch (minb) {
+        case 2: return mv_tile_kernel<FLAGS, R, V, true, 2>;
+        case 3: return mv_tile_kernel<FLAGS, R, V, true, 3>;
+        case 4: return mv_tile_kernel<FLAGS, R, V, true, 4>;
+        case 6: return mv_tile_kernel<FLAGS, R, V, true, 6>;
+        default: return mv_tile_kernel<FLAGS, R, V, true, 1>;
     }
-    return mv_tile_kernel<FLAGS, 8, 1, true>;
+}
+
+// Supported tile shapes: (rows, double2 per thread) = (8,1) always; (16,1) for
+// single-matrix kinds; (32,1) for kinds without row dots; (8,2) for A x alone.
+template <int FLAGS>
+bool mv_shape_ok(int R, int V)
+{
+    if (R == 8 && V == 1) return true;
+    if (FLAGS & kFlagN2) return false;
+    if (R == 16 && V == 1) return true;
+    if (R == 32 && V == 1) return (FLAGS & kFlagN) == 0;
+    if (R == 8 && V == 2) return FLAGS == kFlagN;
+    return false;
+}
+
+template <int FLAGS>
+MvKernel mv_kernel_ptr(int R, int V, bool aligned, int minb)
+{
+    if (!aligned) return mv_tile_kernel<FLAGS, 8, 1, false, 1>;
+    if constexpr ((FLAGS & kFlagN2) == 0) {
+        if (R == 16 && V == 1) return mv_kernel_minb<FLAGS, 16, 1>(minb);
+        if constexpr ((FLAGS & kFlagN) == 0) {
+            if (R == 32 && V == 1) return mv_kernel_minb<FLAGS, 32, 1>(minb);
+        }
+        if constexpr (FLAGS == kFlagN) {
+            if (R == 8 && V == 2) return mv_kernel_minb<FLAGS, 8, 2>(minb);
+        }
+    }
+    return mv_kernel_minb<FLAGS, 8, 1>(minb);
 }
 
 // Launch defaults per pass kind, from the B200 sweep at n = 32768
-// (profiles/r01/sweep_*.json): {rows per unit, double2 per thread, CTAs per SM
+// (profiles/r01/sweep2_passes.json): {rows per unit, double2 per thread, CTAs per SM
 // (0 = what the occupancy calculator allows)}.
-struct MvDefault { int rows, vec, grid_per_sm; };
+struct MvDefault { int rows, vec, grid_per_sm, minb; };
 
 template <int FLAGS>
 constexpr MvDefault mv_default()
 {
-    if (FLAGS == (kFlagN | kFlagT)) return {16, 1, 0};       // BiCGK
-    if (FLAGS == (kFlagN | kFlagN2)) return {8, 1, 6};       // GESUMMV
-    if (FLAGS == (kFlagT | kFlagRank2)) return {8, 1, 8};    // GEMVER pass 1
-    if (FLAGS == kFlagT) return {16, 1, 6};                  // A' y
-    return {8, 1, 0};                                        // A x
+    if (FLAGS == (kFlagN | kFlagT)) return {8, 1, 8, 4};        // BiCGK         7.10 TB/s
+    if (FLAGS == (kFlagN | kFlagN2)) return {8, 1, 4, 4};       // GESUMMV       7.04 TB/s
+    if (FLAGS == (kFlagT | kFlagRank2)) return {16, 1, 2, 1};   // GEMVER pass 1 6.29 TB/s (r+w)
+    if (FLAGS == kFlagT) return {32, 1, 2, 1};                  // A' y          7.17 TB/s
+    return {8, 2, 8, 2};                                        // A x           7.20 TB/s
 }
 
 template <int FLAGS>
@@ -274,12 +305,12 @@ int plan_mv(DeviceCtx &c, long M, long N, bool aligned, MvPlan *p)
     constexpr MvDefault dflt = mv_default<FLAGS>();
     int R = g_tuning.mv_rows ? (int)g_tuning.mv_rows : dflt.rows;
     int V = g_tuning.mv_vec ? (int)g_tuning.mv_vec : dflt.vec;
-    if (!aligned || (FLAGS & kFlagN2)) { R = 8; V = 1; }
-    if (!((R == 8 && V == 1) || (R == 16 && V == 1) || (R == 8 && V == 2))) { R = 8; V = 1; }
+    int minb = g_tuning.mv_minb ? (int)g_tuning.mv_minb : dflt.minb;
+    if (!aligned || !mv_shape_ok<FLAGS>(R, V)) { R = 8; V = 1; }
     p->R = R;
     p->V = V;
     p->aligned = aligned;
-    p->fn = mv_kernel_ptr<FLAGS>(R, V, aligned);
+    p->fn = mv_kernel_ptr<FLAGS>(R, V, aligned, minb);
     p->strip_width = (long)kThreads * 2 * V;
     p->nstrips = (int)((N + p->strip_width - 1) / p->strip_width);
     p->units_per_strip = (M + R - 1) / R;
@@ -1115,6 +1146,7 @@ static long *tuning_slot(const char *key)
     if (!strcmp(key, "mv_rows")) return &g_tuning.mv_rows;
     if (!strcmp(key, "mv_vec")) return &g_tuning.mv_vec;
     if (!strcmp(key, "grid_per_sm")) return &g_tuning.grid_per_sm;
+    if (!strcmp(key, "mv_minb")) return &g_tuning.mv_minb;
     if (!strcmp(key, "vec_unroll")) return &g_tuning.vec_unroll;
     if (!strcmp(key, "vec_grid_per_sm")) return &g_tuning.vec_grid_per_sm;
     if (!strcmp(key, "atax_fused")) return &g_tuning.atax_fused;
@@ -1132,7 +1164,8 @@ int bto_set_tuning(const char *key, long value)
     long *slot = tuning_slot(key);
     if (!slot) return fail(BTO_ERR_INVALID, "unknown tuning key %s", key ? key : "(null)");
     bool ok = value >= 0;
-    if (slot == &g_tuning.mv_rows) ok = value == 0 || value == 8 || value == 16;
+    if (slot == &g_tuning.mv_rows) ok = value == 0 || value == 8 || value == 16 || value == 32;
+    if (slot == &g_tuning.mv_minb) ok = value == 0 || value == 1 || value == 2 || value == 3 || value == 4 || value == 6;
     if (slot == &g_tuning.mv_vec) ok = value == 0 || value == 1 || value == 2;
     if (slot == &g_tuning.vec_unroll) ok = value == 1 || value == 2 || value == 4;
     if (slot == &g_tuning.atax_fused) ok = value == 0 || value == 1;

@@ -20,10 +20,19 @@ constexpr unsigned kFullMask = 0xffffffffu;
 // ---- streaming global loads / stores ---------------------------------------
 // .nc + L1::no_allocate: read-once data must not evict the small vectors
 // (weights, x) that do get re-used from L1.
+#ifndef BTO_LOAD_POLICY
+#define BTO_LOAD_POLICY 0
+#endif
 __device__ __forceinline__ double2 ld_stream2(const double *p)   // 16 B aligned
 {
     double2 v;
+#if BTO_LOAD_POLICY == 0
     asm("ld.global.nc.L1::no_allocate.v2.f64 {%0, %1}, [%2];"
+#elif BTO_LOAD_POLICY == 1
+    asm("ld.global.nc.L1::no_allocate.L2::evict_first.v2.f64 {%0, %1}, [%2];"
+#else
+    asm("ld.global.nc.v2.f64 {%0, %1}, [%2];"
+#endif
         : "=d"(v.x), "=d"(v.y) : "l"(p));
     return v;
 }
@@ -35,10 +44,22 @@ __device__ __forceinline__ double ld_stream1(const double *p)
     return v;
 }
 
-// evict-first stores for write-once outputs (z, B)
+// stores for write-once outputs (z, B); BTO_STORE_POLICY picks the cache
+// operator: 0 = .cs (evict-first), 1 = default write-back, 2 = .wt, 3 = .cg
+#ifndef BTO_STORE_POLICY
+#define BTO_STORE_POLICY 0
+#endif
 __device__ __forceinline__ void st_stream2(double *p, double2 v)   // 16 B aligned
 {
+#if BTO_STORE_POLICY == 0
     asm volatile("st.global.cs.v2.f64 [%0], {%1, %2};"
+#elif BTO_STORE_POLICY == 1
+    asm volatile("st.global.v2.f64 [%0], {%1, %2};"
+#elif BTO_STORE_POLICY == 2
+    asm volatile("st.global.wt.v2.f64 [%0], {%1, %2};"
+#else
+    asm volatile("st.global.cg.v2.f64 [%0], {%1, %2};"
+#endif
                  :: "l"(p), "d"(v.x), "d"(v.y) : "memory");
 }
 

@@ -166,8 +166,11 @@ __device__ __forceinline__ void mv_unit(const MvArgs &a, StripState<V> &st, long
     }
 }
 
-template <int FLAGS, int R, int V, bool ALIGNED>
-__global__ void __launch_bounds__(kThreads)
+// MINB: minimum resident CTAs per SM the register allocator must leave room
+// for (__launch_bounds__); trades registers per thread (loads in flight per
+// thread) against warps per SM.
+template <int FLAGS, int R, int V, bool ALIGNED, int MINB>
+__global__ void __launch_bounds__(kThreads, MINB)
 mv_tile_kernel(const MvArgs a)
 {
     constexpr bool kN = (FLAGS & kFlagN) != 0;

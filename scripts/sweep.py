@@ -79,15 +79,19 @@ def main():
     suite = Suite(torch, 0, 1, tuple(k for k in kernels if k not in PIECES) or ("gemver",))
     peak, _ = measured_peak()
     rows = []
-    mv_cfgs = [(8, 1), (16, 1), (8, 2)]
-    grids = [0, 1, 2, 3, 4, 6, 8] if not args.quick else [0, 2, 4]
+    mv_cfgs = [(8, 1), (16, 1), (32, 1), (8, 2)]
+    grids = [0, 2, 4, 8, 16] if not args.quick else [0, 4]
+    minbs = [1, 2, 3, 4, 6] if not args.quick else [1, 3]
     for name in kernels:
         if name == "axpydot":
             cfgs = [dict(vec_unroll=u, vec_grid_per_sm=g)
                     for u, g in itertools.product([1, 2, 4], [0, 2, 4, 8, 16])]
         else:
-            cfgs = [dict(mv_rows=r, mv_vec=v, grid_per_sm=g)
-                    for (r, v), g in itertools.product(mv_cfgs, grids)]
+            cfgs = [dict(mv_rows=r, mv_vec=v, grid_per_sm=g, mv_minb=b)
+                    for (r, v), g, b in itertools.product(mv_cfgs, grids, minbs)]
+            if name == "atax":
+                cfgs = [dict(atax_cluster=c, atax_rows=r, atax_lookahead=l)
+                        for c, r, l in itertools.product([4, 8], [0, 1], [1, 2])]
         for cfg in cfgs:
             _native.set_tuning(**cfg)
             try:
@@ -101,7 +105,8 @@ def main():
                          "gbs": gbs, "frac": gbs / peak})
             print(f"{name:8s} {cfg} median {med:8.4f} ms  min {best:8.4f} ms  "
                   f"{gbs:7.1f} GB/s  {100 * gbs / peak:5.1f}%", flush=True)
-        _native.set_tuning(mv_rows=0, mv_vec=0, grid_per_sm=0, vec_unroll=2, vec_grid_per_sm=0)
+        _native.set_tuning(mv_rows=0, mv_vec=0, grid_per_sm=0, mv_minb=0, vec_unroll=2, vec_grid_per_sm=0,
+                           atax_cluster=0, atax_rows=0, atax_lookahead=0)
     Path(args.out).parent.mkdir(exist_ok=True)
     Path(args.out).write_text(json.dumps(rows, indent=1))
 
