@@ -227,6 +227,37 @@ def test_bad_extents_are_errors(bto_lib):
         _native.check(rc)
 
 
+def test_reference_style_ctypes_binding(bto_lib, oracle):
+    """Bind the library the way the reference's loader does (runtime.py:99-150):
+    raw CDLL, symbol by kernel name, POINTER(c_double) numpy buffers, c_double
+    scalars, c_long extents, restype None, NaN-prefilled outputs."""
+    import ctypes
+    lib = ctypes.CDLL(str(bto.library_path()))
+    g = bto.load_graph("gemver")
+    ext = {"M": 123, "N": 310}
+    inputs = bto.gen_inputs(g, ext, seed=4)
+    fn = getattr(lib, g.spec.name.lower())
+    fn.restype = None
+    dp = ctypes.POINTER(ctypes.c_double)
+    args, keep, outs = [], [], {}
+    for name, decl in g.spec.inputs:
+        if decl.kind == "scalar":
+            args.append(ctypes.c_double(inputs[name]))
+        else:
+            flat = np.ascontiguousarray(inputs[name].ravel())
+            keep.append(flat)
+            args.append(flat.ctypes.data_as(dp))
+    for name, decl in g.spec.outputs:
+        buf = np.full(int(np.prod([ext[d] for d in g.dims[name]])), np.nan)
+        outs[name] = buf
+        args.append(buf.ctypes.data_as(dp))
+    args += [ctypes.c_long(ext[e]) for e in g.extent_names]
+    fn(*args)
+    assert lib.bto_last_error() == 0
+    got = {n: outs[n].reshape([ext[d] for d in g.dims[n]]) for n in outs}
+    assert_matches("gemver", got, oracle.oracle_run("gemver", inputs, ext, threads=8), ext)
+
+
 def test_known_answers_on_gpu(bto_lib):
     # the reference's own KATs (tests/test_codegen.py:46-59)
     out = run_host("batax", {"A": np.eye(3), "x": np.array([1.0, 2.0, 3.0]), "beta": 2.0},
