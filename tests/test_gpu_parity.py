@@ -227,6 +227,38 @@ def test_bad_extents_are_errors(bto_lib):
         _native.check(rc)
 
 
+def test_host_operand_pipeline(bto_lib, oracle):
+    """Host buffers above the streaming threshold go through the panel pipeline
+    (copy-in / compute / copy-out on three streams): GEMVER and AXPYDOT, many
+    small panels, pageable and pinned memory, odd lengths, more panels than rows."""
+    try:
+        for panel_mib, (m, n) in ((1, (2100, 2050)), (8, (2048, 2048)), (1, (3, 1500000))):
+            _native.set_tuning(host_pipeline=1, host_panel_mib=panel_mib)
+            ext = {"M": m, "N": n}
+            g = bto.load_graph("gemver")
+            inputs = bto.gen_inputs(g, ext, seed=m)
+            want = oracle.oracle_run("gemver", inputs, ext, threads=8)
+            assert_matches("gemver", run_host("gemver", inputs, ext), want, ext, f"panels {panel_mib} MiB")
+            pinned = {k: (torch.from_numpy(v).pin_memory().numpy() if isinstance(v, np.ndarray) else v)
+                      for k, v in inputs.items()}
+            assert_matches("gemver", run_host("gemver", pinned, ext), want, ext, "pinned")
+        for panel_mib, k in ((1, 5000001), (4, 1 << 22), (256, (1 << 22) + 2)):
+            _native.set_tuning(host_pipeline=1, host_panel_mib=panel_mib)
+            g = bto.load_graph("axpydot")
+            inputs = bto.gen_inputs(g, {"M": k}, seed=k % 97)
+            want = oracle.oracle_run("axpydot", inputs, {"M": k}, threads=8)
+            assert_matches("axpydot", run_host("axpydot", inputs, {"M": k}), want, {"M": k},
+                           f"chunks {panel_mib} MiB")
+        _native.set_tuning(host_pipeline=0)
+        ext = {"M": 2100, "N": 2050}
+        g = bto.load_graph("gemver")
+        inputs = bto.gen_inputs(g, ext, seed=1)
+        assert_matches("gemver", run_host("gemver", inputs, ext),
+                       oracle.oracle_run("gemver", inputs, ext, threads=8), ext, "unpipelined")
+    finally:
+        _native.set_tuning(host_pipeline=1, host_panel_mib=256)
+
+
 def test_reference_style_ctypes_binding(bto_lib, oracle):
     """Bind the library the way the reference's loader does (runtime.py:99-150):
     raw CDLL, symbol by kernel name, POINTER(c_double) numpy buffers, c_double
