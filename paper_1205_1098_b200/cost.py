@@ -406,8 +406,8 @@ def variant_space(kernel: str) -> list[GpuVariant]:
                 for u in (1, 2, 4) for g in (0, 4, 8, 16)]
     out = []
     if kernel in ("atax", "batax"):
-        out += [GpuVariant(kernel, (("atax_fused", 1), ("atax_cluster", c), ("atax_lookahead", l)))
-                for c in (0, 4, 8) for l in (1, 2)]
+        out += [GpuVariant(kernel, (("atax_fused", 1), ("atax_cluster", c), ("atax_rows", r)))
+                for c in (0, 4, 8) for r in (0, 1)]
         out.append(GpuVariant(kernel, (("atax_fused", 0),)))
         return out
     for rows, vec in ((8, 1), (16, 1), (8, 2)):

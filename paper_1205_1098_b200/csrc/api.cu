@@ -67,8 +67,7 @@ struct Tuning {
     long atax_fused = 1;     // 1: single-pass cluster kernel when applicable, 0: two passes
     long atax_cluster = 0;   // cluster size of the fused ATAX (0 = auto | 1 | 2 | 4 | 8 | 16)
     long atax_stages = 0;    // TMA ring depth (0 = as many as fit, at most 8)
-    long atax_rows = 0;      // rows per panel (0 = auto)
-    long atax_lookahead = 0; // panels phase 1 runs ahead of phase 2 (0 = auto | 1..3)
+    long atax_rows = 0;      // 0: 16 double2 per thread per panel, 1: half-height panels
     long debug = 0;          // print launch plans to stderr
     long host_pipeline = 1;  // overlap H2D / compute / D2H in row panels for host operands
     long host_panel_mib = 256;   // panel size of that pipeline
@@ -476,32 +475,41 @@ using AtaxKernel = void (*)(const AtaxArgs);
 
 struct AtaxPlan {
     AtaxKernel fn = nullptr;     // nullptr: not applicable, use the two-pass sequence
-    int C = 1, KMAX = 1, RG = 1, W = 0, S = 0, L = 1;
+    int C = 1, KMAX = 1, RG = 1, W = 0, S = 0;
     size_t smem = 0;
     int nclusters = 0;
 };
 
+// TR (rows per panel) is 16 / KMAX capped at 8: a panel is 16 double2 per thread.
+// `small` halves it (fewer registers per tile, more panels per byte).
 template <int C>
-AtaxKernel atax_kernel_ptr(int kmax)
+AtaxKernel atax_kernel_ptr(int kmax, bool small)
 {
     switch (kmax) {
-        case 1: return atax_cluster_kernel<C, 1>;
-        case 2: return atax_cluster_kernel<C, 2>;
-        case 4: return atax_cluster_kernel<C, 4>;
-        case 8: return atax_cluster_kernel<C, 8>;
-        case 16: return atax_cluster_kernel<C, 16>;
+        case 1: return small ? atax_cluster_kernel<C, 1, 4> : atax_cluster_kernel<C, 1, 8>;
+        case 2: return small ? atax_cluster_kernel<C, 2, 4> : atax_cluster_kernel<C, 2, 8>;
+        case 4: return small ? atax_cluster_kernel<C, 4, 2> : atax_cluster_kernel<C, 4, 4>;
+        case 8: return small ? atax_cluster_kernel<C, 8, 1> : atax_cluster_kernel<C, 8, 2>;
+        case 16: return atax_cluster_kernel<C, 16, 1>;
     }
     return nullptr;
 }
 
-AtaxKernel atax_kernel_ptr(int c, int kmax)
+int atax_rows_of(int kmax, bool small)
+{
+    const int full = (16 / kmax) < kAtaxMaxRows ? (16 / kmax) : kAtaxMaxRows;
+    if (!small || kmax == 16) return full;
+    return kmax == 1 ? 4 : full / 2;
+}
+
+AtaxKernel atax_kernel_ptr(int c, int kmax, bool small)
 {
     switch (c) {
-        case 1: return atax_kernel_ptr<1>(kmax);
-        case 2: return atax_kernel_ptr<2>(kmax);
-        case 4: return atax_kernel_ptr<4>(kmax);
-        case 8: return atax_kernel_ptr<8>(kmax);
-        case 16: return atax_kernel_ptr<16>(kmax);
+        case 1: return atax_kernel_ptr<1>(kmax, small);
+        case 2: return atax_kernel_ptr<2>(kmax, small);
+        case 4: return atax_kernel_ptr<4>(kmax, small);
+        case 8: return atax_kernel_ptr<8>(kmax, small);
+        case 16: return atax_kernel_ptr<16>(kmax, small);
     }
     return nullptr;
 }
@@ -542,10 +550,10 @@ int plan_atax(DeviceCtx &c, const double *A, const double *x, long M, long N, At
     while ((long)kmax * 2 * kThreads < W) kmax *= 2;
     if (kmax > 16) return BTO_OK;
     if ((long)(C - 1) * W >= N && C > 1) return BTO_OK;   // a CTA would own no column
-    AtaxKernel fn = atax_kernel_ptr(C, kmax);
+    const bool small = g_tuning.atax_rows == 1;     // 1: half-height panels
+    AtaxKernel fn = atax_kernel_ptr(C, kmax, small);
     if (!fn) return BTO_OK;
-    int rg = (16 / kmax) < kAtaxMaxRows ? (16 / kmax) : kAtaxMaxRows;
-    if (g_tuning.atax_rows > 0 && g_tuning.atax_rows < rg) rg = (int)g_tuning.atax_rows;
+    const int rg = atax_rows_of(kmax, small);
     const size_t stage = (size_t)rg * W * sizeof(double);
     cudaFuncAttributes fattr;
     CUDA_TRY(cudaFuncGetAttributes(&fattr, fn));
@@ -554,12 +562,7 @@ int plan_atax(DeviceCtx &c, const double *A, const double *x, long M, long N, At
     int S = (int)(budget / stage);
     if (S > 8) S = 8;
     if (g_tuning.atax_stages > 0 && g_tuning.atax_stages < S) S = (int)g_tuning.atax_stages;
-    if (S < 3) return BTO_OK;           // lookahead 1 + one panel in flight
-    int L = S >= 5 ? 2 : 1;
-    if (g_tuning.atax_lookahead > 0) L = (int)g_tuning.atax_lookahead;
-    if (L > S - 2) L = S - 2;
-    if (L > 3) L = 3;
-    p->L = L;
+    if (S < 2) return BTO_OK;
     p->C = C;
     p->KMAX = kmax;
     p->RG = rg;
@@ -605,10 +608,10 @@ int seq_atax_fused(DeviceCtx &c, const AtaxPlan &p, const double *A, const doubl
     AtaxArgs a{};
     a.A = A; a.x = x; a.M = M; a.N = N;
     a.ypart = reinterpret_cast<double *>(c.ws + off);
-    a.W = p.W; a.stages = p.S; a.rows = p.RG; a.lookahead = p.L; a.nclusters = p.nclusters;
+    a.W = p.W; a.stages = p.S; a.nclusters = p.nclusters;
     if (g_tuning.debug) {
-        fprintf(stderr, "[bto] atax fused: C=%d KMAX=%d rows=%d W=%d stages=%d lookahead=%d smem=%zu clusters=%d\n",
-                p.C, p.KMAX, p.RG, p.W, p.S, p.L, p.smem, p.nclusters);
+        fprintf(stderr, "[bto] atax fused: C=%d KMAX=%d rows=%d W=%d stages=%d smem=%zu clusters=%d\n",
+                p.C, p.KMAX, p.RG, p.W, p.S, p.smem, p.nclusters);
     }
     cudaLaunchConfig_t cfg;
     cudaLaunchAttribute attr[1];
@@ -1365,7 +1368,6 @@ static long *tuning_slot(const char *key)
     if (!strcmp(key, "atax_cluster")) return &g_tuning.atax_cluster;
     if (!strcmp(key, "atax_stages")) return &g_tuning.atax_stages;
     if (!strcmp(key, "atax_rows")) return &g_tuning.atax_rows;
-    if (!strcmp(key, "atax_lookahead")) return &g_tuning.atax_lookahead;
     if (!strcmp(key, "debug")) return &g_tuning.debug;
     if (!strcmp(key, "host_pipeline")) return &g_tuning.host_pipeline;
     if (!strcmp(key, "host_panel_mib")) return &g_tuning.host_panel_mib;
@@ -1385,9 +1387,8 @@ int bto_set_tuning(const char *key, long value)
     if (slot == &g_tuning.atax_fused || slot == &g_tuning.host_pipeline) ok = value == 0 || value == 1;
     if (slot == &g_tuning.host_panel_mib) ok = value >= 1 && value <= 4096;
     if (slot == &g_tuning.atax_cluster) ok = value == 0 || value == 1 || value == 2 || value == 4 || value == 8 || value == 16;
-    if (slot == &g_tuning.atax_stages) ok = value == 0 || (value >= 3 && value <= 8);
-    if (slot == &g_tuning.atax_lookahead) ok = value >= 0 && value <= 3;
-    if (slot == &g_tuning.atax_rows) ok = value >= 0 && value <= 8;
+    if (slot == &g_tuning.atax_stages) ok = value == 0 || (value >= 2 && value <= 8);
+    if (slot == &g_tuning.atax_rows) ok = value == 0 || value == 1;
     if (slot == &g_tuning.grid_per_sm || slot == &g_tuning.vec_grid_per_sm) ok = value >= 0 && value <= 64;
     if (!ok) return fail(BTO_ERR_INVALID, "tuning %s=%ld is not supported", key, value);
     *slot = value;

@@ -14,14 +14,23 @@
 //            shuffle -> shared memory) and PUSHES its partial sums into the
 //            shared memory of every CTA of the cluster with st.async, which
 //            counts the bytes on the RECEIVER's mbarrier for that panel;
-//   phase 2  L panels later (software pipeline: the exchange latency is hidden
-//            behind L iterations of work, no lock-step cluster barrier) every
-//            CTA waits on its own mbarrier, adds the C partials in rank order
-//            (t_i, identical bits in all CTAs), then y[j] += A[i,j] * t_i from
-//            the SAME shared-memory tile, column sums living in registers for
-//            the whole kernel.
-// A ninth warp is the TMA producer: it refills a stage as soon as the eight
-// consumer warps have released it (an "empty" mbarrier per stage).
+//            the tile is read from shared memory ONCE, into registers, and the
+//            stage goes back to the producer right away;
+//   phase 2  one panel later (software pipeline: the exchange latency hides
+//            behind the next panel's phase 1, no lock-step cluster barrier)
+//            every CTA waits on its own mbarrier, adds the C partials in rank
+//            order (t_i, identical bits in all CTAs), then y[j] += A[i,j] * t_i
+//            from the tile it still holds in REGISTERS; column sums live in
+//            registers for the whole kernel.
+// Thread 0 issues the TMA copies: phase 1 ends with a CTA barrier after every
+// warp has its part of the tile in registers, so right after that barrier the
+// stage is free and is refilled with the panel S steps ahead (no "empty"
+// mbarrier, and no extra warp -- a ninth warp would cap the kernel at 168
+// registers per thread, too few for two register tiles).
+// Shared-memory reads are 8 bytes per matrix byte-pair less than a two-touch
+// scheme would need, which matters because under the 1 kW power cap the SM
+// clock drops to ~1.75 GHz and the per-panel latency chain is what bounds the
+// kernel (profiles/r01/drift_probe.log).
 //
 // HBM traffic is therefore 8*M*N bytes + the y partials (one N-vector per
 // cluster), the algorithmic minimum of SURVEY.md section 8d.  Clusters take
@@ -39,8 +48,6 @@ struct AtaxArgs {
     long M, N;
     int W;               // columns per CTA (even)
     int stages;          // ring depth S
-    int rows;            // rows per panel (<= the kernel's RG bound)
-    int lookahead;       // L: phase 1 runs L panels ahead of phase 2 (1..3, <= stages-2)
     int nclusters;
 };
 
@@ -48,7 +55,7 @@ constexpr int kAtaxMaxCluster = 16;
 constexpr int kAtaxMaxRows = 8;
 constexpr int kAtaxMaxStages = 8;
 constexpr int kAtaxSlots = 8;                      // exchange slots; needs > 2*L + 1
-constexpr int kAtaxThreads = kThreads + 32;        // 8 consumer warps + 1 producer warp
+constexpr int kAtaxThreads = kThreads;             // 8 warps; thread 0 also issues the TMA copies
 
 __device__ __forceinline__ uint32_t smem_u32(const void *p)
 {
@@ -151,66 +158,75 @@ __device__ __forceinline__ void st_cluster(double *local, uint32_t rank, double 
     asm volatile("st.shared::cluster.f64 [%0], %1;" ::"r"(remote), "d"(v) : "memory");
 }
 
+// fixed pairwise tree over n values (n a power of two): log2(n) dependent adds
+template <int n>
+__device__ __forceinline__ double tree_sum(const double *v)
+{
+    if constexpr (n == 1) {
+        return v[0];
+    } else {
+        return tree_sum<n / 2>(v) + tree_sum<n / 2>(v + n / 2);
+    }
+}
+
 // C    cluster size (1 = plain CTA, a whole row fits one CTA's slice)
 // KMAX double2 column pairs per thread: the CTA slice is at most 512*KMAX columns
-// RG   bound on rows per panel = min(8, 16 / KMAX)  (a stage is <= 64 KiB)
-template <int C, int KMAX>
+// TR   rows per panel; a panel is TR*KMAX double2 (<= 16) per thread in registers
+template <int C, int KMAX, int TR>
 __global__ void __launch_bounds__(kAtaxThreads, 1)
 atax_cluster_kernel(const AtaxArgs a)
 {
-    constexpr int RG = (16 / KMAX) < kAtaxMaxRows ? (16 / KMAX) : kAtaxMaxRows;
+    static_assert(TR * KMAX <= 16 && TR <= kAtaxMaxRows, "register tile too large");
+    static_assert(kWarps == 8, "the warp-sum tree below is written for 8 warps");
     extern __shared__ __align__(128) unsigned char smem_raw[];
-    double *tiles = reinterpret_cast<double *>(smem_raw);        // [S][rows][W]
+    double *tiles = reinterpret_cast<double *>(smem_raw);        // [S][TR][W]
     __shared__ __align__(8) uint64_t full[kAtaxMaxStages];       // TMA landed (tx bytes)
-    __shared__ __align__(8) uint64_t empty[kAtaxMaxStages];      // 8 consumer warps released
     __shared__ __align__(8) uint64_t pbar[kAtaxSlots];           // C partials of a panel arrived
-    __shared__ double warp_part[2][RG][kWarps];                  // phase-1 warp sums
-    __shared__ double part[kAtaxSlots][RG][C];                   // pushed by every CTA of the cluster
+    __shared__ double warp_part[2][TR][kWarps];                  // phase-1 warp sums
+    __shared__ double part[kAtaxSlots][TR][C];                   // pushed by every CTA of the cluster
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const uint32_t rank = C > 1 ? cluster_rank() : 0u;
     const long cluster = C > 1 ? (long)cluster_index() : (long)blockIdx.x;
     const long N = a.N;
-    const int W = a.W, S = a.stages, L = a.lookahead;
-    const int rg = a.rows;                                       // rows per panel, <= RG
+    const int W = a.W, S = a.stages;
     const long c0 = (long)rank * W;
     const int wlen = (int)((N - c0) < W ? (N - c0 > 0 ? N - c0 : 0) : W);   // my columns
     const long row_lo = (a.M * cluster) / a.nclusters;
     const long row_hi = (a.M * (cluster + 1)) / a.nclusters;
-    const int ngroups = (int)((row_hi - row_lo + rg - 1) / rg);
+    const int ngroups = (int)((row_hi - row_lo + TR - 1) / TR);
 
     if (tid == 0) {
         for (int s = 0; s < S; ++s) {
             mbar_init(&full[s], 1);
-            mbar_init(&empty[s], kWarps);
         }
         for (int s = 0; s < kAtaxSlots; ++s) mbar_init(&pbar[s], 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
-    if (C > 1) {          // every CTA's barriers exist before any remote arrive
+    if (C > 1) {          // every CTA's barriers exist before any remote store
         cluster_arrive();
         cluster_wait();
     }
 
-    if (warp == kWarps) {
-        // ---------------- TMA producer warp ----------------
-        if (lane == 0 && wlen > 0) {
-            const uint32_t seg = (uint32_t)wlen * 8u;
-            for (int g = 0; g < ngroups; ++g) {
-                const int s = g % S;
-                if (g >= S) mbar_wait(&empty[s], (uint32_t)((g / S - 1) & 1));
-                const long r0 = row_lo + (long)g * rg;
-                const int nr = (int)((row_hi - r0) < rg ? (row_hi - r0) : rg);
-                mbar_expect_tx(&full[s], seg * (uint32_t)nr);
-                double *dst = tiles + (size_t)s * rg * W;
-                for (int r = 0; r < nr; ++r) {
-                    bulk_load(dst + (size_t)r * W, a.A + (r0 + r) * N + c0, seg, &full[s]);
-                }
-            }
+    // thread 0: fill stage g % S with panel g
+    auto issue = [&](int g) {
+        if (wlen <= 0) return;
+        const int s = g % S;
+        const uint32_t seg = (uint32_t)wlen * 8u;
+        const long r0 = row_lo + (long)g * TR;
+        const int nr = (int)((row_hi - r0) < TR ? (row_hi - r0) : TR);
+        mbar_expect_tx(&full[s], seg * (uint32_t)nr);
+        double *dst = tiles + (size_t)s * TR * W;
+        for (int r = 0; r < nr; ++r) {
+            bulk_load(dst + (size_t)r * W, a.A + (r0 + r) * N + c0, seg, &full[s]);
         }
-    } else {
-        // ---------------- consumer warps ----------------
+    };
+    if (tid == 0) {
+        for (int g = 0; g < S && g < ngroups; ++g) issue(g);
+    }
+
+    {
         // column weights x and the running column sums live in registers
         double2 xr[KMAX], ysum[KMAX];
 #pragma unroll
@@ -221,48 +237,61 @@ atax_cluster_kernel(const AtaxArgs a)
             ysum[k] = make_double2(0.0, 0.0);
         }
 
-        // phase 1 of panel g: this CTA's slice of the row dots, pushed to the cluster
-        auto phase1 = [&](int g) {
+        // phase 1 of panel g: shared memory -> registers (once), this CTA's slice
+        // of the row dots, pushed to the cluster
+        auto phase1 = [&](int g, double2 (&tile)[TR][KMAX]) {
             const int s = g % S, par = g & 1, slot = g % kAtaxSlots;
             if (wlen > 0) mbar_wait(&full[s], (uint32_t)((g / S) & 1));
-            const double *tile = tiles + (size_t)s * rg * W;
-            const long r0 = row_lo + (long)g * rg;
-            const int nr = (int)((row_hi - r0) < rg ? (row_hi - r0) : rg);
-            double d[RG];
+            const double *src = tiles + (size_t)s * TR * W;
+            const long r0 = row_lo + (long)g * TR;
+            const int nr = (int)((row_hi - r0) < TR ? (row_hi - r0) : TR);
 #pragma unroll
-            for (int r = 0; r < RG; ++r) {
-                double acc = 0.0;
-                if (r < nr) {
+            for (int r = 0; r < TR; ++r) {
 #pragma unroll
-                    for (int k = 0; k < KMAX; ++k) {
-                        const int j = 2 * tid + 2 * kThreads * k;
-                        if (j < wlen) {
-                            const double2 e =
-                                *reinterpret_cast<const double2 *>(tile + (size_t)r * W + j);
-                            acc = fma(e.x, xr[k].x, acc);
-                            acc = fma(e.y, xr[k].y, acc);
-                        }
+                for (int k = 0; k < KMAX; ++k) {
+                    const int j = 2 * tid + 2 * kThreads * k;
+                    tile[r][k] = (r < nr && j < wlen)
+                                     ? *reinterpret_cast<const double2 *>(src + (size_t)r * W + j)
+                                     : make_double2(0.0, 0.0);
+                }
+            }
+            double d[TR];
+#pragma unroll
+            for (int r = 0; r < TR; ++r) {
+                // independent accumulators: with two warps per scheduler a single
+                // 2*KMAX-long FMA chain would expose the fp64 latency
+                double acc0 = 0.0, acc1 = 0.0, acc2 = 0.0, acc3 = 0.0;
+#pragma unroll
+                for (int k = 0; k < KMAX; k += 2) {
+                    acc0 = fma(tile[r][k].x, xr[k].x, acc0);
+                    acc1 = fma(tile[r][k].y, xr[k].y, acc1);
+                    if (k + 1 < KMAX) {
+                        acc2 = fma(tile[r][k + 1].x, xr[k + 1].x, acc2);
+                        acc3 = fma(tile[r][k + 1].y, xr[k + 1].y, acc3);
                     }
                 }
-                d[r] = acc;
+                d[r] = (acc0 + acc1) + (acc2 + acc3);
             }
 #pragma unroll
-            for (int off = 16; off >= 1; off >>= 1) {     // RG independent shuffle chains
+            for (int off = 16; off >= 1; off >>= 1) {     // TR independent shuffle chains
 #pragma unroll
-                for (int r = 0; r < RG; ++r) d[r] += __shfl_xor_sync(kFullMask, d[r], off);
+                for (int r = 0; r < TR; ++r) d[r] += __shfl_xor_sync(kFullMask, d[r], off);
             }
             if (lane == 0) {
 #pragma unroll
-                for (int r = 0; r < RG; ++r) warp_part[par][r][warp] = d[r];
+                for (int r = 0; r < TR; ++r) warp_part[par][r][warp] = d[r];
             }
-            consumer_sync();
+            __syncthreads();
+            // every warp holds its part of the tile in registers (the FMAs above
+            // consumed the loads): the stage is free, refill it S panels ahead
+            if (tid == 0 && g + S < ngroups) issue(g + S);
             if (tid < C) {
                 // thread p serves peer p: the same 8-warp sum in every thread (same bits)
                 if (C > 1 && tid == 0) mbar_expect_tx(&pbar[slot], (uint32_t)(C * nr * 8));
                 for (int r = 0; r < nr; ++r) {
-                    double sum = warp_part[par][r][0];
-#pragma unroll
-                    for (int w = 1; w < kWarps; ++w) sum += warp_part[par][r][w];
+                    const double *wp = warp_part[par][r];      // fixed pairwise tree
+                    const double sum = ((wp[0] + wp[1]) + (wp[2] + wp[3])) +
+                                       ((wp[4] + wp[5]) + (wp[6] + wp[7]));
                     if (C > 1) st_async_cluster(&part[slot][r][rank], &pbar[slot], (uint32_t)tid, sum);
                     else part[slot][r][0] = sum;
                 }
@@ -270,42 +299,32 @@ atax_cluster_kernel(const AtaxArgs a)
             }
         };
 
-        for (int g = 0; g < L && g < ngroups; ++g) phase1(g);
-
-        for (int g = 0; g < ngroups; ++g) {
-            if (g + L < ngroups) phase1(g + L);
-            const int s = g % S, slot = g % kAtaxSlots;
+        // phase 2 of panel g from the register tile
+        auto phase2 = [&](int g, const double2 (&tile)[TR][KMAX]) {
+            const int slot = g % kAtaxSlots;
             mbar_wait(&pbar[slot], (uint32_t)((g / kAtaxSlots) & 1));
-            // t_i: the C partials in rank order -- every CTA computes the same bits
-            double t[RG];
 #pragma unroll
-            for (int r = 0; r < RG; ++r) {
-                double sum = part[slot][r][0];
+            for (int r = 0; r < TR; ++r) {
+                // t_i: the C partials in rank order -- every CTA computes the same bits
+                // (rows past the end of the range hold zeros in the tile)
+                double t = tree_sum<C>(part[slot][r]);
 #pragma unroll
-                for (int peer = 1; peer < C; ++peer) sum += part[slot][r][peer];
-                t[r] = sum;
-            }
-            // phase 2 on the tile that is still in shared memory
-            const double *tile = tiles + (size_t)s * rg * W;
-            const long r0 = row_lo + (long)g * rg;
-            const int nr = (int)((row_hi - r0) < rg ? (row_hi - r0) : rg);
-#pragma unroll
-            for (int r = 0; r < RG; ++r) {
-                if (r < nr) {
-#pragma unroll
-                    for (int k = 0; k < KMAX; ++k) {
-                        const int j = 2 * tid + 2 * kThreads * k;
-                        if (j < wlen) {
-                            const double2 e =
-                                *reinterpret_cast<const double2 *>(tile + (size_t)r * W + j);
-                            ysum[k].x = fma(e.x, t[r], ysum[k].x);
-                            ysum[k].y = fma(e.y, t[r], ysum[k].y);
-                        }
-                    }
+                for (int k = 0; k < KMAX; ++k) {
+                    ysum[k].x = fma(tile[r][k].x, t, ysum[k].x);
+                    ysum[k].y = fma(tile[r][k].y, t, ysum[k].y);
                 }
             }
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&empty[s]);     // this warp is done with stage s
+        };
+
+        // two register tiles, loop unrolled by two so neither is ever copied
+        double2 tile_a[TR][KMAX], tile_b[TR][KMAX];
+        if (ngroups > 0) phase1(0, tile_a);
+        for (int g = 0; g < ngroups; g += 2) {
+            if (g + 1 < ngroups) phase1(g + 1, tile_b);
+            phase2(g, tile_a);
+            if (g + 1 >= ngroups) break;
+            if (g + 2 < ngroups) phase1(g + 2, tile_a);
+            phase2(g + 1, tile_b);
         }
 
         double *dst = a.ypart + cluster * N + c0;

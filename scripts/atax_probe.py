@@ -34,8 +34,8 @@ def main():
         want = oracle_lib.oracle_run("atax", inputs, {"M": m, "N": n}, threads=8)["y"]
         A, x = torch.from_numpy(inputs["A"]).cuda(), torch.from_numpy(inputs["x"]).cuda()
         for C in (0, 1, 2, 4, 8, 16):
-            for S, R, L in ((0, 0, 0), (3, 0, 1), (0, 1, 3), (4, 1, 2)):
-                _native.set_tuning(atax_cluster=C, atax_stages=S, atax_rows=R, atax_lookahead=L, atax_fused=1)
+            for S, R, L in ((0, 0, 0), (2, 0, 0), (0, 1, 0), (4, 1, 0)):
+                _native.set_tuning(atax_cluster=C, atax_stages=S, atax_rows=R, atax_fused=1)
                 got = run(A, x).cpu().numpy()
                 err = float(np.max(np.abs(got - want) / np.maximum(np.abs(want), 1.0)))
                 flag = "" if err < 1e-11 else "  <-- BAD"
@@ -55,12 +55,11 @@ def main():
     _native.set_tuning(debug=1)
     cfgs = [(0, 0, 0, 0, 0)]
     for C in (4, 8, 16):
-        for R in (0, 1, 2):
-            for L in (1, 2, 3):
-                cfgs.append((1, C, 0, R, L))
+        for R in (0, 1):
+            for S in (0, 2, 3):
+                cfgs.append((1, C, S, R, 0))
     for fused, C, S, R, L in cfgs:
-        _native.set_tuning(atax_fused=fused, atax_cluster=C, atax_stages=S, atax_rows=R,
-                           atax_lookahead=L)
+        _native.set_tuning(atax_fused=fused, atax_cluster=C, atax_stages=S, atax_rows=R)
         got = run(A, x)
         err = float(torch.max(torch.abs(got - ref) / torch.clamp(torch.abs(ref), min=1.0)))
         evs = []

@@ -46,18 +46,31 @@ def launch_piece(suite, name):
     _native.check(rc)
 
 
+THRASH = None      # a launch closure run (untimed) before every timed rep
+SUSTAIN = 0.0      # seconds of back-to-back launches before timing (power-capped state)
+
+
 def time_kernel(suite, name, reps):
     if name in PIECES:
         orig = suite.launch
         launch = lambda _n: launch_piece(suite, name)
     else:
         launch = suite.launch
+    if SUSTAIN > 0:
+        import time
+        t_end = time.perf_counter() + SUSTAIN       # reach the power-capped steady state
+        while time.perf_counter() < t_end:
+            for _ in range(20):
+                launch(name)
+            torch.cuda.synchronize()
     for _ in range(3):
         launch(name)
     torch.cuda.synchronize()
     evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
            for _ in range(reps)]
     for a, b in evs:
+        if THRASH is not None:
+            THRASH()
         a.record()
         launch(name)
         b.record()
@@ -71,12 +84,20 @@ def main():
     ap.add_argument("--kernels", default=",".join(SUITE))
     ap.add_argument("--reps", type=int, default=10)
     ap.add_argument("--quick", action="store_true")
+    ap.add_argument("--sustain", type=float, default=0.0,
+                    help="seconds of back-to-back launches before timing each config")
+    ap.add_argument("--thrash", action="store_true",
+                    help="run GEMVER (16 GiB of other traffic) before every timed rep, as in the suite")
     ap.add_argument("--out", default=str(REPO / "gpurun_out" / "sweep.json"))
     args = ap.parse_args()
     kernels = tuple(args.kernels.split(","))
     torch.cuda.set_device(0)
     _native.load()
-    suite = Suite(torch, 0, 1, tuple(k for k in kernels if k not in PIECES) or ("gemver",))
+    global THRASH, SUSTAIN
+    SUSTAIN = args.sustain
+    suite = Suite(torch, 0, 1, tuple(set(k for k in kernels if k not in PIECES) | {"gemver"}))
+    if args.thrash:
+        THRASH = lambda: suite.launch("gemver")
     peak, _ = measured_peak()
     rows = []
     mv_cfgs = [(8, 1), (16, 1), (32, 1), (8, 2)]
@@ -90,8 +111,8 @@ def main():
             cfgs = [dict(mv_rows=r, mv_vec=v, grid_per_sm=g, mv_minb=b)
                     for (r, v), g, b in itertools.product(mv_cfgs, grids, minbs)]
             if name == "atax":
-                cfgs = [dict(atax_cluster=c, atax_rows=r, atax_lookahead=l)
-                        for c, r, l in itertools.product([4, 8], [0, 1], [1, 2])]
+                cfgs = [dict(atax_cluster=c, atax_rows=r, atax_stages=st)
+                        for c, r, st in itertools.product([4, 8, 16], [0, 1], [0, 2, 3])]
         for cfg in cfgs:
             _native.set_tuning(**cfg)
             try:
@@ -106,7 +127,7 @@ def main():
             print(f"{name:8s} {cfg} median {med:8.4f} ms  min {best:8.4f} ms  "
                   f"{gbs:7.1f} GB/s  {100 * gbs / peak:5.1f}%", flush=True)
         _native.set_tuning(mv_rows=0, mv_vec=0, grid_per_sm=0, mv_minb=0, vec_unroll=2, vec_grid_per_sm=0,
-                           atax_cluster=0, atax_rows=0, atax_lookahead=0)
+                           atax_cluster=0, atax_rows=0, atax_stages=0)
     Path(args.out).parent.mkdir(exist_ok=True)
     Path(args.out).write_text(json.dumps(rows, indent=1))
 

@@ -130,7 +130,7 @@ ATAX_SHAPES = [(2048, 1024), (8, 2), (1, 4096), (100, 514), (333, 8192), (64, 16
 @pytest.mark.parametrize("cluster", [0, 1, 2, 4, 8, 16])
 def test_fused_atax_every_cluster_size(bto_lib, oracle, cluster):
     """Single-pass ATAX/BATAX (cluster-resident row panels, TMA ring, st.async
-    exchange): every cluster size, ring depth, panel height and lookahead must
+    exchange): every cluster size, ring depth and panel height must
     give the oracle's result; shapes include slices that leave the last CTA of
     the cluster short, fewer rows than clusters, and a single row."""
     try:
@@ -140,14 +140,13 @@ def test_fused_atax_every_cluster_size(bto_lib, oracle, cluster):
                 graph = bto.load_graph(name)
                 inputs = bto.gen_inputs(graph, ext, seed=m + n)
                 want = oracle.oracle_run(name, inputs, ext, threads=8)
-                for stages, rows, look in ((0, 0, 0), (3, 0, 1), (0, 1, 3), (4, 1, 2)):
+                for stages, rows in ((0, 0), (2, 0), (0, 1), (4, 1)):
                     _native.set_tuning(atax_fused=1, atax_cluster=cluster, atax_stages=stages,
-                                       atax_rows=rows, atax_lookahead=look)
+                                       atax_rows=rows)
                     assert_matches(name, run_device(name, inputs, ext), want, ext,
-                                   f"C{cluster} S{stages} R{rows} L{look}")
+                                   f"C{cluster} S{stages} R{rows}")
     finally:
-        _native.set_tuning(atax_fused=1, atax_cluster=0, atax_stages=0, atax_rows=0,
-                           atax_lookahead=0)
+        _native.set_tuning(atax_fused=1, atax_cluster=0, atax_stages=0, atax_rows=0)
 
 
 def test_two_pass_atax_fallback(bto_lib, oracle):
