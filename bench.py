@@ -419,6 +419,13 @@ def run_gpu_arm(args) -> int:
                          "bytes_min": bytes_min(k, *BENCH[k]), "extents": list(BENCH[k])}
     dominant = max(kernels, key=lambda k: per_ms[k])
     dom = per_kernel[dominant]
+    traffic, traffic_src = None, None
+    try:        # DRAM bytes of the same launches from the committed ncu capture (single GPU)
+        tj = json.loads((REPO / "profiles" / "traffic.json").read_text())
+        if world == 1:
+            traffic, traffic_src = tj[dominant]["dram_bytes"], tj["_source"]
+    except Exception:
+        pass
     line = {
         "metric": "effective HBM GB/s (min bytes/time), fused suite",
         "value": round(value, 1), "unit": "GB/s", "n_gpus": world, "steps": args.steps,
@@ -437,7 +444,7 @@ def run_gpu_arm(args) -> int:
         "roofline": {"bound": "hbm", "kernel": dominant, "achieved": dom["gbs"],
                      "peak": peak * world, "unit": "GB/s",
                      "frac": round(dom["gbs"] / (peak * world), 4),
-                     "traffic": None, "peak_source": peak_src,
+                     "traffic": traffic, "traffic_source": traffic_src, "peak_source": peak_src,
                      "algorithmic_bytes": dom["bytes_min"]},
         "clocks": clocks.summary(),
         "gpu_launches": launches,
