@@ -121,11 +121,6 @@ __device__ __forceinline__ void st_async_cluster(double *local, uint64_t *local_
                  : "memory");
 }
 
-__device__ __forceinline__ void consumer_sync()      // the 256 consumer threads only
-{
-    asm volatile("bar.sync 1, %0;" ::"n"(kThreads) : "memory");
-}
-
 __device__ __forceinline__ uint32_t cluster_rank()
 {
     uint32_t r;
@@ -148,14 +143,6 @@ __device__ __forceinline__ void cluster_arrive()
 __device__ __forceinline__ void cluster_wait()
 {
     asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
-}
-
-// store a double into the same shared-memory variable of CTA `rank` of the cluster
-__device__ __forceinline__ void st_cluster(double *local, uint32_t rank, double v)
-{
-    uint32_t remote;
-    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(smem_u32(local)), "r"(rank));
-    asm volatile("st.shared::cluster.f64 [%0], %1;" ::"r"(remote), "d"(v) : "memory");
 }
 
 // fixed pairwise tree over n values (n a power of two): log2(n) dependent adds

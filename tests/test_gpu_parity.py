@@ -369,3 +369,57 @@ def test_bench_size_axpydot_properties(bto_lib):
     assert torch.equal(out["z"], w - v * (-0.625))       # mul then sub, each rounded once
     ref = float(torch.dot(out["z"], u))
     assert abs(out["beta"] - ref) / max(abs(ref), 1.0) <= 1e-12 * 27
+
+
+def test_random_extents_like_reference_criterion_1(bto_lib, oracle):
+    """The reference's acceptance criterion 1 (tests/test_acceptance.py:55-94) walks
+    every kernel over a grid of extents; here 40 seeded random extent pairs per
+    kernel, including degenerate ones, against the live oracle."""
+    rng = np.random.default_rng(20121205)
+    for name in KERNELS:
+        graph = bto.load_graph(name)
+        pairs = [(1, 1), (2, 2), (1, 7), (7, 1)]
+        pairs += [(int(rng.integers(1, 700)), int(rng.integers(1, 3000))) for _ in range(18)]
+        pairs += [(int(rng.integers(1, 3000)), int(rng.integers(1, 700))) for _ in range(18)]
+        for idx, (m, n) in enumerate(pairs):
+            ext = ext_of(name, m, n)
+            inputs = bto.random_inputs(graph, ext, seed=idx)
+            want = oracle.oracle_run(name, inputs, ext, threads=1 + idx % 8)
+            assert_matches(name, run_device(name, inputs, ext), want, ext, "random extents")
+
+
+def test_cuda_graph_capture_and_replay(bto_lib, oracle):
+    """The asynchronous entry points are stream-ordered and allocation-free after a
+    warm-up call, so a whole sequence can be captured into a CUDA graph (what the
+    sharded runtime does to hide launch gaps) and replayed on new data."""
+    from paper_1205_1098_b200.sharded import GpuShardOps
+    m, n = 1536, 2048
+    g = bto.load_graph("gemver")
+    inputs = bto.gen_inputs(g, {"M": m, "N": n}, seed=3)
+    dev = {k: (torch.from_numpy(v).cuda() if isinstance(v, np.ndarray) else v) for k, v in inputs.items()}
+    B = torch.empty(m, n, dtype=torch.float64, device="cuda")
+    x = torch.empty(n, dtype=torch.float64, device="cuda")
+    w = torch.empty(m, dtype=torch.float64, device="cuda")
+    ops = GpuShardOps()
+
+    def launch():
+        ops.gemver(dev["A"], dev["u1"], dev["v1"], dev["u2"], dev["v2"], inputs["alpha"],
+                   inputs["beta"], dev["y"], dev["z"], B, x, w)
+
+    launch()                       # warm-up: sizes the workspace outside the capture
+    torch.cuda.synchronize()
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(graph):
+        launch()
+    # new data in the same buffers, then replay
+    inputs2 = bto.gen_inputs(g, {"M": m, "N": n}, seed=4)
+    inputs2["alpha"], inputs2["beta"] = inputs["alpha"], inputs["beta"]   # scalars are baked in
+    for k, v in inputs2.items():
+        if isinstance(v, np.ndarray):
+            dev[k].copy_(torch.from_numpy(v))
+    B.fill_(float("nan")); x.fill_(float("nan")); w.fill_(float("nan"))
+    graph.replay()
+    torch.cuda.synchronize()
+    want = oracle.oracle_run("gemver", inputs2, {"M": m, "N": n}, threads=8)
+    got = {"B": B.cpu().numpy(), "x": x.cpu().numpy(), "w": w.cpu().numpy()}
+    assert_matches("gemver", got, want, {"M": m, "N": n}, "graph replay")
