@@ -210,14 +210,23 @@ def run_reference_arm(args) -> int:
 class Suite:
     """Device buffers + launch closures for the five sequences on one rank."""
 
-    def __init__(self, torch, rank: int, world: int, kernels):
+    def __init__(self, torch, rank: int, world: int, kernels, exchange: str = "nccl"):
         from paper_1205_1098_b200 import _native
         from paper_1205_1098_b200.sharded import GpuShardOps, ShardedRunner, TorchComm, row_block
         self.torch, self.rank, self.world = torch, rank, world
         self.native = _native
         self.ops = GpuShardOps()
         comm = TorchComm() if world > 1 else None
-        self.runner = ShardedRunner(self.ops, comm, rank, world)
+        self.exchange_kind = "none" if world == 1 else "nccl"
+        fused = False
+        if world > 1 and exchange == "fused":
+            try:        # join-fused NVLink exchange (include/bto_b200.h 3b)
+                from paper_1205_1098_b200.sharded import NvlinkExchange
+                self.exchange = NvlinkExchange(max_vector=32768)
+                fused, self.exchange_kind = True, "fused-join (NVLink peer memory)"
+            except Exception as exc:  # symmetric memory unavailable: library all-reduce
+                self.exchange_kind = f"nccl (fused exchange unavailable: {type(exc).__name__})"
+        self.runner = ShardedRunner(self.ops, comm, rank, world, fused=fused)
         self.kernels = kernels
         dev = torch.device("cuda", torch.cuda.current_device())
         gen = torch.Generator(device=dev).manual_seed(1234 + rank)
@@ -362,7 +371,7 @@ def run_gpu_arm(args) -> int:
 
     from paper_1205_1098_b200 import _native
     _native.load()
-    suite = Suite(torch, rank, world, kernels)
+    suite = Suite(torch, rank, world, kernels, exchange=args.exchange)
 
     def barrier():
         if world > 1:
@@ -436,7 +445,8 @@ def run_gpu_arm(args) -> int:
             "workload": "suite5: AXPYDOT n=2^27, BiCGK n=32768, ATAX n=32768, GESUMMV n=24576, "
                         "GEMVER n=32768" if args.kernel == "suite" else
                         f"{args.kernel} at BASELINE bench size {BENCH[args.kernel]}",
-            "parallelism": f"row-shard x{world}" if world > 1 else "single GPU",
+            "parallelism": f"row-shard x{world}, exchange: {suite.exchange_kind}" if world > 1
+                           else "single GPU",
             "l2": "every input >= 4 GiB >> 126 MB L2; no flush between iterations",
             "timing": "CUDA events on the launch stream, max over ranks",
         },
@@ -476,6 +486,8 @@ def main() -> int:
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=("b200", "reference"), default="b200")
     ap.add_argument("--kernel", choices=("suite",) + SUITE, default="suite")
+    ap.add_argument("--exchange", choices=("nccl", "fused"), default="nccl",
+                    help="N > 1: NCCL all-reduce after the join, or the exchange fused into the join")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     args = ap.parse_args()

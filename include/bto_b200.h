@@ -127,12 +127,46 @@ int bto_gemver_xupdate_async(const double *colsum, double beta, const double *z,
 int bto_gemver_pass2_async(const double *B, const double *x, double alpha,
                            double *w, long M, long N, bto_stream_t stream);
 
+/* ---- 3b. the exchange fused into the join (NVLink / NVSwitch peer memory) ---
+ * Instead of "join locally, then all-reduce", the join kernel of a sharded
+ * sequence writes this rank's partial of the column-indexed result into a
+ * symmetric exchange buffer, publishes a flag in every peer's flag array, waits
+ * for the peers' flags and adds all partials in rank order straight from peer
+ * memory (one-shot; the payload is <= 256 KiB, so this is latency-optimal and
+ * every rank gets bit-identical results).  GEMVER's x = beta*sum + z epilogue
+ * runs in the same kernel.
+ *   exch_ptrs[p]  : rank p's exchange buffer as mapped on THIS device,
+ *                   capacity_doubles doubles (>= 2 * the longest reduced vector:
+ *                   two halves alternate between consecutive exchanges)
+ *   flag_ptrs[p]  : rank p's flag array, bto_exchange_flag_bytes(world) bytes,
+ *                   zeroed before the first exchange
+ *   epoch0        : exchanges already performed on these buffers (0 at start)
+ * Every rank must call the same *_sharded_async sequence in the same order.  */
+int bto_exchange_init(int rank, int world, void *const *exch_ptrs, void *const *flag_ptrs,
+                      long capacity_doubles, unsigned int epoch0);
+int bto_exchange_shutdown(void);
+int bto_exchange_flag_bytes(int world);
+int bto_axpydot_sharded_async(const double *w, const double *v, const double *u,
+                              double alpha, double *z, double *beta, long M,
+                              bto_stream_t stream);
+int bto_bicgk_sharded_async(const double *A, const double *p, const double *r,
+                            double *q, double *s, long M, long N, bto_stream_t stream);
+int bto_atax_sharded_async(const double *A, const double *x, double *y,
+                           long M, long N, bto_stream_t stream);
+int bto_gemver_sharded_async(const double *A, const double *u1, const double *v1,
+                             const double *u2, const double *v2, double alpha,
+                             double beta, const double *y, const double *z,
+                             double *B, double *x, double *w, long M, long N,
+                             bto_stream_t stream);
+
 /* ---- 4. runtime control and introspection --------------------------------- */
 int   bto_abi_version(void);
 int   bto_set_stream(bto_stream_t stream);      /* stream for section-1 calls */
 /* Tunables of the launch heuristics (what the GPU variant search explores):
  * "mv_rows" (8|16|32 rows per unit), "mv_vec" (1|2 double2 per thread per row),
- * "grid_per_sm" (0 = occupancy), "vec_unroll" (1|2|4), ...  Unknown key or an
+ * "grid_per_sm" (0 = default), "mv_minb", "vec_unroll" (1|2|4), "atax_fused",
+ * "atax_cluster", "atax_rows", "atax_stages", "host_pipeline", "host_panel_mib",
+ * "exchange_phases", "debug".  Unknown key or an
  * unsupported value returns BTO_ERR_INVALID.  bto_get_tuning returns -1 for
  * an unknown key.                                                           */
 int   bto_set_tuning(const char *key, long value);

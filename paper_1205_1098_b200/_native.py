@@ -51,6 +51,9 @@ _CT = {"p": _P, "d": _D, "l": _L}
 #: every symbol include/bto_b200.h declares (tests check the library exports them)
 EXPORTED = tuple(SIGNATURES) + tuple(f"bto_{k}_async" for k in SIGNATURES) + (
     "bto_gemver_pass1_async", "bto_gemver_xupdate_async", "bto_gemver_pass2_async",
+    "bto_exchange_init", "bto_exchange_shutdown", "bto_exchange_flag_bytes",
+    "bto_axpydot_sharded_async", "bto_bicgk_sharded_async", "bto_atax_sharded_async",
+    "bto_gemver_sharded_async",
     "bto_last_error", "bto_last_error_string", "bto_clear_error",
     "bto_abi_version", "bto_set_stream", "bto_set_tuning", "bto_get_tuning",
     "bto_kernel_launches", "bto_bytes_min", "bto_device_info",
@@ -89,6 +92,16 @@ def load() -> ctypes.CDLL:
     lib.bto_gemver_xupdate_async.argtypes = [_P, _D, _P, _P, _L, _S]
     lib.bto_gemver_pass2_async.restype = c_int
     lib.bto_gemver_pass2_async.argtypes = [_P, _P, _D, _P, _L, _L, _S]
+    for name in ("axpydot", "bicgk", "atax", "gemver"):
+        sfn = getattr(lib, f"bto_{name}_sharded_async")
+        sfn.restype = c_int
+        sfn.argtypes = [_CT[ch] for ch in SIGNATURES[name]] + [_S]
+    lib.bto_exchange_init.restype = c_int
+    lib.bto_exchange_init.argtypes = [c_int, c_int, POINTER(c_void_p), POINTER(c_void_p), _L,
+                                      ctypes.c_uint]
+    lib.bto_exchange_shutdown.restype = c_int
+    lib.bto_exchange_flag_bytes.restype = c_int
+    lib.bto_exchange_flag_bytes.argtypes = [c_int]
     lib.bto_last_error.restype = c_int
     lib.bto_last_error_string.restype = c_char_p
     lib.bto_clear_error.restype = None

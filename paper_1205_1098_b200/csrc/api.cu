@@ -69,6 +69,7 @@ struct Tuning {
     long atax_stages = 0;    // TMA ring depth (0 = as many as fit, at most 8)
     long atax_rows = 0;      // 0: 16 double2 per thread per panel, 1: half-height panels
     long debug = 0;          // print launch plans to stderr
+    long exchange_phases = 3;    // bit 0 publish, bit 1 wait+reduce (tests emulate ranks with 1, 2)
     long host_pipeline = 1;  // overlap H2D / compute / D2H in row panels for host operands
     long host_panel_mib = 256;   // panel size of that pipeline
 };
@@ -88,6 +89,13 @@ struct DeviceCtx {
     cudaStream_t stream = nullptr; // stream of the section-1 entry points
     std::map<const void *, int> occupancy;
     std::map<const void *, int> max_clusters;
+    // NVLink exchange fused into the join (row-sharded runtime)
+    bool exch_ready = false, exch_active = false;
+    int exch_rank = 0, exch_world = 1;
+    long exch_capacity = 0;            // doubles per rank, both parity halves together
+    double **exch_bufs = nullptr;      // device array [world] of peer-mapped buffers
+    unsigned int **exch_flags = nullptr;
+    unsigned int exch_epoch = 0;
     // host-pointer pipeline: copy-in and copy-out streams, reusable events
     cudaStream_t copy_in = nullptr, copy_out = nullptr;
     std::vector<cudaEvent_t> events;
@@ -353,7 +361,36 @@ int launch_mv(const MvPlan &p, const MvArgs &a, cudaStream_t stream)
     return check_launch("mv_tile_kernel");
 }
 
-int launch_finalize(const MvPlan &p, FinArgs f, long M, long N, cudaStream_t stream)
+// Launch the join of `f` (geometry already filled in).  While a sharded
+// entry point is active and the join has a column side, the cross-GPU exchange
+// is fused into it (join_exchange_kernel); otherwise the plain local join runs.
+int launch_join(DeviceCtx &c, FinArgs f, cudaStream_t stream)
+{
+    const long rb = f.rmode != kRowNone ? (f.M + kThreads - 1) / kThreads : 0;
+    if (c.exch_active && f.cmode != kColNone) {
+        if (2 * f.N > c.exch_capacity) {
+            return fail(BTO_ERR_INVALID, "exchange buffer holds %ld doubles, need %ld",
+                        c.exch_capacity, 2 * f.N);
+        }
+        ExchArgs e{};
+        e.fin = f;
+        e.exch = c.exch_bufs;
+        e.flags = c.exch_flags;
+        e.epoch = ++c.exch_epoch;
+        e.buf_offset = (long)(e.epoch & 1u) * (c.exch_capacity / 2);
+        e.rank = c.exch_rank;
+        e.world = c.exch_world;
+        e.phases = (int)g_tuning.exchange_phases;
+        join_exchange_kernel<<<(unsigned)(kExchCtas + rb), kThreads, 0, stream>>>(e);
+        return check_launch("join_exchange_kernel");
+    }
+    const long cb = f.cmode != kColNone ? (f.N + kThreads - 1) / kThreads : 0;
+    f.col_blocks = (int)cb;
+    finalize_kernel<<<(unsigned)(cb + rb), kThreads, 0, stream>>>(f);
+    return check_launch("finalize_kernel");
+}
+
+int launch_finalize(DeviceCtx &c, const MvPlan &p, FinArgs f, long M, long N, cudaStream_t stream)
 {
     f.M = M;
     f.N = N;
@@ -362,11 +399,7 @@ int launch_finalize(const MvPlan &p, FinArgs f, long M, long N, cudaStream_t str
     f.grid = p.grid;
     f.strip_width = p.strip_width;
     f.nstrips = p.nstrips;
-    const long cb = f.cmode != kColNone ? (N + kThreads - 1) / kThreads : 0;
-    const long rb = f.rmode != kRowNone ? (M + kThreads - 1) / kThreads : 0;
-    f.col_blocks = (int)cb;
-    finalize_kernel<<<(unsigned)(cb + rb), kThreads, 0, stream>>>(f);
-    return check_launch("finalize_kernel");
+    return launch_join(c, f, stream);
 }
 
 int check_mn(long M, long N)
@@ -417,7 +450,7 @@ struct Pass {
         f.colpart = a.colpart;
         if (!(FLAGS & kFlagN)) f.rmode = kRowNone;
         if (!(FLAGS & kFlagT)) f.cmode = kColNone;
-        return launch_finalize(plan, f, M, N, stream);
+        return launch_finalize(c, plan, f, M, N, stream);
     }
 };
 
@@ -631,9 +664,7 @@ int seq_atax_fused(DeviceCtx &c, const AtaxPlan &p, const double *A, const doubl
     f.total_units = p.nclusters;
     f.grid = p.nclusters;
     f.rmode = kRowNone;
-    f.col_blocks = (int)((N + kThreads - 1) / kThreads);
-    finalize_kernel<<<(unsigned)f.col_blocks, kThreads, 0, st>>>(f);
-    return check_launch("finalize_kernel");
+    return launch_join(c, f, st);
 }
 
 // y = [beta *] A'(A x): pass 1 contracts t = A x into a workspace vector (it
@@ -1345,6 +1376,119 @@ int bto_gemver_pass2_async(const double *B, const double *x, double alpha,
     return seq_pass2(*ac.ctx, B, x, alpha, w, M, N, st);
 }
 
+// ---- section 5: exchange fused into the join (NVLink peer memory) -----------------
+
+int bto_exchange_init(int rank, int world, void *const *exch_ptrs, void *const *flag_ptrs,
+                      long capacity_doubles, unsigned int epoch0)
+{
+    AsyncCall ac;
+    if (ac.rc != BTO_OK) return ac.rc;
+    DeviceCtx &c = *ac.ctx;
+    if (world < 1 || world > 64 || rank < 0 || rank >= world || !exch_ptrs || !flag_ptrs ||
+        capacity_doubles < 2) {
+        return fail(BTO_ERR_INVALID, "exchange: bad rank/world/pointers/capacity");
+    }
+    for (int p = 0; p < world; ++p) {
+        if (!exch_ptrs[p] || !flag_ptrs[p]) return fail(BTO_ERR_INVALID, "exchange: null peer pointer");
+    }
+    CUDA_TRY(cudaDeviceSynchronize());
+    if (!c.exch_bufs) {
+        CUDA_TRY(cudaMalloc(&c.exch_bufs, 64 * sizeof(double *)));
+        CUDA_TRY(cudaMalloc(&c.exch_flags, 64 * sizeof(unsigned int *)));
+    }
+    CUDA_TRY(cudaMemcpy(c.exch_bufs, exch_ptrs, (size_t)world * sizeof(void *), cudaMemcpyHostToDevice));
+    CUDA_TRY(cudaMemcpy(c.exch_flags, flag_ptrs, (size_t)world * sizeof(void *), cudaMemcpyHostToDevice));
+    c.exch_rank = rank;
+    c.exch_world = world;
+    c.exch_capacity = (capacity_doubles / 2) * 2;
+    c.exch_epoch = epoch0;
+    c.exch_ready = true;
+    return BTO_OK;
+}
+
+int bto_exchange_shutdown(void)
+{
+    AsyncCall ac;
+    if (ac.rc != BTO_OK) return ac.rc;
+    CUDA_TRY(cudaDeviceSynchronize());
+    ac.ctx->exch_ready = false;
+    return BTO_OK;
+}
+
+int bto_exchange_flag_bytes(int world) { return world * kExchCtas * (int)sizeof(unsigned int); }
+
+namespace {
+// marks the sequence as sharded for the joins it launches
+struct ExchangeScope {
+    explicit ExchangeScope(DeviceCtx &c) : ctx(c)
+    {
+        // a reduce-only call (tests) re-uses the epoch of the publish it pairs with
+        if (!(g_tuning.exchange_phases & 1)) --ctx.exch_epoch;
+        ctx.exch_active = true;
+    }
+    ~ExchangeScope() { ctx.exch_active = false; }
+    DeviceCtx &ctx;
+};
+}  // namespace
+
+#define SHARDED_PROLOGUE()                                                      \
+    ASYNC_PROLOGUE();                                                           \
+    if (!ac.ctx->exch_ready) return fail(BTO_ERR_INVALID, "bto_exchange_init has not been called"); \
+    ExchangeScope scope(*ac.ctx)
+
+int bto_axpydot_sharded_async(const double *w, const double *v, const double *u, double alpha,
+                              double *z, double *beta, long M, bto_stream_t stream)
+{
+    SHARDED_PROLOGUE();
+    DeviceCtx &c = *ac.ctx;
+    if (M < 1) return fail(BTO_ERR_INVALID, "extent M=%ld must be >= 1", M);
+    // local dot into a workspace scalar (kept clear of the kernel's own partials)
+    WsLayout lay;
+    lay.take((size_t)c.sm_count * 64);
+    const size_t off = lay.take(1);
+    BTO_TRY(size_ws(c, lay));
+    double *local = reinterpret_cast<double *>(c.ws + off);
+    c.exch_active = false;
+    int rc = seq_axpydot(c, w, v, u, alpha, z, local, M, st);
+    c.exch_active = true;
+    BTO_TRY(rc);
+    FinArgs f{};
+    f.colpart = local;
+    f.colout = beta;
+    f.cmode = kColPlain;
+    f.N = 1;
+    f.M = 1;
+    f.strip_width = 1;
+    f.units_per_strip = 1;
+    f.total_units = 1;
+    f.grid = 1;
+    f.rmode = kRowNone;
+    return launch_join(c, f, st);
+}
+
+int bto_bicgk_sharded_async(const double *A, const double *p, const double *r, double *q,
+                            double *s, long M, long N, bto_stream_t stream)
+{
+    SHARDED_PROLOGUE();
+    return seq_bicgk(*ac.ctx, A, p, r, q, s, M, N, st);
+}
+
+int bto_atax_sharded_async(const double *A, const double *x, double *y, long M, long N,
+                           bto_stream_t stream)
+{
+    SHARDED_PROLOGUE();
+    return seq_atax(*ac.ctx, A, x, y, M, N, false, 1.0, st);
+}
+
+int bto_gemver_sharded_async(const double *A, const double *u1, const double *v1,
+                             const double *u2, const double *v2, double alpha, double beta,
+                             const double *y, const double *z, double *B, double *x, double *w,
+                             long M, long N, bto_stream_t stream)
+{
+    SHARDED_PROLOGUE();
+    return seq_gemver(*ac.ctx, A, u1, v1, u2, v2, alpha, beta, y, z, B, x, w, M, N, st);
+}
+
 // ---- section 4: control ----------------------------------------------------------
 
 int bto_set_stream(bto_stream_t stream)
@@ -1369,6 +1513,7 @@ static long *tuning_slot(const char *key)
     if (!strcmp(key, "atax_stages")) return &g_tuning.atax_stages;
     if (!strcmp(key, "atax_rows")) return &g_tuning.atax_rows;
     if (!strcmp(key, "debug")) return &g_tuning.debug;
+    if (!strcmp(key, "exchange_phases")) return &g_tuning.exchange_phases;
     if (!strcmp(key, "host_pipeline")) return &g_tuning.host_pipeline;
     if (!strcmp(key, "host_panel_mib")) return &g_tuning.host_panel_mib;
     return nullptr;
@@ -1386,6 +1531,7 @@ int bto_set_tuning(const char *key, long value)
     if (slot == &g_tuning.vec_unroll) ok = value == 1 || value == 2 || value == 4;
     if (slot == &g_tuning.atax_fused || slot == &g_tuning.host_pipeline) ok = value == 0 || value == 1;
     if (slot == &g_tuning.host_panel_mib) ok = value >= 1 && value <= 4096;
+    if (slot == &g_tuning.exchange_phases) ok = value >= 1 && value <= 3;
     if (slot == &g_tuning.atax_cluster) ok = value == 0 || value == 1 || value == 2 || value == 4 || value == 8 || value == 16;
     if (slot == &g_tuning.atax_stages) ok = value == 0 || (value >= 2 && value <= 8);
     if (slot == &g_tuning.atax_rows) ok = value == 0 || value == 1;

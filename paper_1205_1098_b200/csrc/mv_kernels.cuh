@@ -308,39 +308,138 @@ struct FinArgs {
     int col_blocks;           // CTAs [0, col_blocks) do columns, the rest rows
 };
 
+// ascending join of the column partials of column j (no epilogue)
+__device__ __forceinline__ double join_column(const FinArgs &f, long j)
+{
+    const long strip = j / f.strip_width;
+    const long first = split_owner(f.total_units, f.grid, strip * f.units_per_strip);
+    const long last = split_owner(f.total_units, f.grid, (strip + 1) * f.units_per_strip - 1);
+    double s = f.colpart[j];
+    for (long k = 1; k <= last - first; ++k) s += f.colpart[k * f.N + j];
+    return s;
+}
+
+__device__ __forceinline__ double column_epilogue(const FinArgs &f, long j, double s)
+{
+    if (f.cmode == kColAxpz) {            // t4 = t3*beta ; x = t4 + z
+        s = __dadd_rn(__dmul_rn(s, f.cscale), f.colz[j]);
+    } else if (f.cmode == kColScale) {    // y = t1*beta
+        s = __dmul_rn(s, f.cscale);
+    }
+    return s;
+}
+
+// join + epilogue of row i
+__device__ __forceinline__ void finalize_row(const FinArgs &f, long i)
+{
+    double s = f.rowpart[i];
+    for (int c = 1; c < f.nstrips; ++c) s += f.rowpart[(long)c * f.M + i];
+    if (f.rmode == kRowGesummv) {         // t1 = t0*alpha ; t3 = t2*beta ; y = t1 + t3
+        double s2 = f.rowpart2[i];
+        for (int c = 1; c < f.nstrips; ++c) s2 += f.rowpart2[(long)c * f.M + i];
+        s = __dadd_rn(__dmul_rn(s, f.ralpha), __dmul_rn(s2, f.rbeta));
+    } else if (f.rmode == kRowScale) {    // w = t5*alpha
+        s = __dmul_rn(s, f.ralpha);
+    } else if (f.rmode == kRowDgemv) {    // t1 = t0*alpha ; t2 = y*beta ; z = t1 + t2
+        s = __dadd_rn(__dmul_rn(s, f.ralpha), __dmul_rn(f.rowy[i], f.rbeta));
+    }
+    f.rowout[i] = s;
+}
+
 __global__ void __launch_bounds__(kThreads)
 finalize_kernel(const FinArgs f)
 {
     if ((int)blockIdx.x < f.col_blocks) {
         const long j = (long)blockIdx.x * kThreads + threadIdx.x;
-        if (j >= f.N) return;
-        const long strip = j / f.strip_width;
-        const long first = split_owner(f.total_units, f.grid, strip * f.units_per_strip);
-        const long last = split_owner(f.total_units, f.grid,
-                                      (strip + 1) * f.units_per_strip - 1);
-        double s = f.colpart[j];
-        for (long k = 1; k <= last - first; ++k) s += f.colpart[k * f.N + j];
-        if (f.cmode == kColAxpz) {            // t4 = t3*beta ; x = t4 + z
-            s = __dadd_rn(__dmul_rn(s, f.cscale), f.colz[j]);
-        } else if (f.cmode == kColScale) {    // y = t1*beta
-            s = __dmul_rn(s, f.cscale);
-        }
-        f.colout[j] = s;
+        if (j < f.N) f.colout[j] = column_epilogue(f, j, join_column(f, j));
     } else {
         const long i = (long)(blockIdx.x - f.col_blocks) * kThreads + threadIdx.x;
-        if (i >= f.M) return;
-        double s = f.rowpart[i];
-        for (int c = 1; c < f.nstrips; ++c) s += f.rowpart[(long)c * f.M + i];
-        if (f.rmode == kRowGesummv) {         // t1 = t0*alpha ; t3 = t2*beta ; y = t1 + t3
-            double s2 = f.rowpart2[i];
-            for (int c = 1; c < f.nstrips; ++c) s2 += f.rowpart2[(long)c * f.M + i];
-            s = __dadd_rn(__dmul_rn(s, f.ralpha), __dmul_rn(s2, f.rbeta));
-        } else if (f.rmode == kRowScale) {    // w = t5*alpha
-            s = __dmul_rn(s, f.ralpha);
-        } else if (f.rmode == kRowDgemv) {    // t1 = t0*alpha ; t2 = y*beta ; z = t1 + t2
-            s = __dadd_rn(__dmul_rn(s, f.ralpha), __dmul_rn(f.rowy[i], f.rbeta));
+        if (i < f.M) finalize_row(f, i);
+    }
+}
+
+// ---- join fused with the cross-GPU exchange (row-sharded runtime) ------------
+//
+// Every rank owns a row shard and therefore a PARTIAL of each column-indexed
+// result (s = A'r, y = A'(Ax), B'y, the AXPYDOT scalar).  Instead of joining
+// locally and then calling a library all-reduce, the join kernel itself does
+// the exchange over NVLink peer memory (one-shot, for vectors of a few
+// hundred KiB the latency-optimal scheme):
+//   A  join my columns into MY exchange buffer (symmetric memory, mapped by
+//      every peer), double-buffered by call parity;
+//   B  publish: one flag per (source rank, CTA) in every peer's flag array,
+//      st.release.sys after a system fence; then wait until every peer's flag
+//      for this CTA shows this call's epoch (ld.acquire.sys);
+//   C  add the `world` partials of my columns in RANK ORDER straight from the
+//      peers' buffers -- every rank computes the same bits -- apply the
+//      sequence's epilogue, store the result.
+// A CTA only depends on the same-numbered CTA of the peers, so no grid-wide
+// barrier is needed; row-side joins ride in the same launch as extra CTAs.
+// `phases` (bit 0: A+publish, bit 1: wait+C) exists so that one GPU can stand in
+// for all ranks in tests: publish for every rank first, then reduce for every
+// rank -- one kernel over all ranks' data, nobody ever waits.
+constexpr int kExchCtas = 64;
+
+struct ExchArgs {
+    FinArgs fin;                   // local partials + epilogue + row side
+    double *const *exch;           // [world] every rank's exchange buffer (peer-mapped)
+    unsigned int *const *flags;    // [world] every rank's flags [world][kExchCtas]
+    long buf_offset;               // parity half of the exchange buffer, in doubles
+    unsigned int epoch;
+    int rank, world;
+    int phases;
+};
+
+__device__ __forceinline__ void st_release_sys(unsigned int *p, unsigned int v)
+{
+    asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+__device__ __forceinline__ unsigned int ld_acquire_sys(const unsigned int *p)
+{
+    unsigned int v;
+    asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+
+__device__ __forceinline__ double ld_relaxed_sys(const double *p)
+{
+    double v;
+    asm volatile("ld.relaxed.sys.global.f64 %0, [%1];" : "=d"(v) : "l"(p) : "memory");
+    return v;
+}
+
+__global__ void __launch_bounds__(kThreads)
+join_exchange_kernel(const ExchArgs e)
+{
+    const FinArgs &f = e.fin;
+    if ((int)blockIdx.x >= kExchCtas) {          // row side: purely local
+        const long i = (long)(blockIdx.x - kExchCtas) * kThreads + threadIdx.x;
+        if (i < f.M) finalize_row(f, i);
+        return;
+    }
+    const int cta = blockIdx.x;
+    const long c_lo = (f.N * cta) / kExchCtas, c_hi = (f.N * (cta + 1)) / kExchCtas;
+    if (e.phases & 1) {
+        double *mine = e.exch[e.rank] + e.buf_offset;
+        for (long j = c_lo + threadIdx.x; j < c_hi; j += kThreads) mine[j] = join_column(f, j);
+        __syncthreads();
+        if ((int)threadIdx.x < e.world) {
+            __threadfence_system();
+            st_release_sys(e.flags[threadIdx.x] + (long)e.rank * kExchCtas + cta, e.epoch);
         }
-        f.rowout[i] = s;
+    }
+    if (e.phases & 2) {
+        if ((int)threadIdx.x < e.world) {
+            const unsigned int *flag = e.flags[e.rank] + (long)threadIdx.x * kExchCtas + cta;
+            while (ld_acquire_sys(flag) != e.epoch) { }
+        }
+        __syncthreads();
+        for (long j = c_lo + threadIdx.x; j < c_hi; j += kThreads) {
+            double s = ld_relaxed_sys(e.exch[0] + e.buf_offset + j);
+            for (int p = 1; p < e.world; ++p) s += ld_relaxed_sys(e.exch[p] + e.buf_offset + j);
+            f.colout[j] = column_epilogue(f, j, s);
+        }
     }
 }
 

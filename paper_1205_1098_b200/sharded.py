@@ -24,7 +24,8 @@ from __future__ import annotations
 import ctypes
 from dataclasses import dataclass
 
-__all__ = ["row_block", "ShardSpec", "SHARDING", "ShardedRunner", "GpuShardOps"]
+__all__ = ["row_block", "ShardSpec", "SHARDING", "ShardedRunner", "GpuShardOps",
+           "NvlinkExchange", "TorchComm", "shard_inputs"]
 
 
 def row_block(extent: int, rank: int, world: int) -> tuple[int, int]:
@@ -61,24 +62,34 @@ class ShardedRunner:
     """Runs one kernel on this rank's shard and performs the exchange.
 
     comm: an object with `all_reduce_sum(tensor_or_array)` (in place);
-    local: shard compute with methods named after the kernels (see GpuShardOps).
+    local: shard compute with methods named after the kernels (see GpuShardOps);
+    fused: when True (and world > 1) the exchange is done INSIDE the join kernel
+    over NVLink peer memory (`local.<kernel>_sharded`, set up by NvlinkExchange)
+    instead of a separate all-reduce.
     """
 
-    def __init__(self, local, comm, rank: int, world: int):
+    def __init__(self, local, comm, rank: int, world: int, fused: bool = False):
         self.local, self.comm, self.rank, self.world = local, comm, rank, world
+        self.fused = fused and world > 1
 
     def axpydot(self, w, v, u, alpha, z, beta):
+        if self.fused:
+            return self.local.axpydot_sharded(w, v, u, alpha, z, beta)
         self.local.axpydot(w, v, u, alpha, z, beta)
         if self.world > 1:
             self.comm.all_reduce_sum(beta)
 
     def bicgk(self, A, p, r, q, s):
+        if self.fused:
+            return self.local.bicgk_sharded(A, p, r, q, s)
         self.local.bicgk(A, p, r, q, s)
         if self.world > 1:
             self.comm.all_reduce_sum(s)
 
     def atax(self, A, x, y):
         # t = A_g x is complete on the rank (rows are whole), y_g = A_g' t
+        if self.fused:
+            return self.local.atax_sharded(A, x, y)
         self.local.atax(A, x, y)
         if self.world > 1:
             self.comm.all_reduce_sum(y)
@@ -88,6 +99,8 @@ class ShardedRunner:
 
     def gemver(self, A, u1, v1, u2, v2, alpha, beta, y, z, B, x, w, colsum):
         """colsum: N-element scratch for the exchanged B'y partials."""
+        if self.fused:
+            return self.local.gemver_sharded(A, u1, v1, u2, v2, alpha, beta, y, z, B, x, w)
         self.local.gemver_pass1(A, u1, v1, u2, v2, y, B, colsum)
         if self.world > 1:
             self.comm.all_reduce_sum(colsum)
@@ -104,6 +117,45 @@ class TorchComm:
 
     def all_reduce_sum(self, tensor):
         self.dist.all_reduce(tensor, op=self.dist.ReduceOp.SUM, group=self.group)
+
+
+class NvlinkExchange:
+    """Symmetric exchange buffers for the join-fused all-reduce (include/bto_b200.h 3b).
+
+    Allocates one symmetric-memory block per rank (torch.distributed._symmetric_memory:
+    every rank maps every peer's block over NVLink), lays out
+    [capacity doubles of exchange | world*64 u32 flags], zeroes it, and hands the
+    peer pointers to the library.  Needs one process per GPU on an NVLink/NVSwitch
+    node; there is no way to exercise it in a single-GPU environment, where the
+    kernel itself is tested by emulating all ranks on one device
+    (tests/test_gpu_parity.py::test_join_fused_exchange_emulated_ranks).
+    """
+
+    def __init__(self, max_vector: int, group=None):
+        import torch
+        import torch.distributed as dist
+        import torch.distributed._symmetric_memory as symm_mem
+        from . import _native
+
+        lib = _native.load()
+        self.world, self.rank = dist.get_world_size(group), dist.get_rank(group)
+        capacity = 2 * int(max_vector)
+        flag_bytes = int(lib.bto_exchange_flag_bytes(self.world))
+        total = capacity + (flag_bytes + 7) // 8
+        self.block = symm_mem.empty(total, dtype=torch.float64, device=torch.device(
+            "cuda", torch.cuda.current_device()))
+        self.block.zero_()
+        self.handle = symm_mem.rendezvous(self.block, group or dist.group.WORLD)
+        torch.cuda.synchronize()
+        dist.barrier(group)
+        ptrs = [int(p) for p in self.handle.buffer_ptrs]
+        exch = (ctypes.c_void_p * self.world)(*ptrs)
+        flags = (ctypes.c_void_p * self.world)(*[p + 8 * capacity for p in ptrs])
+        _native.check(lib.bto_exchange_init(self.rank, self.world, exch, flags, capacity, 0))
+        self._lib, self._native = lib, _native
+
+    def close(self):
+        self._native.check(self._lib.bto_exchange_shutdown())
 
 
 class GpuShardOps:
@@ -149,6 +201,27 @@ class GpuShardOps:
 
     def gemver(self, A, u1, v1, u2, v2, alpha, beta, y, z, B, x, w):
         self._native.check(self.lib.bto_gemver_async(
+            self._p(A), self._p(u1), self._p(v1), self._p(u2), self._p(v2),
+            float(alpha), float(beta), self._p(y), self._p(z), self._p(B), self._p(x),
+            self._p(w), A.shape[0], A.shape[1], self._st()))
+
+    # -- exchange fused into the join (needs NvlinkExchange / bto_exchange_init) --
+    def axpydot_sharded(self, w, v, u, alpha, z, beta):
+        self._native.check(self.lib.bto_axpydot_sharded_async(
+            self._p(w), self._p(v), self._p(u), float(alpha), self._p(z), self._p(beta),
+            w.numel(), self._st()))
+
+    def bicgk_sharded(self, A, p, r, q, s):
+        self._native.check(self.lib.bto_bicgk_sharded_async(
+            self._p(A), self._p(p), self._p(r), self._p(q), self._p(s),
+            A.shape[0], A.shape[1], self._st()))
+
+    def atax_sharded(self, A, x, y):
+        self._native.check(self.lib.bto_atax_sharded_async(
+            self._p(A), self._p(x), self._p(y), A.shape[0], A.shape[1], self._st()))
+
+    def gemver_sharded(self, A, u1, v1, u2, v2, alpha, beta, y, z, B, x, w):
+        self._native.check(self.lib.bto_gemver_sharded_async(
             self._p(A), self._p(u1), self._p(v1), self._p(u2), self._p(v2),
             float(alpha), float(beta), self._p(y), self._p(z), self._p(B), self._p(x),
             self._p(w), A.shape[0], A.shape[1], self._st()))

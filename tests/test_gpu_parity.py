@@ -423,3 +423,77 @@ def test_cuda_graph_capture_and_replay(bto_lib, oracle):
     want = oracle.oracle_run("gemver", inputs2, {"M": m, "N": n}, threads=8)
     got = {"B": B.cpu().numpy(), "x": x.cpu().numpy(), "w": w.cpu().numpy()}
     assert_matches("gemver", got, want, {"M": m, "N": n}, "graph replay")
+
+
+@pytest.mark.parametrize("world", [2, 3, 8])
+def test_join_fused_exchange_emulated_ranks(bto_lib, oracle, world):
+    """The join kernel that does the cross-GPU all-reduce itself (peer-memory one-shot,
+    include/bto_b200.h 3b), with ONE GPU standing in for all ranks: the exchange
+    buffers and flag arrays of every "rank" live on this device; first every rank
+    runs its sequence with exchange_phases=1 (join + publish), then every rank with
+    exchange_phases=2 (wait -- already satisfied -- + rank-ordered reduce).  No kernel
+    ever waits on another, so this is safe on one device, and it covers the index
+    math, the flag protocol and the rank-ordered sum; only the concurrency of real
+    peers is not exercised."""
+    import ctypes
+    from paper_1205_1098_b200.sharded import GpuShardOps, row_block, shard_inputs
+    lib = _native.load()
+    ops = GpuShardOps()
+    m, n = 1030, 2050
+    capacity = 2 * max(m, n)
+    exch = [torch.zeros(capacity, dtype=torch.float64, device="cuda") for _ in range(world)]
+    flags = [torch.zeros(lib.bto_exchange_flag_bytes(world) // 4, dtype=torch.int32, device="cuda")
+             for _ in range(world)]
+    exch_ptrs = (ctypes.c_void_p * world)(*[t.data_ptr() for t in exch])
+    flag_ptrs = (ctypes.c_void_p * world)(*[t.data_ptr() for t in flags])
+    epoch = 0
+    try:
+        for name in ("bicgk", "atax", "gemver", "axpydot"):
+            graph = bto.load_graph(name)
+            ext = {"M": m} if name == "axpydot" else {"M": m, "N": n}
+            full = bto.gen_inputs(graph, ext, seed=bto.SEEDS[name])
+            want = oracle.oracle_run(name, full, ext, threads=8)
+            outs = []
+            for r in range(world):
+                lo, hi = row_block(m, r, world)
+                mine = {k: (torch.from_numpy(np.ascontiguousarray(v)).cuda() if isinstance(v, np.ndarray) else v)
+                        for k, v in shard_inputs(name, full, r, world, m).items()}
+                nan = lambda *shape: torch.full(shape, float("nan"), dtype=torch.float64, device="cuda")
+                if name == "bicgk":
+                    o = {"q": nan(hi - lo), "s": nan(n)}
+                    call = lambda t=mine, o=o: ops.bicgk_sharded(t["A"], t["p"], t["r"], o["q"], o["s"])
+                elif name == "atax":
+                    o = {"y": nan(n)}
+                    call = lambda t=mine, o=o: ops.atax_sharded(t["A"], t["x"], o["y"])
+                elif name == "gemver":
+                    o = {"B": nan(hi - lo, n), "x": nan(n), "w": nan(hi - lo)}
+                    call = lambda t=mine, o=o: ops.gemver_sharded(
+                        t["A"], t["u1"], t["v1"], t["u2"], t["v2"], t["alpha"], t["beta"], t["y"],
+                        t["z"], o["B"], o["x"], o["w"])
+                else:
+                    o = {"z": nan(hi - lo), "beta": nan(1)}
+                    call = lambda t=mine, o=o: ops.axpydot_sharded(t["w"], t["v"], t["u"], t["alpha"],
+                                                                   o["z"], o["beta"])
+                outs.append((o, call))
+            for phase, epoch0 in ((1, epoch), (2, epoch + 1)):
+                _native.set_tuning(exchange_phases=phase)
+                for r, (o, call) in enumerate(outs):
+                    _native.check(lib.bto_exchange_init(r, world, exch_ptrs, flag_ptrs, capacity, epoch0))
+                    call()
+                    torch.cuda.synchronize()
+            epoch += 1
+            from paper_1205_1098_b200.sharded import SHARDING
+            spec = SHARDING[name]
+            got = {}
+            for out_name in want:
+                if out_name in spec.sharded_out:
+                    got[out_name] = torch.cat([o[out_name] for o, _ in outs]).cpu().numpy()
+                else:
+                    first = outs[0][0][out_name]
+                    for o, _ in outs[1:]:
+                        assert torch.equal(o[out_name], first), f"{name}.{out_name}: ranks disagree"
+                    got[out_name] = first.cpu().numpy() if first.numel() > 1 else float(first[0])
+            assert_matches(name, got, want, ext, f"fused exchange, world {world}")
+    finally:
+        _native.set_tuning(exchange_phases=3)
+        _native.check(lib.bto_exchange_shutdown())
