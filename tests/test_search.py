@@ -1,0 +1,93 @@
+"""Variant search driver: budgets, determinism, incumbent, log/summary formats.
+Hermetic: the analytic cost model is the fitness (as in the reference's
+tests/test_search.py); one GPU test runs the empirical timer through it."""
+from __future__ import annotations
+
+import json
+
+import pytest
+
+import paper_1205_1098_b200 as bto
+from paper_1205_1098_b200 import cost as C
+from paper_1205_1098_b200 import search as S
+
+MACHINE = C.GpuMachineModel(extents=(("M", 32768), ("N", 32768)))
+
+
+def fitness(name):
+    return C.cached(C.AnalyticGpuCost(bto.load_graph(name), MACHINE))
+
+
+@pytest.mark.parametrize("strategy", S.STRATEGIES)
+def test_every_strategy_returns_a_valid_incumbent(strategy):
+    g = bto.load_graph("bicgk")
+    res = S.run_strategy(strategy, g, S.SearchConfig(seed=1), fitness("bicgk"))
+    assert res.best.kernel == "bicgk" and not res.best_report.failed
+    assert res.best_fitness == min(e.fitness for e in res.log)
+    assert res.evaluations == len(res.log) >= 1
+    assert res.log[0].key == "bicgk{}"                 # the shipped defaults come first
+
+
+def test_exhaustive_visits_the_whole_space_and_finds_the_minimum():
+    g = bto.load_graph("atax")
+    fn = fitness("atax")
+    res = S.run_strategy("exhaustive", g, S.SearchConfig(), fn)
+    space = C.variant_space("atax")
+    assert res.evaluations == len({v.key() for v in space} | {"atax{}"})
+    assert res.best_fitness == min(fn(v).total for v in space + [C.GpuVariant("atax")])
+    assert res.best.get("atax_fused", 1) == 1          # single pass beats two passes
+
+
+def test_budget_caps_unique_evaluations():
+    g = bto.load_graph("gemver")
+    res = S.run_strategy("ga", g, S.SearchConfig(budget=5, seed=3), fitness("gemver"))
+    assert res.evaluations <= 5
+    res0 = S.run_strategy("exhaustive", g, S.SearchConfig(budget=0), fitness("gemver"))
+    assert res0.evaluations == 1                        # the seed is always allowed
+
+
+def test_search_is_deterministic_for_a_seed():
+    g = bto.load_graph("gesummv")
+    a = S.run_strategy("ga", g, S.SearchConfig(seed=7, generations=4), fitness("gesummv"))
+    b = S.run_strategy("ga", g, S.SearchConfig(seed=7, generations=4), fitness("gesummv"))
+    assert [e.key for e in a.log] == [e.key for e in b.log] and a.best_key == b.best_key
+
+
+def test_ga_never_loses_the_incumbent():
+    g = bto.load_graph("bicgk")
+    res = S.run_strategy("ga", g, S.SearchConfig(seed=2, generations=6), fitness("bicgk"))
+    best_so_far = float("inf")
+    for e in res.log:
+        best_so_far = min(best_so_far, e.fitness)
+    assert res.best_fitness == best_so_far
+
+
+def test_log_and_summary_formats(tmp_path):
+    g = bto.load_graph("bicgk")
+    cfg = S.SearchConfig(seed=5)
+    res = S.run_strategy("random", g, cfg, fitness("bicgk"))
+    summary = S.write_run(tmp_path, g, res, cfg, "analytic")
+    lines = [json.loads(l) for l in (tmp_path / "log.jsonl").read_text().splitlines()]
+    assert len(lines) == len(res.log)
+    assert set(lines[0]) == {"key", "fitness", "generation", "elapsed_s", "strategy"}
+    assert json.loads((tmp_path / "summary.json").read_text()) == summary
+    assert set(summary) == {"kernel", "strategy", "best", "fitness", "evaluations", "cache_hits",
+                            "seed", "fitness_source"}
+    S.write_run(tmp_path, g, res, cfg, "analytic")       # append-only log
+    assert len((tmp_path / "log.jsonl").read_text().splitlines()) == 2 * len(res.log)
+
+
+def test_unknown_strategy_and_unsupported_kernel():
+    g = bto.load_graph("bicgk")
+    with pytest.raises(ValueError):
+        S.run_strategy("annealing", g, S.SearchConfig(), fitness("bicgk"))
+
+
+@pytest.mark.gpu
+def test_empirical_search_on_device():
+    g = bto.load_graph("bicgk")
+    timer = C.cached(C.GpuEmpiricalTimer(g, {"M": 4096, "N": 4096}, reps=2))
+    space = [C.GpuVariant("bicgk", (("mv_minb", b), ("mv_rows", 8))) for b in (1, 4)]
+    res = S.run_strategy("exhaustive", g, S.SearchConfig(), timer, space=space)
+    assert res.evaluations == 3 and not res.best_report.failed
+    assert all(e.elapsed_s > 0 for e in res.log)
