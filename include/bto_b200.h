@@ -159,6 +159,25 @@ int bto_gemver_sharded_async(const double *A, const double *u1, const double *v1
                              double *B, double *x, double *w, long M, long N,
                              bto_stream_t stream);
 
+/* ---- 3c. unfused primitives --------------------------------------------------
+ * Building blocks of the generic executor: a valid kernel spec with no
+ * hand-written fused sequence is evaluated statement by statement with these
+ * (what the reference's unfused organism does on the CPU).  Device pointers.
+ *   matvec : out = A x (transposed = 0, out has M entries) or A' x (1, N entries),
+ *            A row-major M x N
+ *   axpby  : mode 0 out = x*alpha; 1 out = x*alpha + y*beta; 2 out = x + y;
+ *            3 out = x - y  (n elements; every op rounded on its own)
+ *   outer  : out[i,j] = u[i]*v[j]  (row-major M x N)
+ *   dot    : *out = sum x[i]*y[i]  (device scalar)                             */
+int bto_prim_matvec_async(const double *A, const double *x, double *out, long M, long N,
+                          int transposed, bto_stream_t stream);
+int bto_prim_axpby_async(double alpha, const double *x, double beta, const double *y,
+                         double *out, long n, int mode, bto_stream_t stream);
+int bto_prim_outer_async(const double *u, const double *v, double *out, long M, long N,
+                         bto_stream_t stream);
+int bto_prim_dot_async(const double *x, const double *y, double *out, long n,
+                       bto_stream_t stream);
+
 /* ---- 4. runtime control and introspection --------------------------------- */
 int   bto_abi_version(void);
 int   bto_set_stream(bto_stream_t stream);      /* stream for section-1 calls */

@@ -54,6 +54,7 @@ EXPORTED = tuple(SIGNATURES) + tuple(f"bto_{k}_async" for k in SIGNATURES) + (
     "bto_exchange_init", "bto_exchange_shutdown", "bto_exchange_flag_bytes",
     "bto_axpydot_sharded_async", "bto_bicgk_sharded_async", "bto_atax_sharded_async",
     "bto_gemver_sharded_async",
+    "bto_prim_matvec_async", "bto_prim_axpby_async", "bto_prim_outer_async", "bto_prim_dot_async",
     "bto_last_error", "bto_last_error_string", "bto_clear_error",
     "bto_abi_version", "bto_set_stream", "bto_set_tuning", "bto_get_tuning",
     "bto_kernel_launches", "bto_bytes_min", "bto_device_info",
@@ -96,6 +97,14 @@ def load() -> ctypes.CDLL:
         sfn = getattr(lib, f"bto_{name}_sharded_async")
         sfn.restype = c_int
         sfn.argtypes = [_CT[ch] for ch in SIGNATURES[name]] + [_S]
+    lib.bto_prim_matvec_async.restype = c_int
+    lib.bto_prim_matvec_async.argtypes = [_P, _P, _P, _L, _L, c_int, _S]
+    lib.bto_prim_axpby_async.restype = c_int
+    lib.bto_prim_axpby_async.argtypes = [_D, _P, _D, _P, _P, _L, c_int, _S]
+    lib.bto_prim_outer_async.restype = c_int
+    lib.bto_prim_outer_async.argtypes = [_P, _P, _P, _L, _L, _S]
+    lib.bto_prim_dot_async.restype = c_int
+    lib.bto_prim_dot_async.argtypes = [_P, _P, _P, _L, _S]
     lib.bto_exchange_init.restype = c_int
     lib.bto_exchange_init.argtypes = [c_int, c_int, POINTER(c_void_p), POINTER(c_void_p), _L,
                                       ctypes.c_uint]

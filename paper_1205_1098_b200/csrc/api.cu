@@ -17,6 +17,7 @@
 #include "atax_cluster.cuh"
 #include "bto_b200.h"
 #include "mv_kernels.cuh"
+#include "prim_kernels.cuh"
 #include "vec_kernels.cuh"
 
 namespace {
@@ -1487,6 +1488,76 @@ int bto_gemver_sharded_async(const double *A, const double *u1, const double *v1
 {
     SHARDED_PROLOGUE();
     return seq_gemver(*ac.ctx, A, u1, v1, u2, v2, alpha, beta, y, z, B, x, w, M, N, st);
+}
+
+// ---- section 6: unfused primitives (generic executor) -------------------------------
+
+int bto_prim_matvec_async(const double *A, const double *x, double *out, long M, long N,
+                          int transposed, bto_stream_t stream)
+{
+    ASYNC_PROLOGUE();
+    BTO_TRY(check_mn(M, N));
+    DeviceCtx &c = *ac.ctx;
+    WsLayout lay;
+    MvArgs a{};
+    FinArgs f{};
+    a.A = A;
+    if (transposed) {                    // out[j] = sum_i A[i,j] x[i]
+        Pass<kFlagT> pass;
+        BTO_TRY(pass.prepare(c, M, N, mat_aligned(N, A), &lay));
+        BTO_TRY(size_ws(c, lay));
+        a.roww = x;
+        f.cmode = kColPlain; f.colout = out;
+        return pass.run(c, a, f, st);
+    }
+    Pass<kFlagN> pass;                   // out[i] = sum_j A[i,j] x[j]
+    BTO_TRY(pass.prepare(c, M, N, mat_aligned(N, A), &lay));
+    BTO_TRY(size_ws(c, lay));
+    a.colw = x;
+    f.rmode = kRowPlain; f.rowout = out;
+    return pass.run(c, a, f, st);
+}
+
+int bto_prim_axpby_async(double alpha, const double *x, double beta, const double *y,
+                         double *out, long n, int mode, bto_stream_t stream)
+{
+    ASYNC_PROLOGUE();
+    if (n < 1 || mode < 0 || mode > 3 || !x || !out || (mode != 0 && !y)) {
+        return fail(BTO_ERR_INVALID, "prim_axpby: bad arguments");
+    }
+    long grid = (n + kThreads - 1) / kThreads;
+    const long cap = (long)ac.ctx->sm_count * 16;
+    if (grid > cap) grid = cap;
+    prim_axpby_kernel<<<(unsigned)grid, kThreads, 0, st>>>(alpha, x, beta, y, out, n, mode);
+    return check_launch("prim_axpby_kernel");
+}
+
+int bto_prim_outer_async(const double *u, const double *v, double *out, long M, long N,
+                         bto_stream_t stream)
+{
+    ASYNC_PROLOGUE();
+    BTO_TRY(check_mn(M, N));
+    long grid = (M * N + kThreads - 1) / kThreads;
+    const long cap = (long)ac.ctx->sm_count * 16;
+    if (grid > cap) grid = cap;
+    prim_outer_kernel<<<(unsigned)grid, kThreads, 0, st>>>(u, v, out, M, N);
+    return check_launch("prim_outer_kernel");
+}
+
+int bto_prim_dot_async(const double *x, const double *y, double *out, long n, bto_stream_t stream)
+{
+    ASYNC_PROLOGUE();
+    if (n < 1) return fail(BTO_ERR_INVALID, "extent %ld must be >= 1", n);
+    DeviceCtx &c = *ac.ctx;
+    long grid = (n + kThreads - 1) / kThreads;
+    const long cap = (long)c.sm_count * 8;
+    if (grid > cap) grid = cap;
+    WsLayout lay;
+    const size_t off = lay.take((size_t)grid);
+    BTO_TRY(size_ws(c, lay));
+    prim_dot_kernel<<<(unsigned)grid, kThreads, 0, st>>>(
+        x, y, out, reinterpret_cast<double *>(c.ws + off), c.tickets + 1, n);
+    return check_launch("prim_dot_kernel");
 }
 
 // ---- section 4: control ----------------------------------------------------------

@@ -95,12 +95,25 @@ def _c_params(inputs, outputs, extent_names) -> tuple[tuple[str, str], ...]:
     return tuple(out)
 
 
-def gpu_kernel(graph) -> GeneratedKernel:
-    """The hand-written sm_100a sequence implementing `graph`'s spec."""
+def gpu_kernel(graph, allow_generic: bool = True) -> GeneratedKernel:
+    """The kernel handle for `graph`'s spec: the hand-written fused sm_100a
+    sequence when the spec is one of the corpus structures, otherwise (unless
+    `allow_generic=False`, which raises UnsupportedKernelError) the generic
+    unfused executor of generic.py -- the analogue of the reference compiling
+    ANY valid spec, with the unfused organism."""
+    from .spec import UnsupportedKernelError
     typed = _as_typed(graph) if not hasattr(graph, "data") else None
     spec = typed.spec if typed is not None else graph.spec
     if typed is not None:
-        name = match_corpus(spec)
+        try:
+            name = match_corpus(spec)
+        except UnsupportedKernelError:
+            if not allow_generic:
+                raise
+            return GeneratedKernel(
+                source="libbto_b200:generic", kernel_name=spec.name.lower(),
+                params=_c_params(spec.inputs, spec.outputs, typed.extent_names),
+                organism_key="gpu-unfused{" + " ".join(str(i + 1) for i in range(len(spec.statements))) + "}")
         extent_names = typed.extent_names
     else:
         # the reference's DataflowGraph: re-parse its printed spec with our parser
@@ -242,6 +255,9 @@ def run_kernel(binary, kernel: GeneratedKernel, graph, inputs: dict,
     numpy in -> numpy out (host buffers cross PCIe inside the call);
     torch CUDA tensors in -> CUDA tensors out, synchronised before returning.
     """
+    if kernel.source.endswith(":generic"):
+        from .generic import run_generic
+        return run_generic(_as_typed(graph), inputs, extents)
     lib, args, out_bufs, keep, on_gpu = _marshal(binary, kernel, graph, inputs, extents)
     fn = getattr(lib, kernel.kernel_name)
     if on_gpu:

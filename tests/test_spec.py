@@ -51,10 +51,14 @@ def test_renamed_spec_still_matches():
     assert S.match_corpus(S.parse_kernel(text)) == "bicgk"
 
 
-def test_unknown_structure_is_rejected_loudly():
+def test_unknown_structure_gets_the_generic_executor_or_a_loud_error():
     text = "T in: a : vector(column), b : vector(column) out: c : vector(column) { c = a - b }"
+    typed = S.infer_shapes(S.parse_kernel(text))
     with pytest.raises(S.UnsupportedKernelError):
-        bto.gpu_kernel(S.infer_shapes(S.parse_kernel(text)))
+        bto.gpu_kernel(typed, allow_generic=False)
+    k = bto.gpu_kernel(typed)
+    assert k.source == "libbto_b200:generic" and k.kernel_name == "t"
+    assert k.organism_key == "gpu-unfused{1}"
 
 
 def test_declaration_order_matters():
