@@ -242,7 +242,10 @@ class Suite:
         if need_mat:
             self.A = rnd(self.rows, n)
             self.Bm = rnd(self.rows, n)            # GEMVER output; GESUMMV's 2nd input lives here
-        self.vecN = [rnd(n) for _ in range(4)]     # p/x, v1, v2, z
+        # column-indexed vectors are REPLICATED: the same values on every rank
+        rep = torch.Generator(device=dev).manual_seed(99)
+        self.vecN = [torch.rand(n, dtype=torch.float64, device=dev, generator=rep) * 2 - 1
+                     for _ in range(4)]            # p/x, v1, v2, z
         self.vecM = [rnd(self.rows) for _ in range(4)]   # r/y, u1, u2
         self.q = torch.empty(self.rows, dtype=torch.float64, device=dev)
         self.s = torch.empty(n, dtype=torch.float64, device=dev)

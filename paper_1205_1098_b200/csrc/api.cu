@@ -277,7 +277,7 @@ bool mv_shape_ok(int R, int V)
     if (FLAGS & kFlagN2) return false;
     if (R == 16 && V == 1) return true;
     if (R == 32 && V == 1) return (FLAGS & kFlagN) == 0;
-    if (R == 8 && V == 2) return FLAGS == kFlagN;
+    if (R == 8 && V == 2) return FLAGS == kFlagN || FLAGS == (kFlagT | kFlagRank2);
     return false;
 }
 
@@ -290,7 +290,7 @@ MvKernel mv_kernel_ptr(int R, int V, bool aligned, int minb)
         if constexpr ((FLAGS & kFlagN) == 0) {
             if (R == 32 && V == 1) return mv_kernel_minb<FLAGS, 32, 1>(minb);
         }
-        if constexpr (FLAGS == kFlagN) {
+        if constexpr (FLAGS == kFlagN || FLAGS == (kFlagT | kFlagRank2)) {
             if (R == 8 && V == 2) return mv_kernel_minb<FLAGS, 8, 2>(minb);
         }
     }
