@@ -138,7 +138,7 @@ def _pass_geometry(kind: str, variant: GpuVariant, machine: GpuMachineModel, M: 
     strip = 512 * vec
     nstrips = -(-N // strip)
     units = -(-M // rows) * nstrips
-    grid = max(1, min(machine.sm_count * per_sm, units))
+    grid = max(1, min(machine.sm_count * per_sm, -(-units // 4)))    # >= 4 units per CTA
     slots = min(grid, -(-grid // nstrips) + 1)
     matrices = 2 if kind == "NN" else 1
     inflight = resident * 256 * rows * vec * 16 * matrices     # bytes in flight per SM

@@ -90,6 +90,7 @@ struct DeviceCtx {
     cudaStream_t stream = nullptr; // stream of the section-1 entry points
     std::map<const void *, int> occupancy;
     std::map<const void *, int> max_clusters;
+    std::map<const void *, size_t> static_smem;
     // NVLink exchange fused into the join (row-sharded runtime)
     bool exch_ready = false, exch_active = false;
     int exch_rank = 0, exch_world = 1;
@@ -108,11 +109,15 @@ Tuning g_tuning;
 
 int get_ctx(DeviceCtx **out)
 {
-    int ndev = 0;
-    cudaError_t e = cudaGetDeviceCount(&ndev);
-    if (e != cudaSuccess || ndev == 0) {
-        return fail(BTO_ERR_NO_DEVICE, "no CUDA device: %s",
-                    e == cudaSuccess ? "device count is 0" : cudaGetErrorString(e));
+    static bool have_device = false;     // guarded by g_mu (every caller holds it)
+    if (!have_device) {
+        int ndev = 0;
+        cudaError_t e = cudaGetDeviceCount(&ndev);
+        if (e != cudaSuccess || ndev == 0) {
+            return fail(BTO_ERR_NO_DEVICE, "no CUDA device: %s",
+                        e == cudaSuccess ? "device count is 0" : cudaGetErrorString(e));
+        }
+        have_device = true;
     }
     int dev = 0;
     CUDA_TRY(cudaGetDevice(&dev));
@@ -333,7 +338,10 @@ int plan_mv(DeviceCtx &c, long M, long N, bool aligned, MvPlan *p)
     long per_sm = g_tuning.grid_per_sm > 0 ? g_tuning.grid_per_sm : dflt.grid_per_sm;
     if (per_sm <= 0) per_sm = occ;
     long grid = (long)c.sm_count * per_sm;
-    if (grid > p->total_units) grid = p->total_units;
+    // small matrices: at least 4 units per CTA, so that few CTAs share a strip and
+    // the join (one partial per CTA and strip) stays short
+    const long by_work = (p->total_units + 3) / 4;
+    if (grid > by_work) grid = by_work;
     if (grid < 1) grid = 1;
     p->grid = grid;
     long slots = 1;
@@ -589,10 +597,14 @@ int plan_atax(DeviceCtx &c, const double *A, const double *x, long M, long N, At
     if (!fn) return BTO_OK;
     const int rg = atax_rows_of(kmax, small);
     const size_t stage = (size_t)rg * W * sizeof(double);
-    cudaFuncAttributes fattr;
-    CUDA_TRY(cudaFuncGetAttributes(&fattr, fn));
+    auto sm = c.static_smem.find(reinterpret_cast<const void *>(fn));
+    if (sm == c.static_smem.end()) {
+        cudaFuncAttributes fattr;
+        CUDA_TRY(cudaFuncGetAttributes(&fattr, fn));
+        sm = c.static_smem.emplace(reinterpret_cast<const void *>(fn), fattr.sharedSizeBytes).first;
+    }
     // 227 KiB per CTA on sm_100, minus the kernel's static shared memory
-    const size_t budget = ((227 * 1024 - fattr.sharedSizeBytes) / 1024) * 1024;
+    const size_t budget = ((227 * 1024 - sm->second) / 1024) * 1024;
     int S = (int)(budget / stage);
     if (S > 8) S = 8;
     if (g_tuning.atax_stages > 0 && g_tuning.atax_stages < S) S = (int)g_tuning.atax_stages;

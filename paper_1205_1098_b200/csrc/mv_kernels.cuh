@@ -308,15 +308,32 @@ struct FinArgs {
     int col_blocks;           // CTAs [0, col_blocks) do columns, the rest rows
 };
 
+// Sum of `count` partials `stride` apart in a FIXED order that exposes 8
+// independent load/add chains (the partials sit in L2; a single dependent chain
+// would pay the L2 latency `count` times): lane k takes partials k, k+8, ..;
+// the eight lane sums are added pairwise.
+__device__ __forceinline__ double strided_sum(const double *p, long count, long stride)
+{
+    double acc[8] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+    long k = 0;
+    for (; k + 8 <= count; k += 8) {
+#pragma unroll
+        for (int u = 0; u < 8; ++u) acc[u] += p[(k + u) * stride];
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {          // tail, predicated so acc[] stays in registers
+        if (k + u < count) acc[u] += p[(k + u) * stride];
+    }
+    return ((acc[0] + acc[1]) + (acc[2] + acc[3])) + ((acc[4] + acc[5]) + (acc[6] + acc[7]));
+}
+
 // ascending join of the column partials of column j (no epilogue)
 __device__ __forceinline__ double join_column(const FinArgs &f, long j)
 {
     const long strip = j / f.strip_width;
     const long first = split_owner(f.total_units, f.grid, strip * f.units_per_strip);
     const long last = split_owner(f.total_units, f.grid, (strip + 1) * f.units_per_strip - 1);
-    double s = f.colpart[j];
-    for (long k = 1; k <= last - first; ++k) s += f.colpart[k * f.N + j];
-    return s;
+    return strided_sum(f.colpart + j, last - first + 1, f.N);
 }
 
 __device__ __forceinline__ double column_epilogue(const FinArgs &f, long j, double s)
@@ -332,11 +349,9 @@ __device__ __forceinline__ double column_epilogue(const FinArgs &f, long j, doub
 // join + epilogue of row i
 __device__ __forceinline__ void finalize_row(const FinArgs &f, long i)
 {
-    double s = f.rowpart[i];
-    for (int c = 1; c < f.nstrips; ++c) s += f.rowpart[(long)c * f.M + i];
+    double s = strided_sum(f.rowpart + i, f.nstrips, f.M);
     if (f.rmode == kRowGesummv) {         // t1 = t0*alpha ; t3 = t2*beta ; y = t1 + t3
-        double s2 = f.rowpart2[i];
-        for (int c = 1; c < f.nstrips; ++c) s2 += f.rowpart2[(long)c * f.M + i];
+        const double s2 = strided_sum(f.rowpart2 + i, f.nstrips, f.M);
         s = __dadd_rn(__dmul_rn(s, f.ralpha), __dmul_rn(s2, f.rbeta));
     } else if (f.rmode == kRowScale) {    // w = t5*alpha
         s = __dmul_rn(s, f.ralpha);
