@@ -69,6 +69,7 @@ struct Tuning {
     long atax_cluster = 0;   // cluster size of the fused ATAX (0 = auto | 1 | 2 | 4 | 8 | 16)
     long atax_stages = 0;    // TMA ring depth (0 = as many as fit, at most 8)
     long atax_rows = 0;      // 0: 16 double2 per thread per panel, 1: half-height panels
+    long pdl = 1;            // joins launched as programmatic dependents of their producer
     long debug = 0;          // print launch plans to stderr
     long exchange_phases = 3;    // bit 0 publish, bit 1 wait+reduce (tests emulate ranks with 1, 2)
     long host_pipeline = 1;  // overlap H2D / compute / D2H in row panels for host operands
@@ -370,6 +371,26 @@ int launch_mv(const MvPlan &p, const MvArgs &a, cudaStream_t stream)
     return check_launch("mv_tile_kernel");
 }
 
+// Launch `kernel(arg)` as a programmatic dependent of the previous kernel in the
+// stream (the kernel itself calls griddepcontrol.wait before touching memory).
+template <typename Arg>
+int launch_dependent(void (*kernel)(const Arg), unsigned grid, const Arg &arg,
+                     cudaStream_t stream, const char *what)
+{
+    cudaLaunchConfig_t cfg;
+    memset(&cfg, 0, sizeof(cfg));
+    cfg.gridDim = dim3(grid, 1, 1);
+    cfg.blockDim = dim3(kThreads, 1, 1);
+    cfg.stream = stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = g_tuning.pdl ? 1 : 0;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    CUDA_TRY(cudaLaunchKernelEx(&cfg, kernel, arg));
+    return check_launch(what);
+}
+
 // Launch the join of `f` (geometry already filled in).  While a sharded
 // entry point is active and the join has a column side, the cross-GPU exchange
 // is fused into it (join_exchange_kernel); otherwise the plain local join runs.
@@ -390,13 +411,12 @@ int launch_join(DeviceCtx &c, FinArgs f, cudaStream_t stream)
         e.rank = c.exch_rank;
         e.world = c.exch_world;
         e.phases = (int)g_tuning.exchange_phases;
-        join_exchange_kernel<<<(unsigned)(kExchCtas + rb), kThreads, 0, stream>>>(e);
-        return check_launch("join_exchange_kernel");
+        return launch_dependent(join_exchange_kernel, (unsigned)(kExchCtas + rb), e, stream,
+                                "join_exchange_kernel");
     }
     const long cb = f.cmode != kColNone ? (f.N + kThreads - 1) / kThreads : 0;
     f.col_blocks = (int)cb;
-    finalize_kernel<<<(unsigned)(cb + rb), kThreads, 0, stream>>>(f);
-    return check_launch("finalize_kernel");
+    return launch_dependent(finalize_kernel, (unsigned)(cb + rb), f, stream, "finalize_kernel");
 }
 
 int launch_finalize(DeviceCtx &c, const MvPlan &p, FinArgs f, long M, long N, cudaStream_t stream)
@@ -1012,8 +1032,7 @@ int join_partials(const double *parts, long count, long n, int cmode, double sca
     f.grid = count;
     f.rmode = kRowNone;
     f.col_blocks = (int)((n + kThreads - 1) / kThreads);
-    finalize_kernel<<<(unsigned)f.col_blocks, kThreads, 0, st>>>(f);
-    return check_launch("finalize_kernel");
+    return launch_dependent(finalize_kernel, (unsigned)f.col_blocks, f, st, "finalize_kernel");
 }
 
 // GEMVER with A and B in host memory.  d* are device copies (dA, dB reserved but
@@ -1596,6 +1615,7 @@ static long *tuning_slot(const char *key)
     if (!strcmp(key, "atax_stages")) return &g_tuning.atax_stages;
     if (!strcmp(key, "atax_rows")) return &g_tuning.atax_rows;
     if (!strcmp(key, "debug")) return &g_tuning.debug;
+    if (!strcmp(key, "pdl")) return &g_tuning.pdl;
     if (!strcmp(key, "exchange_phases")) return &g_tuning.exchange_phases;
     if (!strcmp(key, "host_pipeline")) return &g_tuning.host_pipeline;
     if (!strcmp(key, "host_panel_mib")) return &g_tuning.host_panel_mib;

@@ -361,9 +361,18 @@ __device__ __forceinline__ void finalize_row(const FinArgs &f, long i)
     f.rowout[i] = s;
 }
 
+// Programmatic dependent launch: the join is launched while the streaming
+// kernel is still running and waits here until that kernel's writes are
+// visible, so its launch latency hides under the producer's tail.
+__device__ __forceinline__ void wait_for_producer_grid()
+{
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+}
+
 __global__ void __launch_bounds__(kThreads)
 finalize_kernel(const FinArgs f)
 {
+    wait_for_producer_grid();
     if ((int)blockIdx.x < f.col_blocks) {
         const long j = (long)blockIdx.x * kThreads + threadIdx.x;
         if (j < f.N) f.colout[j] = column_epilogue(f, j, join_column(f, j));
@@ -427,6 +436,7 @@ __device__ __forceinline__ double ld_relaxed_sys(const double *p)
 __global__ void __launch_bounds__(kThreads)
 join_exchange_kernel(const ExchArgs e)
 {
+    wait_for_producer_grid();
     const FinArgs &f = e.fin;
     if ((int)blockIdx.x >= kExchCtas) {          // row side: purely local
         const long i = (long)(blockIdx.x - kExchCtas) * kThreads + threadIdx.x;
