@@ -203,6 +203,26 @@ int check_launch(const char *what)
     return BTO_OK;
 }
 
+// Launch `kernel(arg)` as a programmatic dependent of the previous kernel in the
+// stream (the kernel itself calls griddepcontrol.wait before touching memory).
+template <typename Arg>
+int launch_dependent(void (*kernel)(const Arg), unsigned grid, const Arg &arg,
+                     cudaStream_t stream, const char *what)
+{
+    cudaLaunchConfig_t cfg;
+    memset(&cfg, 0, sizeof(cfg));
+    cfg.gridDim = dim3(grid, 1, 1);
+    cfg.blockDim = dim3(kThreads, 1, 1);
+    cfg.stream = stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = g_tuning.pdl ? 1 : 0;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    CUDA_TRY(cudaLaunchKernelEx(&cfg, kernel, arg));
+    return check_launch(what);
+}
+
 bool aligned16(const void *p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
 
 // ---------------------------------------------------------------------------
@@ -242,8 +262,7 @@ int launch_vec(DeviceCtx &c, VecArgs g, cudaStream_t stream)
         g.partials = reinterpret_cast<double *>(c.ws + off);
         g.ticket = c.tickets;
     }
-    fn<<<(unsigned)grid, kThreads, 0, stream>>>(g);
-    return check_launch("vec_kernel");
+    return launch_dependent(fn, (unsigned)grid, g, stream, "vec_kernel");
 }
 
 // ---------------------------------------------------------------------------
@@ -367,28 +386,7 @@ void fill_geometry(const MvPlan &p, MvArgs *a, long M, long N)
 
 int launch_mv(const MvPlan &p, const MvArgs &a, cudaStream_t stream)
 {
-    p.fn<<<(unsigned)p.grid, kThreads, 0, stream>>>(a);
-    return check_launch("mv_tile_kernel");
-}
-
-// Launch `kernel(arg)` as a programmatic dependent of the previous kernel in the
-// stream (the kernel itself calls griddepcontrol.wait before touching memory).
-template <typename Arg>
-int launch_dependent(void (*kernel)(const Arg), unsigned grid, const Arg &arg,
-                     cudaStream_t stream, const char *what)
-{
-    cudaLaunchConfig_t cfg;
-    memset(&cfg, 0, sizeof(cfg));
-    cfg.gridDim = dim3(grid, 1, 1);
-    cfg.blockDim = dim3(kThreads, 1, 1);
-    cfg.stream = stream;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    attr[0].val.programmaticStreamSerializationAllowed = g_tuning.pdl ? 1 : 0;
-    cfg.attrs = attr;
-    cfg.numAttrs = 1;
-    CUDA_TRY(cudaLaunchKernelEx(&cfg, kernel, arg));
-    return check_launch(what);
+    return launch_dependent(p.fn, (unsigned)p.grid, a, stream, "mv_tile_kernel");
 }
 
 // Launch the join of `f` (geometry already filled in).  While a sharded
@@ -584,12 +582,14 @@ int fill_launch_config(const AtaxPlan &p, cudaLaunchConfig_t *cfg, cudaLaunchAtt
     cfg->blockDim = dim3(kAtaxThreads, 1, 1);
     cfg->dynamicSmemBytes = p.smem;
     cfg->stream = stream;
-    attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = (unsigned)p.C;
-    attr[0].val.clusterDim.y = 1;
-    attr[0].val.clusterDim.z = 1;
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = g_tuning.pdl ? 1 : 0;
+    attr[1].id = cudaLaunchAttributeClusterDimension;
+    attr[1].val.clusterDim.x = (unsigned)p.C;
+    attr[1].val.clusterDim.y = 1;
+    attr[1].val.clusterDim.z = 1;
     cfg->attrs = attr;
-    cfg->numAttrs = p.C > 1 ? 1 : 0;
+    cfg->numAttrs = p.C > 1 ? 2 : 1;
     return BTO_OK;
 }
 
@@ -648,7 +648,7 @@ int plan_atax(DeviceCtx &c, const double *A, const double *x, long M, long N, At
             probe.nclusters = c.sm_count / C;
             probe.smem = budget;
             cudaLaunchConfig_t cfg;
-            cudaLaunchAttribute attr[1];
+            cudaLaunchAttribute attr[2];
             fill_launch_config(probe, &cfg, attr, nullptr);
             CUDA_TRY(cudaOccupancyMaxActiveClusters(&n, fn, &cfg));
         } else {
@@ -680,7 +680,7 @@ int seq_atax_fused(DeviceCtx &c, const AtaxPlan &p, const double *A, const doubl
                 p.C, p.KMAX, p.RG, p.W, p.S, p.smem, p.nclusters);
     }
     cudaLaunchConfig_t cfg;
-    cudaLaunchAttribute attr[1];
+    cudaLaunchAttribute attr[2];
     fill_launch_config(p, &cfg, attr, st);
     CUDA_TRY(cudaLaunchKernelEx(&cfg, p.fn, a));
     BTO_TRY(check_launch("atax_cluster_kernel"));

@@ -172,6 +172,7 @@ atax_cluster_kernel(const AtaxArgs a)
     __shared__ double warp_part[2][TR][kWarps];                  // phase-1 warp sums
     __shared__ double part[kAtaxSlots][TR][C];                   // pushed by every CTA of the cluster
 
+    wait_for_producer_grid();
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const uint32_t rank = C > 1 ? cluster_rank() : 0u;
     const long cluster = C > 1 ? (long)cluster_index() : (long)blockIdx.x;

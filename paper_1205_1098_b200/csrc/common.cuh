@@ -76,6 +76,15 @@ __device__ __forceinline__ double ld_cg(const double *p)
     return v;
 }
 
+// Programmatic dependent launch: every kernel of the library is launched while
+// its predecessor in the stream is still running and waits here, before it
+// touches memory, until that grid has completed and flushed; the launch latency
+// hides under the predecessor's tail.  A no-op for a normally launched kernel.
+__device__ __forceinline__ void wait_for_producer_grid()
+{
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+}
+
 // ---- reductions with a fixed order ------------------------------------------
 __device__ __forceinline__ double warp_sum(double v)
 {

@@ -184,6 +184,7 @@ mv_tile_kernel(const MvArgs a)
 
     __shared__ double red[2][kRowSets][kWarps][R];
 
+    wait_for_producer_grid();
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const long G = gridDim.x, cta = blockIdx.x;
     const long u_begin = split_begin(a.total_units, G, cta);
@@ -359,14 +360,6 @@ __device__ __forceinline__ void finalize_row(const FinArgs &f, long i)
         s = __dadd_rn(__dmul_rn(s, f.ralpha), __dmul_rn(f.rowy[i], f.rbeta));
     }
     f.rowout[i] = s;
-}
-
-// Programmatic dependent launch: the join is launched while the streaming
-// kernel is still running and waits here until that kernel's writes are
-// visible, so its launch latency hides under the producer's tail.
-__device__ __forceinline__ void wait_for_producer_grid()
-{
-    asm volatile("griddepcontrol.wait;" ::: "memory");
 }
 
 __global__ void __launch_bounds__(kThreads)

@@ -47,6 +47,7 @@ vec_kernel(const VecArgs g)
 {
     constexpr bool kHasC = OP != kWaxpby;
     constexpr bool kDot = OP == kAxpydot;
+    wait_for_producer_grid();
     const long tid = (long)blockIdx.x * kThreads + threadIdx.x;
     const long nthreads = (long)gridDim.x * kThreads;
     double acc = 0.0;
