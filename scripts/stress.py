@@ -1,0 +1,48 @@
+#!/usr/bin/env python
+"""Race hunt: every sequence repeated many times must return bit-identical results
+(all reductions have a fixed order; a rare race in the smem double-buffering, the
+TMA ring or the DSMEM exchange would show up as a sporadic difference)."""
+import sys
+import time
+from pathlib import Path
+
+import torch
+
+REPO = Path(__file__).resolve().parent.parent
+sys.path.insert(0, str(REPO))
+import paper_1205_1098_b200 as bto  # noqa: E402
+from paper_1205_1098_b200 import _native  # noqa: E402
+
+torch.cuda.set_device(0)
+_native.load()
+reps = int(sys.argv[1]) if len(sys.argv) > 1 else 300
+bad = 0
+t0 = time.time()
+cases = []
+for name in ("bicgk", "gesummv", "gemver", "atax", "batax", "dgemvt", "axpydot"):
+    for (m, n) in [(4096, 4096), (1000, 8192), (8192, 1026), (333, 32768)]:
+        cases.append((name, m, n, {}))
+for c in (1, 2, 4, 8, 16):
+    for (m, n) in [(2048, 4096), (777, 16384), (5000, 2050)]:
+        for rows in (0, 1):
+            cases.append(("atax", m, n, {"atax_cluster": c, "atax_rows": rows}))
+for name, m, n, tune in cases:
+    g = bto.load_graph(name)
+    k = bto.gpu_kernel(g)
+    ext = {"M": m * 64} if g.extent_names == ("M",) else {"M": m, "N": n}
+    inp = bto.gen_inputs(g, ext, seed=1)
+    dev = {a: (torch.from_numpy(v).cuda() if hasattr(v, "shape") else v) for a, v in inp.items()}
+    _native.set_tuning(atax_cluster=0, atax_rows=0)
+    if tune:
+        _native.set_tuning(**tune)
+    first = bto.run_kernel(bto.library_path(), k, g, dev, ext)
+    diffs = 0
+    for _ in range(reps):
+        out = bto.run_kernel(bto.library_path(), k, g, dev, ext)
+        for key, val in first.items():
+            same = torch.equal(out[key], val) if hasattr(val, "shape") else out[key] == val
+            diffs += 0 if same else 1
+    bad += diffs
+    print(f"{name:8s} {ext} {tune}: {reps} repeats, {diffs} differing outputs", flush=True)
+print(f"stress done in {time.time() - t0:.0f}s, total differing outputs: {bad}")
+sys.exit(1 if bad else 0)
