@@ -1,0 +1,223 @@
+// host_context.cuh -- error channel, per-device context, cached workspace, launch helpers
+// Part of the host side of libbto_b200.so; included by api.cu (one translation unit).
+#pragma once
+#include <atomic>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <mutex>
+#include <vector>
+
+#include "bto_b200.h"
+#include "common.cuh"
+
+namespace bto_host {
+namespace {          // internal linkage: nothing here is part of the C ABI
+
+using namespace bto;
+
+// ---------------------------------------------------------------------------
+// error channel
+
+thread_local int g_err = BTO_OK;
+thread_local char g_errmsg[512] = "";
+std::atomic<long> g_launches{0};
+
+int fail(int code, const char *fmt, ...)
+{
+    g_err = code;
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(g_errmsg, sizeof(g_errmsg), fmt, ap);
+    va_end(ap);
+    return code;
+}
+
+#define CUDA_TRY(expr)                                                         \
+    do {                                                                       \
+        cudaError_t e_ = (expr);                                               \
+        if (e_ != cudaSuccess)                                                 \
+            return fail(BTO_ERR_CUDA, "%s failed: %s", #expr,                  \
+                        cudaGetErrorString(e_));                               \
+    } while (0)
+
+#define BTO_TRY(expr)                                                          \
+    do {                                                                       \
+        int rc_ = (expr);                                                      \
+        if (rc_ != BTO_OK) return rc_;                                         \
+    } while (0)
+
+// ---------------------------------------------------------------------------
+// per-device context
+
+struct Tuning {
+    long mv_rows = 0;        // rows per unit (0 = per-kind default | 8 | 16)
+    long mv_vec = 0;         // double2 per thread per row (0 = per-kind default | 1 | 2)
+    long grid_per_sm = 0;    // CTAs per SM for the matrix kernels (0 = per-kind default)
+    long mv_minb = 0;        // __launch_bounds__ min CTAs/SM variant (0 = default | 1 2 3 4 6)
+    long vec_unroll = 2;     // independent double2 triples in flight (1 | 2 | 4)
+    long vec_grid_per_sm = 0;
+    long atax_fused = 1;     // 1: single-pass cluster kernel when applicable, 0: two passes
+    long atax_cluster = 0;   // cluster size of the fused ATAX (0 = auto | 1 | 2 | 4 | 8 | 16)
+    long atax_stages = 0;    // TMA ring depth (0 = as many as fit, at most 8)
+    long atax_rows = 0;      // 0: 16 double2 per thread per panel, 1: half-height panels
+    long pdl = 1;            // joins launched as programmatic dependents of their producer
+    long debug = 0;          // print launch plans to stderr
+    long exchange_phases = 3;    // bit 0 publish, bit 1 wait+reduce (tests emulate ranks with 1, 2)
+    long host_pipeline = 1;  // overlap H2D / compute / D2H in row panels for host operands
+    long host_panel_mib = 256;   // panel size of that pipeline
+};
+
+struct DeviceCtx {
+    bool ready = false;
+    int device = -1;
+    int sm_count = 0;
+    int max_threads_per_sm = 0;
+    long l2_bytes = 0;
+    long global_bytes = 0;
+    char *ws = nullptr;            // partial sums
+    size_t ws_bytes = 0;
+    unsigned int *tickets = nullptr;
+    char *arena = nullptr;         // device staging for host arguments
+    size_t arena_bytes = 0;
+    cudaStream_t stream = nullptr; // stream of the section-1 entry points
+    std::map<const void *, int> occupancy;
+    std::map<const void *, int> max_clusters;
+    std::map<const void *, size_t> static_smem;
+    // NVLink exchange fused into the join (row-sharded runtime)
+    bool exch_ready = false, exch_active = false;
+    int exch_rank = 0, exch_world = 1;
+    long exch_capacity = 0;            // doubles per rank, both parity halves together
+    double **exch_bufs = nullptr;      // device array [world] of peer-mapped buffers
+    unsigned int **exch_flags = nullptr;
+    unsigned int exch_epoch = 0;
+    // host-pointer pipeline: copy-in and copy-out streams, reusable events
+    cudaStream_t copy_in = nullptr, copy_out = nullptr;
+    std::vector<cudaEvent_t> events;
+};
+
+std::mutex g_mu;
+DeviceCtx g_ctx[64];
+Tuning g_tuning;
+
+int get_ctx(DeviceCtx **out)
+{
+    static bool have_device = false;     // guarded by g_mu (every caller holds it)
+    if (!have_device) {
+        int ndev = 0;
+        cudaError_t e = cudaGetDeviceCount(&ndev);
+        if (e != cudaSuccess || ndev == 0) {
+            return fail(BTO_ERR_NO_DEVICE, "no CUDA device: %s",
+                        e == cudaSuccess ? "device count is 0" : cudaGetErrorString(e));
+        }
+        have_device = true;
+    }
+    int dev = 0;
+    CUDA_TRY(cudaGetDevice(&dev));
+    if (dev < 0 || dev >= 64) return fail(BTO_ERR_INVALID, "device index %d", dev);
+    DeviceCtx &c = g_ctx[dev];
+    if (!c.ready) {
+        cudaDeviceProp prop;
+        CUDA_TRY(cudaGetDeviceProperties(&prop, dev));
+        if (prop.major < 10) {
+            return fail(BTO_ERR_NO_DEVICE,
+                        "device %d is sm_%d%d; this library is built for sm_100a only",
+                        dev, prop.major, prop.minor);
+        }
+        c.device = dev;
+        c.sm_count = prop.multiProcessorCount;
+        c.max_threads_per_sm = prop.maxThreadsPerMultiProcessor;
+        c.l2_bytes = prop.l2CacheSize;
+        c.global_bytes = (long)prop.totalGlobalMem;
+        CUDA_TRY(cudaMalloc(&c.tickets, 64 * sizeof(unsigned int)));
+        CUDA_TRY(cudaMemset(c.tickets, 0, 64 * sizeof(unsigned int)));
+        c.ready = true;
+    }
+    *out = &c;
+    return BTO_OK;
+}
+
+int grow(char **buf, size_t *have, size_t want, const char *what)
+{
+    if (want <= *have) return BTO_OK;
+    // nothing of ours may still be running on the old buffer
+    CUDA_TRY(cudaDeviceSynchronize());
+    if (*buf) CUDA_TRY(cudaFree(*buf));
+    *buf = nullptr;
+    *have = 0;
+    size_t bytes = want + want / 8 + (1u << 20);
+    cudaError_t e = cudaMalloc(buf, bytes);
+    if (e != cudaSuccess) {
+        bytes = want;
+        e = cudaMalloc(buf, bytes);
+    }
+    if (e != cudaSuccess) {
+        return fail(BTO_ERR_ALLOC, "cannot allocate %zu bytes of %s: %s", want, what,
+                    cudaGetErrorString(e));
+    }
+    *have = bytes;
+    return BTO_OK;
+}
+
+// bump allocator over the workspace; sizes first, pointers after ensure()
+struct WsLayout {
+    size_t total = 0;
+    size_t take(size_t doubles)
+    {
+        const size_t off = total;
+        total += ((doubles * sizeof(double) + 255) / 256) * 256;
+        return off;
+    }
+};
+
+template <typename K>
+int occupancy_of(DeviceCtx &c, K kernel, int *occ)
+{
+    const void *key = reinterpret_cast<const void *>(kernel);
+    auto it = c.occupancy.find(key);
+    if (it == c.occupancy.end()) {
+        int n = 0;
+        CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, kernel, kThreads, 0));
+        if (n < 1) n = 1;
+        it = c.occupancy.emplace(key, n).first;
+    }
+    *occ = it->second;
+    return BTO_OK;
+}
+
+int check_launch(const char *what)
+{
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) {
+        return fail(BTO_ERR_CUDA, "launch of %s failed: %s", what, cudaGetErrorString(e));
+    }
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    return BTO_OK;
+}
+
+// Launch `kernel(arg)` as a programmatic dependent of the previous kernel in the
+// stream (the kernel itself calls griddepcontrol.wait before touching memory).
+template <typename Arg>
+int launch_dependent(void (*kernel)(const Arg), unsigned grid, const Arg &arg,
+                     cudaStream_t stream, const char *what)
+{
+    cudaLaunchConfig_t cfg;
+    memset(&cfg, 0, sizeof(cfg));
+    cfg.gridDim = dim3(grid, 1, 1);
+    cfg.blockDim = dim3(kThreads, 1, 1);
+    cfg.stream = stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = g_tuning.pdl ? 1 : 0;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    CUDA_TRY(cudaLaunchKernelEx(&cfg, kernel, arg));
+    return check_launch(what);
+}
+
+bool aligned16(const void *p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+
+}  // namespace
+}  // namespace bto_host

@@ -1,0 +1,276 @@
+// host_plan.cuh -- launch planning: vector kernels, the matrix tile engine, joins
+// Part of the host side of libbto_b200.so; included by api.cu (one translation unit).
+#pragma once
+#include "host_context.cuh"
+#include "mv_kernels.cuh"
+#include "vec_kernels.cuh"
+
+namespace bto_host {
+namespace {          // internal linkage: nothing here is part of the C ABI
+
+using namespace bto;
+
+// ---------------------------------------------------------------------------
+// vector kernels
+
+using VecKernel = void (*)(const VecArgs);
+
+template <int OP>
+VecKernel vec_kernel_ptr(int unroll, bool aligned)
+{
+    if (!aligned) return vec_kernel<OP, 1, false>;
+    switch (unroll) {
+        case 1: return vec_kernel<OP, 1, true>;
+        case 2: return vec_kernel<OP, 2, true>;
+        default: return vec_kernel<OP, 4, true>;
+    }
+}
+
+template <int OP>
+int launch_vec(DeviceCtx &c, VecArgs g, cudaStream_t stream)
+{
+    if (g.n < 1) return fail(BTO_ERR_INVALID, "extent M=%ld must be >= 1", g.n);
+    const bool aligned = aligned16(g.a) && aligned16(g.b) && aligned16(g.out) &&
+                         (OP == kWaxpby || aligned16(g.c));
+    VecKernel fn = vec_kernel_ptr<OP>((int)g_tuning.vec_unroll, aligned);
+    int occ = 1;
+    BTO_TRY(occupancy_of(c, fn, &occ));
+    const long per_sm = g_tuning.vec_grid_per_sm > 0 ? g_tuning.vec_grid_per_sm : occ;
+    long grid = (long)c.sm_count * per_sm;
+    const long work = ((aligned ? (g.n + 1) / 2 : g.n) + kThreads - 1) / kThreads;
+    if (grid > work) grid = work;
+    if (grid < 1) grid = 1;
+    if (OP == kAxpydot) {
+        WsLayout lay;
+        const size_t off = lay.take((size_t)grid);
+        BTO_TRY(grow(&c.ws, &c.ws_bytes, lay.total, "workspace"));
+        g.partials = reinterpret_cast<double *>(c.ws + off);
+        g.ticket = c.tickets;
+    }
+    return launch_dependent(fn, (unsigned)grid, g, stream, "vec_kernel");
+}
+
+// ---------------------------------------------------------------------------
+// matrix kernels
+
+using MvKernel = void (*)(const MvArgs);
+
+struct MvPlan {
+    int R = 8, V = 1;
+    bool aligned = true;
+    long strip_width = 512;
+    int nstrips = 1;
+    long units_per_strip = 1, total_units = 1;
+    long grid = 1;
+    long slots = 1;        // max CTAs sharing one strip
+    MvKernel fn = nullptr;
+};
+
+template <int FLAGS, int R, int V>
+MvKernel mv_kernel_minb(int minb)
+{
+    switch (minb) {
+        case 2: return mv_tile_kernel<FLAGS, R, V, true, 2>;
+        case 3: return mv_tile_kernel<FLAGS, R, V, true, 3>;
+        case 4: return mv_tile_kernel<FLAGS, R, V, true, 4>;
+        case 6: return mv_tile_kernel<FLAGS, R, V, true, 6>;
+        default: return mv_tile_kernel<FLAGS, R, V, true, 1>;
+    }
+}
+
+// Supported tile shapes: (rows, double2 per thread) = (8,1) always; (16,1) for
+// single-matrix kinds; (32,1) for kinds without row dots; (8,2) for A x alone.
+template <int FLAGS>
+bool mv_shape_ok(int R, int V)
+{
+    if (R == 8 && V == 1) return true;
+    if (FLAGS & kFlagN2) return false;
+    if (R == 16 && V == 1) return true;
+    if (R == 32 && V == 1) return (FLAGS & kFlagN) == 0;
+    if (R == 8 && V == 2) return FLAGS == kFlagN || FLAGS == (kFlagT | kFlagRank2);
+    return false;
+}
+
+template <int FLAGS>
+MvKernel mv_kernel_ptr(int R, int V, bool aligned, int minb)
+{
+    if (!aligned) return mv_tile_kernel<FLAGS, 8, 1, false, 1>;
+    if constexpr ((FLAGS & kFlagN2) == 0) {
+        if (R == 16 && V == 1) return mv_kernel_minb<FLAGS, 16, 1>(minb);
+        if constexpr ((FLAGS & kFlagN) == 0) {
+            if (R == 32 && V == 1) return mv_kernel_minb<FLAGS, 32, 1>(minb);
+        }
+        if constexpr (FLAGS == kFlagN || FLAGS == (kFlagT | kFlagRank2)) {
+            if (R == 8 && V == 2) return mv_kernel_minb<FLAGS, 8, 2>(minb);
+        }
+    }
+    return mv_kernel_minb<FLAGS, 8, 1>(minb);
+}
+
+// Launch defaults per pass kind, from the B200 sweep at n = 32768
+// (profiles/r01/sweep2_passes.json): {rows per unit, double2 per thread, CTAs per SM
+// (0 = what the occupancy calculator allows)}.
+struct MvDefault { int rows, vec, grid_per_sm, minb; };
+
+template <int FLAGS>
+constexpr MvDefault mv_default()
+{
+    if (FLAGS == (kFlagN | kFlagT)) return {8, 1, 8, 4};        // BiCGK         7.10 TB/s
+    if (FLAGS == (kFlagN | kFlagN2)) return {8, 1, 4, 4};       // GESUMMV       7.04 TB/s
+    if (FLAGS == (kFlagT | kFlagRank2)) return {16, 1, 2, 1};   // GEMVER pass 1 6.29 TB/s (r+w)
+    if (FLAGS == kFlagT) return {32, 1, 2, 1};                  // A' y          7.17 TB/s
+    return {8, 2, 8, 2};                                        // A x           7.20 TB/s
+}
+
+template <int FLAGS>
+int plan_mv(DeviceCtx &c, long M, long N, bool aligned, MvPlan *p)
+{
+    constexpr MvDefault dflt = mv_default<FLAGS>();
+    int R = g_tuning.mv_rows ? (int)g_tuning.mv_rows : dflt.rows;
+    int V = g_tuning.mv_vec ? (int)g_tuning.mv_vec : dflt.vec;
+    int minb = g_tuning.mv_minb ? (int)g_tuning.mv_minb : dflt.minb;
+    if (!aligned || !mv_shape_ok<FLAGS>(R, V)) { R = 8; V = 1; }
+    p->R = R;
+    p->V = V;
+    p->aligned = aligned;
+    p->fn = mv_kernel_ptr<FLAGS>(R, V, aligned, minb);
+    p->strip_width = (long)kThreads * 2 * V;
+    p->nstrips = (int)((N + p->strip_width - 1) / p->strip_width);
+    p->units_per_strip = (M + R - 1) / R;
+    p->total_units = p->units_per_strip * p->nstrips;
+    int occ = 1;
+    BTO_TRY(occupancy_of(c, p->fn, &occ));
+    long per_sm = g_tuning.grid_per_sm > 0 ? g_tuning.grid_per_sm : dflt.grid_per_sm;
+    if (per_sm <= 0) per_sm = occ;
+    long grid = (long)c.sm_count * per_sm;
+    // small matrices: at least 4 units per CTA, so that few CTAs share a strip and
+    // the join (one partial per CTA and strip) stays short
+    const long by_work = (p->total_units + 3) / 4;
+    if (grid > by_work) grid = by_work;
+    if (grid < 1) grid = 1;
+    p->grid = grid;
+    long slots = 1;
+    for (int s = 0; s < p->nstrips; ++s) {
+        const long first = split_owner(p->total_units, grid, (long)s * p->units_per_strip);
+        const long last = split_owner(p->total_units, grid,
+                                      (long)(s + 1) * p->units_per_strip - 1);
+        if (last - first + 1 > slots) slots = last - first + 1;
+    }
+    p->slots = slots;
+    return BTO_OK;
+}
+
+void fill_geometry(const MvPlan &p, MvArgs *a, long M, long N)
+{
+    a->M = M;
+    a->N = N;
+    a->units_per_strip = p.units_per_strip;
+    a->total_units = p.total_units;
+    a->nstrips = p.nstrips;
+}
+
+int launch_mv(const MvPlan &p, const MvArgs &a, cudaStream_t stream)
+{
+    return launch_dependent(p.fn, (unsigned)p.grid, a, stream, "mv_tile_kernel");
+}
+
+// Launch the join of `f` (geometry already filled in).  While a sharded
+// entry point is active and the join has a column side, the cross-GPU exchange
+// is fused into it (join_exchange_kernel); otherwise the plain local join runs.
+int launch_join(DeviceCtx &c, FinArgs f, cudaStream_t stream)
+{
+    const long rb = f.rmode != kRowNone ? (f.M + kThreads - 1) / kThreads : 0;
+    if (c.exch_active && f.cmode != kColNone) {
+        if (2 * f.N > c.exch_capacity) {
+            return fail(BTO_ERR_INVALID, "exchange buffer holds %ld doubles, need %ld",
+                        c.exch_capacity, 2 * f.N);
+        }
+        ExchArgs e{};
+        e.fin = f;
+        e.exch = c.exch_bufs;
+        e.flags = c.exch_flags;
+        e.epoch = ++c.exch_epoch;
+        e.buf_offset = (long)(e.epoch & 1u) * (c.exch_capacity / 2);
+        e.rank = c.exch_rank;
+        e.world = c.exch_world;
+        e.phases = (int)g_tuning.exchange_phases;
+        return launch_dependent(join_exchange_kernel, (unsigned)(kExchCtas + rb), e, stream,
+                                "join_exchange_kernel");
+    }
+    const long cb = f.cmode != kColNone ? (f.N + kThreads - 1) / kThreads : 0;
+    f.col_blocks = (int)cb;
+    return launch_dependent(finalize_kernel, (unsigned)(cb + rb), f, stream, "finalize_kernel");
+}
+
+int launch_finalize(DeviceCtx &c, const MvPlan &p, FinArgs f, long M, long N, cudaStream_t stream)
+{
+    f.M = M;
+    f.N = N;
+    f.units_per_strip = p.units_per_strip;
+    f.total_units = p.total_units;
+    f.grid = p.grid;
+    f.strip_width = p.strip_width;
+    f.nstrips = p.nstrips;
+    return launch_join(c, f, stream);
+}
+
+int check_mn(long M, long N)
+{
+    if (M < 1 || N < 1) {
+        return fail(BTO_ERR_INVALID, "extents M=%ld N=%ld must be >= 1", M, N);
+    }
+    return BTO_OK;
+}
+
+bool mat_aligned(long N, const void *a, const void *b = nullptr, const void *c = nullptr)
+{
+    return (N % 2 == 0) && aligned16(a) && aligned16(b) && aligned16(c);
+}
+
+// One streaming pass producing row dots and/or column sums, then the join.
+// prepare() plans the launch and books its partial buffers in the sequence's
+// workspace layout; run() launches after the workspace has been sized once,
+// so no pointer handed out earlier in the sequence can move.
+template <int FLAGS>
+struct Pass {
+    MvPlan plan;
+    size_t off_row = 0, off_row2 = 0, off_col = 0;
+    long M = 0, N = 0;
+
+    int prepare(DeviceCtx &c, long m, long n, bool aligned, WsLayout *lay)
+    {
+        M = m;
+        N = n;
+        BTO_TRY(plan_mv<FLAGS>(c, M, N, aligned, &plan));
+        if (FLAGS & kFlagN) off_row = lay->take((size_t)plan.nstrips * M);
+        if (FLAGS & kFlagN2) off_row2 = lay->take((size_t)plan.nstrips * M);
+        if (FLAGS & kFlagT) off_col = lay->take((size_t)plan.slots * N);
+        return BTO_OK;
+    }
+
+    // Row results go to f.rowout through f.rmode, column results to f.colout
+    // through f.cmode.
+    int run(DeviceCtx &c, MvArgs a, FinArgs f, cudaStream_t stream) const
+    {
+        fill_geometry(plan, &a, M, N);
+        a.rowpart = reinterpret_cast<double *>(c.ws + off_row);
+        a.rowpart2 = reinterpret_cast<double *>(c.ws + off_row2);
+        a.colpart = reinterpret_cast<double *>(c.ws + off_col);
+        BTO_TRY(launch_mv(plan, a, stream));
+        f.rowpart = a.rowpart;
+        f.rowpart2 = a.rowpart2;
+        f.colpart = a.colpart;
+        if (!(FLAGS & kFlagN)) f.rmode = kRowNone;
+        if (!(FLAGS & kFlagT)) f.cmode = kColNone;
+        return launch_finalize(c, plan, f, M, N, stream);
+    }
+};
+
+int size_ws(DeviceCtx &c, const WsLayout &lay)
+{
+    return grow(&c.ws, &c.ws_bytes, lay.total, "workspace");
+}
+
+
+}  // namespace
+}  // namespace bto_host

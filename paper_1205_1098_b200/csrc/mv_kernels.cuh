@@ -469,11 +469,4 @@ axpz_kernel(const double *colsum, double beta, const double *z, double *x, long 
     if (j < n) x[j] = __dadd_rn(__dmul_rn(colsum[j], beta), z[j]);
 }
 
-__global__ void __launch_bounds__(kThreads)
-fill_kernel(double *dst, double value, long n)
-{
-    const long j = (long)blockIdx.x * kThreads + threadIdx.x;
-    if (j < n) dst[j] = value;
-}
-
 }  // namespace bto
