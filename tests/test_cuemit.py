@@ -1,0 +1,122 @@
+"""Organism-driven CUDA emission (cuemit.py), the GPU back end for arbitrary organisms.
+
+Fixtures: tests/golden/organisms.json holds loop-IR snapshots the reference produced
+for 12 organisms per corpus kernel (max-fuse, unfused, 10 random legal ones).
+CPU: emission is deterministic and the CUDA compiles (nvcc cross-compiles without a
+GPU).  GPU: every organism, several extents, against the oracle -- the reference's
+acceptance criterion 1 (tests/test_acceptance.py:55-94) with a GPU back end."""
+from __future__ import annotations
+
+import json
+import math
+from concurrent.futures import ThreadPoolExecutor
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+import paper_1205_1098_b200 as bto
+from paper_1205_1098_b200 import cuemit
+
+IRS = json.loads((Path(__file__).parent / "golden" / "organisms.json").read_text())
+ELEMENTWISE = {"axpydot": ("z",), "gemver": ("B",), "vadd": ("x",), "waxpby": ("w",)}
+
+
+def test_fixture_covers_the_corpus_with_varied_organisms():
+    assert set(IRS) == set(bto.CORPUS)
+    for name, irs in IRS.items():
+        keys = {ir["organism"] for ir in irs}
+        assert len(keys) == len(irs) >= 10, name
+        assert any(r["t"] == "par" for ir in irs for r in ir["roots"]), name
+        assert any(all(r["t"] != "par" for r in ir["roots"]) for ir in irs), name   # unfused/serial
+
+
+def test_emission_is_deterministic_and_keeps_the_reference_signature():
+    for name, irs in IRS.items():
+        typed = bto.load_graph(name)
+        for ir in irs:
+            a, b = cuemit.emit_cuda(ir), cuemit.emit_cuda(ir)
+            assert a.source == b.source
+            assert a.kernel_name == name and a.organism_key == ir["organism"]
+            assert [n for _, n in a.params] == [n for n, _ in typed.params()]
+            assert f'extern "C" void {name}(' in a.source
+
+
+def test_structure_of_the_bicgk_max_fuse_kernel():
+    ir = next(ir for ir in IRS["bicgk"] if ir["organism"].startswith("{_{p(i)}{_i{_j 1 2}}}"))
+    src = cuemit.emit_cuda(ir, blocks=64).source
+    assert "for (long i = i_lo; i < i_hi; ++i)" in src                  # block's rows, uniform
+    assert "for (long j = 0 + threadIdx.x; j < N; j += blockDim.x)" in src   # innermost: strided
+    assert "lacc1 += __dmul_rn(A[i * N + j], p[j]);" in src            # row dot -> thread accumulator
+    assert "s_part[p_ * (N) + j] += __dmul_rn(A[i * N + j], r[i]);" in src   # column sums: own j
+    assert "cta_allreduce(lacc1, scratch_)" in src
+    assert "bicgk_region0<<<64, 256, 0, 0>>>" in src and "bicgk_join1_s" in src
+
+
+def _compile_all(irs, workdir, blocks=cuemit.DEFAULT_BLOCKS):
+    tc = cuemit.NvccToolchain()
+
+    def job(args):
+        idx, ir = args
+        k = cuemit.emit_cuda(ir, blocks=blocks)
+        return idx, k, tc.compile(k.source, workdir, name=f"{ir['name'].lower()}_{idx}")
+
+    with ThreadPoolExecutor(max_workers=8) as pool:
+        return list(pool.map(job, enumerate(irs)))
+
+
+def test_emitted_cuda_compiles_for_sm_100a(tmp_path):
+    if not cuemit.NvccToolchain().available:
+        pytest.skip("nvcc not available")
+    sample = [IRS[name][i] for name in ("gemver", "bicgk", "axpydot", "atax", "dgemvt")
+              for i in (0, 1, 5)]
+    built = _compile_all(sample, tmp_path)
+    assert all(path.exists() for _, _, path in built)
+
+
+def test_compile_failure_is_reported(tmp_path):
+    if not cuemit.NvccToolchain().available:
+        pytest.skip("nvcc not available")
+    k = cuemit.emit_cuda(IRS["vadd"][0])
+    with pytest.raises(bto.ToolchainError, match="compile failed"):
+        cuemit.NvccToolchain().compile(k.source.replace("double", "dubble", 1), tmp_path)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name", sorted(IRS))
+def test_every_organism_matches_the_oracle(bto_lib, oracle, tmp_path, name):
+    typed = bto.load_graph(name)
+    built = _compile_all(IRS[name], tmp_path, blocks=37)       # odd block count: ragged slices
+    worst = 0.0
+    for idx, kernel, path in built:
+        ir = IRS[name][idx]
+        for (m, n) in [(1, 1), (7, 50), (200, 200), (513, 1030)]:
+            ext = {"M": m * n} if typed.extent_names == ("M",) else {"M": m, "N": n}
+            inputs = bto.random_inputs(typed, ext, seed=idx)
+            want = oracle.oracle_run(name, inputs, ext, threads=8)
+            got = cuemit.run_emitted(path, kernel, ir, inputs, ext)
+            for out in want:
+                assert not np.any(np.isnan(np.asarray(got[out]))), (name, ir["organism"], ext, out)
+            err = bto.max_rel_error(got, want)
+            worst = max(worst, err)
+            assert err <= 1e-12 * max(1.0, math.log2(max(ext.values()))), (name, ir["organism"], ext, err)
+            for out in ELEMENTWISE.get(name, ()):
+                assert np.array_equal(np.asarray(got[out]), np.asarray(want[out])), (name, ir["organism"], out)
+    assert worst < 1e-10          # the reference's own gate
+
+
+@pytest.mark.gpu
+def test_default_block_count_and_device_inputs(bto_lib, oracle, tmp_path):
+    import torch
+    ir = IRS["gemver"][0]
+    kernel = cuemit.emit_cuda(ir)
+    path = cuemit.NvccToolchain().compile(kernel.source, tmp_path, name="gemver_default")
+    typed = bto.load_graph("gemver")
+    ext = {"M": 1500, "N": 2051}
+    inputs = bto.gen_inputs(typed, ext, seed=4)
+    dev = {k: (torch.from_numpy(v).cuda() if isinstance(v, np.ndarray) else v) for k, v in inputs.items()}
+    got = cuemit.run_emitted(path, kernel, ir, dev, ext)
+    assert all(hasattr(v, "is_cuda") for v in got.values())
+    want = oracle.oracle_run("gemver", inputs, ext, threads=8)
+    assert bto.max_rel_error(got, want) <= 1e-12 * math.log2(2051)
+    assert np.array_equal(got["B"].cpu().numpy(), want["B"])
