@@ -45,7 +45,8 @@ from pathlib import Path
 
 from .runtime import GeneratedKernel, ToolchainError
 
-__all__ = ["ir_from_matfuse", "emit_cuda", "NvccToolchain", "run_emitted", "DEFAULT_BLOCKS"]
+__all__ = ["ir_from_matfuse", "emit_cuda", "NvccToolchain", "run_emitted", "DEFAULT_BLOCKS",
+           "measure_empirical_ir", "OrganismTimer"]
 
 DEFAULT_BLOCKS = 592          # 4 CTAs per SM on a 148-SM part
 CTA_THREADS = 256
@@ -201,6 +202,16 @@ class _Emitter:
                        for it in items)
         return not has_loop(loop["body"])
 
+    def has_sliced_lane_loop(self, items: list) -> bool:
+        for it in items:
+            if it["t"] == "loop":
+                if self.is_innermost(it):
+                    if it["sliced"]:
+                        return True
+                elif self.has_sliced_lane_loop(it["body"]):
+                    return True
+        return False
+
     def indexed_by(self, storage_name: str, axis: str) -> bool:
         s = self.st[storage_name]
         return s["cls"] != "contracted" and axis in s["labels"]
@@ -339,9 +350,20 @@ class _Emitter:
                 serial_group.append(root)
                 continue
             flush_serial()
-            t = max(int(ir["threads"][root["slot"]]), self.blocks)
+            org_t = int(ir["threads"][root["slot"]])
+            t = max(org_t, self.blocks)
             fname = f"{kname}_region{regions}"
+            nb = f"nb{regions}_"
             regions += 1
+            # When the strided (innermost) loops run over the block's own slice, a
+            # slice narrower than the CTA leaves threads idle: cap the block count
+            # so every CTA gets at least a CTA-width of the axis (never below the
+            # organism's own count).  Any count is legal for the block formula.
+            if self.has_sliced_lane_loop(root["body"]):
+                launches.append(f"long {nb} = {root['extent']} / {CTA_THREADS}; "
+                                f"if ({nb} < {org_t}) {nb} = {org_t}; if ({nb} > {t}) {nb} = {t};")
+            else:
+                launches.append(f"long {nb} = {t};")
             ax, ext = root["axis"], root["extent"]
             w.open(f"__global__ void __launch_bounds__({CTA_THREADS}) {fname}({decl}, long nblocks_)")
             scalars_decl()
@@ -352,7 +374,7 @@ class _Emitter:
             self.emit_items(root["body"], "p_", True)
             w.close()
             w.put()
-            launches.append(f"{fname}<<<{t}, {CTA_THREADS}, 0, 0>>>({call}, {t}L);")
+            launches.append(f"{fname}<<<(unsigned){nb}, {CTA_THREADS}, 0, 0>>>({call}, {nb});")
             for result in root["partials"]:
                 pname = self.partial_for(result)
                 ps = self.st[pname]
@@ -376,7 +398,7 @@ class _Emitter:
                     grid = f"(unsigned)(({e0} + 255) / 256)"
                 w.close()
                 w.put()
-                launches.append(f"{jname}<<<{grid}, 256, 0, 0>>>({call}, {t}L);")
+                launches.append(f"{jname}<<<{grid}, 256, 0, 0>>>({call}, {nb});")
         flush_serial()
 
         # host entry point: the reference's signature (cemit.py:225-241), device pointers
@@ -519,3 +541,95 @@ def run_emitted(binary, kernel: GeneratedKernel, ir: dict, inputs: dict, extents
             val = buf.reshape(shape)
         result[name] = val if on_gpu else val.cpu().numpy()
     return result
+
+
+# ---------------------------------------------------------------------------
+# empirical fitness for organisms (cost.py:124-208 with a GPU back end)
+
+def measure_empirical_ir(ir: dict, graph, extents: dict, reps: int = 5,
+                         validate_extents: dict | None = None, blocks: int = DEFAULT_BLOCKS,
+                         toolchain: NvccToolchain | None = None, source_filter=None,
+                         tolerance: float = 1e-10):
+    """Emit, compile, validate, then time one lowered organism; +inf with the
+    reference's diagnostics on any failure (cost.py:176-207).  `graph` is this
+    package's TypedSpec of the same kernel; validation compares against the
+    independent spec evaluator (cost.evaluate_spec).  `source_filter` is the
+    reference's fault-injection hook (cost.py:148,186)."""
+    import math
+
+    import torch
+
+    from .cost import CostReport, evaluate_spec
+    from .runtime import gen_inputs, max_rel_error, workdir
+
+    def failure(kind: str, detail: str) -> CostReport:
+        return CostReport(total=math.inf, source="empirical", diagnostic=f"{kind}: {detail}")
+
+    kernel = emit_cuda(ir, blocks=blocks)
+    source = source_filter(kernel.source) if source_filter is not None else kernel.source
+    try:
+        lib = (toolchain or NvccToolchain()).compile(source, workdir(), name="kernel", shared=True)
+    except ToolchainError as exc:
+        return failure("compile-failure", str(exc))
+    vext = validate_extents or {k: min(64, v) for k, v in extents.items()}
+    try:
+        inputs = gen_inputs(graph, vext, seed=7)
+        dev = {k: (torch.from_numpy(v).cuda() if hasattr(v, "shape") else v) for k, v in inputs.items()}
+        got = run_emitted(lib, kernel, ir, dev, vext)
+        want = evaluate_spec(graph.spec, dev)
+    except Exception as exc:  # noqa: BLE001 -- a crash is a fitness failure, not an error
+        return failure("runtime-crash", repr(exc))
+    err = max_rel_error({k: (v if isinstance(v, float) else v.cpu().numpy()) for k, v in got.items()},
+                        {k: (v if isinstance(v, float) else v.cpu().numpy()) for k, v in want.items()})
+    if not err < tolerance:
+        return failure("numerical-mismatch", f"max relative error {err:.3e}")
+    try:
+        inputs = gen_inputs(graph, extents, seed=7)
+        dev = {k: (torch.from_numpy(v).cuda() if hasattr(v, "shape") else v) for k, v in inputs.items()}
+        run_emitted(lib, kernel, ir, dev, extents)                 # warm-up, untimed
+        best = math.inf
+        for _ in range(reps):
+            start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            start.record()
+            run_emitted(lib, kernel, ir, dev, extents)
+            stop.record()
+            stop.synchronize()
+            best = min(best, start.elapsed_time(stop) * 1e-3)
+    except Exception as exc:  # noqa: BLE001
+        return failure("runtime-crash", repr(exc))
+    return CostReport(total=best, source="empirical")
+
+
+class OrganismTimer:
+    """Drop-in for the reference's `EmpiricalTimer` (cost.py:124-160) where both the
+    reference and a GPU are present: `fitness(organism) -> CostReport` through
+    lower -> contract_arrays -> CUDA emission -> nvcc -> validate -> CUDA events.
+    Usable directly with `matfuse.search.run_strategy`."""
+
+    parallel_safe = False
+
+    def __init__(self, ref_graph, extents: dict | None = None, reps: int = 5,
+                 validate_extents: dict | None = None, blocks: int = DEFAULT_BLOCKS,
+                 source_filter=None):
+        from .runtime import _convert_expr
+        from .spec import Decl, KernelSpec, infer_shapes
+        spec = ref_graph.spec
+        self.ref_graph = ref_graph
+        self.graph = infer_shapes(KernelSpec(
+            spec.name,
+            tuple((n, Decl(d.kind, d.orientation)) for n, d in spec.inputs),
+            tuple((n, Decl(d.kind, d.orientation)) for n, d in spec.outputs),
+            tuple((s.target, _convert_expr(s.value)) for s in spec.statements)))
+        self.extents = extents or {n: 1000 for n in ref_graph.extent_names}
+        self.reps, self.validate_extents, self.blocks = reps, validate_extents, blocks
+        self.source_filter = source_filter
+
+    def key_salt(self) -> str:
+        return "empirical-cuda:" + ",".join(f"{k}={v}" for k, v in sorted(self.extents.items()))
+
+    def __call__(self, organism):
+        from matfuse import contract_arrays, lower
+        ir = ir_from_matfuse(contract_arrays(lower(organism, self.ref_graph)))
+        return measure_empirical_ir(ir, self.graph, self.extents, self.reps,
+                                    validate_extents=self.validate_extents, blocks=self.blocks,
+                                    source_filter=self.source_filter)

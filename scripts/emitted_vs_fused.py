@@ -1,0 +1,21 @@
+#!/usr/bin/env python
+"""Time the emitted CUDA of the max-fuse organisms next to the hand-written sequences."""
+import json, sys, tempfile
+from pathlib import Path
+import torch
+REPO = Path(__file__).resolve().parent.parent
+sys.path.insert(0, str(REPO))
+import paper_1205_1098_b200 as bto
+from paper_1205_1098_b200 import cost, cuemit
+irs = json.loads((REPO / "tests/golden/organisms.json").read_text())
+n = int(sys.argv[1]) if len(sys.argv) > 1 else 8192
+for name in bto.HOT_PATH:
+    typed = bto.load_graph(name)
+    ext = {"M": n * n} if typed.extent_names == ("M",) else {"M": n, "N": n}
+    fused = cost.measure_empirical(cost.GpuVariant(name), typed, ext, reps=5)
+    emitted = cuemit.measure_empirical_ir(irs[name][0], typed, ext, reps=3)
+    unf = cuemit.measure_empirical_ir(irs[name][1], typed, ext, reps=1)
+    nbytes = bto._native.bytes_min(name, ext["M"], ext.get("N", 1))
+    print(f"{name:8s} n={n}: hand-written {fused.total*1e3:8.3f} ms ({nbytes/fused.total/1e9:6.0f} GB/s)   "
+          f"emitted max-fuse {emitted.total*1e3:8.3f} ms ({nbytes/emitted.total/1e9:6.0f} GB/s)   "
+          f"emitted unfused {unf.total*1e3:9.3f} ms  {emitted.diagnostic or ''} {unf.diagnostic or ''}", flush=True)

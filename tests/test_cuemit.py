@@ -50,7 +50,11 @@ def test_structure_of_the_bicgk_max_fuse_kernel():
     assert "lacc1 += __dmul_rn(A[i * N + j], p[j]);" in src            # row dot -> thread accumulator
     assert "s_part[p_ * (N) + j] += __dmul_rn(A[i * N + j], r[i]);" in src   # column sums: own j
     assert "cta_allreduce(lacc1, scratch_)" in src
-    assert "bicgk_region0<<<64, 256, 0, 0>>>" in src and "bicgk_join1_s" in src
+    assert "long nb0_ = 64;" in src and "bicgk_region0<<<(unsigned)nb0_, 256, 0, 0>>>" in src
+    assert "bicgk_join1_s" in src
+    # a region whose strided loops run over its own slice gets at least a CTA-width per block
+    gem = cuemit.emit_cuda(IRS["gemver"][0], blocks=592).source
+    assert "long nb0_ = N / 256; if (nb0_ < 8) nb0_ = 8; if (nb0_ > 592) nb0_ = 592;" in gem
 
 
 def _compile_all(irs, workdir, blocks=cuemit.DEFAULT_BLOCKS):
@@ -120,3 +124,46 @@ def test_default_block_count_and_device_inputs(bto_lib, oracle, tmp_path):
     want = oracle.oracle_run("gemver", inputs, ext, threads=8)
     assert bto.max_rel_error(got, want) <= 1e-12 * math.log2(2051)
     assert np.array_equal(got["B"].cpu().numpy(), want["B"])
+
+
+@pytest.mark.gpu
+def test_empirical_fitness_of_organisms_and_fault_injection(bto_lib):
+    """measure_empirical's three outcomes (cost.py:163-208, tests/test_cost.py:151-176)
+    with the CUDA back end: finite time, compile-failure, numerical-mismatch."""
+    typed = bto.load_graph("batax")
+    fused, unfused = IRS["batax"][0], IRS["batax"][1]
+    ext = {"M": 2048, "N": 2048}
+    a = cuemit.measure_empirical_ir(fused, typed, ext, reps=2)
+    b = cuemit.measure_empirical_ir(unfused, typed, ext, reps=2)
+    assert a.source == "empirical" and not a.failed and not b.failed
+    assert 0 < a.total < b.total                 # fusion + partitioning beat the serial organism
+    bad = cuemit.measure_empirical_ir(fused, typed, ext, reps=1,
+                                      source_filter=lambda s: s.replace("double", "dubble", 1))
+    assert bad.failed and bad.diagnostic.startswith("compile-failure")
+    wrong = cuemit.measure_empirical_ir(fused, typed, ext, reps=1,
+                                        source_filter=lambda s: s.replace("+=", "=", 1))
+    assert wrong.failed and wrong.diagnostic.startswith("numerical-mismatch")
+
+
+def test_organism_timer_accepts_reference_objects():
+    """Where the reference is importable (the build container), the timer takes its
+    Organism objects directly; without a GPU the evaluation is a reported failure."""
+    import sys
+    ref = Path("/root/reference/pkg/src")
+    if not ref.exists():
+        pytest.skip("reference not mounted")
+    sys.path.insert(0, str(ref))
+    try:
+        from matfuse import max_fuse
+        from matfuse.corpus import load_graph
+        g = load_graph("bicgk")
+        timer = cuemit.OrganismTimer(g, {"M": 64, "N": 64}, reps=1)
+        assert timer.key_salt().startswith("empirical-cuda:")
+        assert timer.graph.dims == bto.load_graph("bicgk").dims
+        import torch
+        report = timer(max_fuse(g, 8))
+        assert report.source == "empirical"
+        if not torch.cuda.is_available():
+            assert report.failed and report.diagnostic.startswith("runtime-crash")
+    finally:
+        sys.path.remove(str(ref))
