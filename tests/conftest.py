@@ -16,6 +16,16 @@ def pytest_configure(config):
     config.addinivalue_line("markers", "gpu: needs a real B200 (run with -m gpu)")
 
 
+def pytest_sessionstart(session):
+    """The shared objects are build products (git-ignored): make sure they exist
+    before collection, so a fresh checkout can run the suite without a prior
+    `__graft_entry__.build()` (nvcc cross-compiles sm_100a without a GPU)."""
+    from paper_1205_1098_b200 import _native
+    if not _native.library_path().exists():
+        from paper_1205_1098_b200.build import build_library
+        build_library()
+
+
 @pytest.fixture(scope="session")
 def oracle():
     import oracle_lib
