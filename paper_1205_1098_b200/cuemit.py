@@ -46,7 +46,8 @@ from pathlib import Path
 from .runtime import GeneratedKernel, ToolchainError
 
 __all__ = ["ir_from_matfuse", "emit_cuda", "NvccToolchain", "run_emitted", "DEFAULT_BLOCKS",
-           "measure_empirical_ir", "OrganismTimer"]
+           "measure_empirical_ir", "OrganismTimer", "EmitModel", "estimate_cost_ir",
+           "AnalyticOrganismCost"]
 
 DEFAULT_BLOCKS = 592          # 4 CTAs per SM on a 148-SM part
 CTA_THREADS = 256
@@ -633,3 +634,141 @@ class OrganismTimer:
         return measure_empirical_ir(ir, self.graph, self.extents, self.reps,
                                     validate_extents=self.validate_extents, blocks=self.blocks,
                                     source_filter=self.source_filter)
+
+
+# ---------------------------------------------------------------------------
+# analytic fitness for organisms: HBM bytes, occupancy and barrier steps of the
+# kernels `emit_cuda` would print (the organism-level half of the GPU cost model)
+
+@dataclass(frozen=True)
+class EmitModel:
+    """Coefficients of `estimate_cost_ir`, fitted on the 360 timings of
+    profiles/r01/organism_times.json (120 organisms x n = 1024, 2048, 4096)."""
+    peak_gbs: float = 6500.0        # HBM ceiling of a full grid
+    cta_gbs: float = 100.0          # what one CTA streams on its own
+    launch_us: float = 15.0         # per kernel launch (incl. its share of the final sync)
+    step_us: float = 0.6            # one strided-loop execution: barriers + CTA reduction
+    trip_us: float = 0.05           # one trip of a thread through a strided loop
+    rmw_trip_us: float = 0.2        # the same when the trip read-modify-writes global memory
+    stmt_us: float = 0.3            # a uniform statement that writes memory (thread 0 + barrier)
+    alloc_us: float = 550.0         # cudaMalloc + cudaFree of one temporary / partial buffer per call
+                                    # (the reference pays malloc/free per call too, cemit.py:183-202)
+    sm_count: int = 148
+
+
+def estimate_cost_ir(ir: dict, extents: dict, model: EmitModel | None = None,
+                     blocks: int = DEFAULT_BLOCKS):
+    """Deterministic seconds estimate of the CUDA `emit_cuda(ir, blocks)` prints.
+
+    Per launch: time = launch + max(bytes / bandwidth(blocks), steps), where
+    * bytes   -- every 2-D operand streams once per execution of the strided loop
+                 that touches it (no cache between loop nests on a GPU: re-reads
+                 count, unlike cost.py:80-86); vectors indexed by the strided
+                 axis stay cache-resident per CTA and count once per block;
+    * bandwidth grows with the number of CTAs up to the HBM ceiling (a serial
+      root runs in ONE CTA -- the GPU analogue of an unpartitioned CPU loop);
+    * steps   -- the longest block's chain of strided-loop executions (barriers,
+                 CTA reductions, read-modify-write trips) and uniform memory
+                 writes, which bounds latency-dominated organisms.
+    Returns cost.CostReport(source="analytic")."""
+    from .cost import CostReport
+
+    m = model or EmitModel()
+    st, ops = ir["storage"], ir["ops"]
+    ext = {k: float(v) for k, v in extents.items()}
+    per_launch = []
+    launches = 0
+
+    def has_loop(items):
+        return any(it["t"] == "loop" for it in items)
+
+    def walk(items, trips, nb, threads, acc):
+        """acc: dict(bytes=, steps=) for one launch; `trips` executions per block."""
+        for it in items:
+            if it["t"] == "stmt":
+                target = it["target"] if it["role"] == "init" else ops[str(it["op"])]["result"]
+                if st[target]["cls"] != "contracted":
+                    acc["steps"] += trips * m.stmt_us
+                continue
+            rng = ext[it["extent"]] / nb if it["sliced"] else ext[it["extent"]]
+            if has_loop(it["body"]):
+                walk(it["body"], trips * max(rng, 1.0), nb, threads, acc)
+                continue
+            # strided (innermost) loop
+            per_thread = max(1.0, rng / threads)
+            mats, vecs, rmw = set(), set(), False
+            for s in it["body"]:
+                if s["role"] == "init":
+                    names, target, red = [s["target"]], s["target"], False
+                else:
+                    op = ops[str(s["op"])]
+                    names, target, red = list(op["operands"]) + [op["result"]], op["result"], op["reduction"]
+                    if red and it["axis"] in st[target]["labels"] and st[target]["cls"] != "contracted":
+                        rmw = True
+                for n in names:
+                    s_ = st[n]
+                    if s_["cls"] == "contracted" or it["axis"] not in s_["labels"]:
+                        continue
+                    (mats if len(s_["labels"]) == 2 else vecs).add(n)
+            acc["bytes"] += 8.0 * len(mats) * rng * trips * nb + 8.0 * len(vecs) * rng * nb
+            acc["steps"] += trips * (m.step_us + per_thread * (m.rmw_trip_us if rmw else m.trip_us))
+
+    def close(acc, nb):
+        bw = min(m.peak_gbs, m.cta_gbs * min(nb, 4 * m.sm_count)) * 1e9
+        per_launch.append((m.launch_us + max(acc["bytes"] / bw * 1e6, acc["steps"])) * 1e-6)
+
+    serial = None
+    for root in ir["roots"]:
+        if root["t"] != "par":
+            if serial is None:
+                serial = {"bytes": 0.0, "steps": 0.0}
+                launches += 1
+            walk([root], 1.0, 1.0, float(SERIAL_THREADS), serial)
+            continue
+        if serial is not None:
+            close(serial, 1.0)
+            serial = None
+        org_t = float(ir["threads"][root["slot"]])
+        nb = max(org_t, float(blocks))
+        em = _Emitter(ir, blocks)
+        if em.has_sliced_lane_loop(root["body"]):
+            nb = min(nb, max(org_t, float(int(ext[root["extent"]]) // CTA_THREADS)))
+        nb = max(1.0, min(nb, ext[root["extent"]]))
+        acc = {"bytes": 0.0, "steps": 0.0}
+        walk(root["body"], 1.0, nb, float(CTA_THREADS), acc)
+        close(acc, nb)
+        launches += 1
+        for result in root["partials"]:          # join: read nb partial rows, write the result
+            p = st[em.partial_for(result)]
+            size = 1.0
+            for e in p["extents"]:
+                size *= ext[e]
+            per_launch.append((m.launch_us + 8.0 * size * (nb + 1) / (m.peak_gbs * 1e9) * 1e6
+                               + (nb * 0.01 if not p["extents"] else 0.0)) * 1e-6)
+            launches += 1
+    if serial is not None:
+        close(serial, 1.0)
+    nalloc = sum(1 for s in st.values() if s["cls"] in ("temp", "partial"))
+    per_launch.append(nalloc * m.alloc_us * 1e-6)
+    contracted = tuple(sorted(n for n, s in st.items() if s["cls"] == "contracted"))
+    return CostReport(total=float(sum(per_launch)), source="analytic", per_root=tuple(per_launch),
+                      contracted=contracted, partition_nodes=launches)
+
+
+class AnalyticOrganismCost:
+    """Fitness callable over the reference's Organism objects (cost.py:106-121 with
+    the GPU model): organism -> lower -> contract_arrays -> estimate_cost_ir."""
+
+    parallel_safe = True
+
+    def __init__(self, ref_graph, extents: dict, model: EmitModel | None = None,
+                 blocks: int = DEFAULT_BLOCKS):
+        self.ref_graph, self.extents, self.model, self.blocks = ref_graph, dict(extents), model, blocks
+
+    def key_salt(self) -> str:
+        return "analytic-cuda:" + ",".join(f"{k}={v}" for k, v in sorted(self.extents.items()))
+
+    def __call__(self, organism):
+        from matfuse import contract_arrays, lower
+        ir = ir_from_matfuse(contract_arrays(lower(organism, self.ref_graph)))
+        return estimate_cost_ir(ir, self.extents, self.model, self.blocks)
