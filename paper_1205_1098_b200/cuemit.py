@@ -392,9 +392,17 @@ class _Emitter:
                     lab, e0 = ps["labels"][0], ps["extents"][0]
                     w.put(f"const long {lab} = (long)blockIdx.x * blockDim.x + threadIdx.x;")
                     w.open(f"if ({lab} < {e0})")
-                    w.put(f"double acc = {pname}[{lab}];")
-                    w.put(f"for (long b = 1; b < nblocks_; ++b) acc += {pname}[b * ({e0}) + {lab}];")
-                    w.put(f"{self.ref(result)} = acc;")
+                    # ascending blocks dealt to 8 independent chains (fixed order): the
+                    # partials sit in L2 and one dependent chain would pay its latency nblocks times
+                    w.put("double a_[8] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};")
+                    w.put("long b = 0;")
+                    w.open("for (; b + 8 <= nblocks_; b += 8)")
+                    w.put("#pragma unroll")
+                    w.put(f"for (int u = 0; u < 8; ++u) a_[u] += {pname}[(b + u) * ({e0}) + {lab}];")
+                    w.close()
+                    w.put("#pragma unroll")
+                    w.put(f"for (int u = 0; u < 8; ++u) if (b + u < nblocks_) a_[u] += {pname}[(b + u) * ({e0}) + {lab}];")
+                    w.put(f"{self.ref(result)} = ((a_[0] + a_[1]) + (a_[2] + a_[3])) + ((a_[4] + a_[5]) + (a_[6] + a_[7]));")
                     w.close()
                     grid = f"(unsigned)(({e0} + 255) / 256)"
                 w.close()
@@ -420,14 +428,25 @@ class _Emitter:
                 t = max(int(ir["threads"][region["slot"]]), self.blocks)
                 size = " * ".join([f"(size_t){t}"] + [f"(size_t){e}" for e in s["extents"]])
                 temps.append((name, size))
+        if temps:
+            # keep freed temporaries in the stream-ordered pool across calls (the default
+            # release threshold of 0 hands them back to the driver at every sync)
+            w.put("static bool pool_ready_ = false;")
+            w.open("if (!pool_ready_)")
+            w.put("int dev_ = 0; cudaGetDevice(&dev_);")
+            w.put("cudaMemPool_t pool_; cudaDeviceGetDefaultMemPool(&pool_, dev_);")
+            w.put("unsigned long long keep_ = ~0ULL;")
+            w.put("cudaMemPoolSetAttribute(pool_, cudaMemPoolAttrReleaseThreshold, &keep_);")
+            w.put("pool_ready_ = true;")
+            w.close()
         for name, size in temps:
             w.put(f"double *{name} = nullptr;")
-            w.put(f"cudaMalloc(&{name}, sizeof(double) * ({size}));")
+            w.put(f"cudaMallocAsync(&{name}, sizeof(double) * ({size}), 0);")
         for stmt in launches:
             w.put(stmt)
+        for name, _ in temps:      # stream-ordered pool: no device-wide sync per temporary
+            w.put(f"cudaFreeAsync({name}, 0);")
         w.put("cudaStreamSynchronize(0);")
-        for name, _ in temps:
-            w.put(f"cudaFree({name});")
         w.close()
         w.put()
         w.open(f'extern "C" int {kname}_last_cuda_error(void)')
@@ -646,12 +665,12 @@ class EmitModel:
     profiles/r01/organism_times.json (120 organisms x n = 1024, 2048, 4096)."""
     peak_gbs: float = 6500.0        # HBM ceiling of a full grid
     cta_gbs: float = 100.0          # what one CTA streams on its own
-    launch_us: float = 15.0         # per kernel launch (incl. its share of the final sync)
-    step_us: float = 0.6            # one strided-loop execution: barriers + CTA reduction
-    trip_us: float = 0.05           # one trip of a thread through a strided loop
-    rmw_trip_us: float = 0.2        # the same when the trip read-modify-writes global memory
-    stmt_us: float = 0.3            # a uniform statement that writes memory (thread 0 + barrier)
-    alloc_us: float = 550.0         # cudaMalloc + cudaFree of one temporary / partial buffer per call
+    launch_us: float = 20.0         # per kernel launch (incl. its share of the final sync)
+    step_us: float = 0.4            # one strided-loop execution: barriers + CTA reduction
+    trip_us: float = 0.06           # one trip of a thread through a strided loop
+    rmw_trip_us: float = 0.25       # the same when the trip read-modify-writes global memory
+    stmt_us: float = 0.6            # a uniform statement that writes memory (thread 0 + barrier)
+    alloc_us: float = 30.0          # stream-ordered malloc + free of one temporary / partial per call
                                     # (the reference pays malloc/free per call too, cemit.py:183-202)
     sm_count: int = 148
 
