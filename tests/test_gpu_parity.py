@@ -497,3 +497,33 @@ def test_join_fused_exchange_emulated_ranks(bto_lib, oracle, world):
     finally:
         _native.set_tuning(exchange_phases=3)
         _native.check(lib.bto_exchange_shutdown())
+
+
+def test_bench_suite_shards_cleanly_as_rank_1_of_4(bto_lib, monkeypatch):
+    """bench.py's per-rank buffers and launches for N > 1 (rank 1 of 4), with the
+    all-reduce stubbed out: exercises the row-block slicing, the views GESUMMV
+    borrows, and the split GEMVER path, which a 1-GPU box cannot run under NCCL."""
+    import sys
+    from pathlib import Path
+    sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
+    import bench
+    from paper_1205_1098_b200 import sharded
+
+    calls = []
+
+    class FakeComm:
+        def all_reduce_sum(self, tensor):
+            calls.append(tensor.numel())
+
+    monkeypatch.setattr(sharded, "TorchComm", FakeComm)
+    suite = bench.Suite(torch, 1, 4, bench.SUITE)
+    assert suite.rows == 8192 and suite.grows == 6144 and suite.an == (1 << 27) // 4
+    for name in bench.SUITE:
+        suite.launch(name)
+    torch.cuda.synchronize()
+    assert calls == [1, 32768, 32768, 32768]          # axpydot, bicgk s, atax y, gemver B'y
+    for t in (suite.q, suite.s, suite.x, suite.w, suite.gy, suite.az, suite.abeta):
+        assert bool(torch.isfinite(t).all())
+    # the shard's GEMVER equals the definition on its rows (x replicated)
+    want_w = 0.83 * torch.mv(suite.Bm, suite.x)
+    assert float(torch.max(torch.abs(suite.w - want_w) / torch.clamp(torch.abs(want_w), min=1.0))) < 1e-11
