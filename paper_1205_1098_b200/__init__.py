@@ -14,6 +14,9 @@ from .runtime import (BENCH_CONFIGS, CHECK_CONFIGS, SEEDS, GeneratedKernel,
                       load_graph, max_rel_error, random_inputs, run_kernel,
                       run_kernel_async, workdir)
 from ._native import BtoError, NativeLibraryMissing, library_path
+from .cost import (AnalyticGpuCost, CostReport, GpuEmpiricalTimer, GpuMachineModel, GpuVariant,
+                   cached, estimate_cost)
+from .search import SearchConfig, SearchResult, run_strategy
 
 __version__ = "0.1.0"
 
@@ -25,4 +28,6 @@ __all__ = [
     "ToolchainError", "gen_inputs", "gpu_kernel", "load_graph", "max_rel_error",
     "random_inputs", "run_kernel", "run_kernel_async", "workdir",
     "BtoError", "NativeLibraryMissing", "library_path",
+    "AnalyticGpuCost", "CostReport", "GpuEmpiricalTimer", "GpuMachineModel", "GpuVariant",
+    "cached", "estimate_cost", "SearchConfig", "SearchResult", "run_strategy",
 ]
