@@ -4,18 +4,18 @@
 // loops of a row back to back, the second touch of the row coming from the
 // CPU cache ({_i{_j 1}{_j 2}}, fuse.py:660-688).
 // A 32768-double row is 256 KiB -- more than one SM's shared memory -- so here
-// a thread-block CLUSTER of C CTAs holds a panel of RG rows between them:
+// a thread-block CLUSTER of C CTAs holds a panel of TR rows between them:
 //
 //   CTA k of the cluster owns columns [k*W, (k+1)*W) of every row of the panel
 //   and keeps them in shared memory, filled by TMA bulk copies
 //   (cp.async.bulk, one per row segment, completion on an mbarrier) through an
-//   S-stage ring, so S-1 panels are always in flight while one is consumed;
+//   S-stage ring, so up to S-1 panels are in flight while one is consumed;
 //   phase 1  every CTA reduces its slice of the row dots (registers -> warp
 //            shuffle -> shared memory) and PUSHES its partial sums into the
 //            shared memory of every CTA of the cluster with st.async, which
 //            counts the bytes on the RECEIVER's mbarrier for that panel;
 //            the tile is read from shared memory ONCE, into registers, and the
-//            stage goes back to the producer right away;
+//            stage is refilled right away;
 //   phase 2  one panel later (software pipeline: the exchange latency hides
 //            behind the next panel's phase 1, no lock-step cluster barrier)
 //            every CTA waits on its own mbarrier, adds the C partials in rank
@@ -27,8 +27,8 @@
 // stage is free and is refilled with the panel S steps ahead (no "empty"
 // mbarrier, and no extra warp -- a ninth warp would cap the kernel at 168
 // registers per thread, too few for two register tiles).
-// Shared-memory reads are 8 bytes per matrix byte-pair less than a two-touch
-// scheme would need, which matters because under the 1 kW power cap the SM
+// One shared-memory read per element instead of two matters because under the
+// 1 kW power cap the SM
 // clock drops to ~1.75 GHz and the per-panel latency chain is what bounds the
 // kernel (profiles/r01/drift_probe.log).
 //
@@ -54,7 +54,7 @@ struct AtaxArgs {
 constexpr int kAtaxMaxCluster = 16;
 constexpr int kAtaxMaxRows = 8;
 constexpr int kAtaxMaxStages = 8;
-constexpr int kAtaxSlots = 8;                      // exchange slots; needs > 2*L + 1
+constexpr int kAtaxSlots = 8;                      // exchange slots; phase 1 runs one panel ahead, needs > 3
 constexpr int kAtaxThreads = kThreads;             // 8 warps; thread 0 also issues the TMA copies
 
 __device__ __forceinline__ uint32_t smem_u32(const void *p)
