@@ -47,6 +47,10 @@ CPU_SAMPLE = {"axpydot": (1 << 26, 1), "bicgk": (16384, 16384), "atax": (16384, 
               "gesummv": (12288, 12288), "gemver": (16384, 16384)}
 
 
+WORKLOAD = ("suite5: AXPYDOT n=2^27, BiCGK n=32768, ATAX n=32768, GESUMMV n=24576, "
+            "GEMVER n=32768")
+
+
 def bytes_min(kernel: str, M: int, N: int) -> float:
     """SURVEY.md section 8d (same table as bto_bytes_min in the library)."""
     m, n = float(M), float(N)
@@ -186,13 +190,16 @@ def run_reference_arm(args) -> int:
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0
-    base = cpu_baseline(steps=max(1, args.steps), warmup=max(1, min(args.warmup, 3)))
+    kernels = SUITE if args.kernel == "suite" else (args.kernel,)
+    base = cpu_baseline(steps=max(1, args.steps), warmup=max(1, min(args.warmup, 3)), kernels=kernels)
     line = {
         "impl": "reference", "metric": "effective HBM GB/s (min bytes/time), fused suite",
         "value": base["value"], "unit": "GB/s", "n_gpus": args.gpus, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": base["ms_per_step"], "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": "suite5 (AXPYDOT, BiCGK, ATAX, GESUMMV, GEMVER), bounded CPU sample",
+        "config": {"workload": WORKLOAD if args.kernel == "suite" else
+                   f"{args.kernel} at BASELINE bench size {BENCH[args.kernel]}",
+                   "parallelism": f"{base['cores']} host threads (OpenMP, the reference's generated C)",
                    "sample": base["sample"]},
         "cpu_baseline": {k: base[k] for k in ("value", "unit", "cores", "kind", "sample")},
         "per_kernel": base["per_kernel"],
@@ -452,8 +459,7 @@ def run_gpu_arm(args) -> int:
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
         "dtype": "f64", "data": "synthetic",
         "config": {
-            "workload": "suite5: AXPYDOT n=2^27, BiCGK n=32768, ATAX n=32768, GESUMMV n=24576, "
-                        "GEMVER n=32768" if args.kernel == "suite" else
+            "workload": WORKLOAD if args.kernel == "suite" else
                         f"{args.kernel} at BASELINE bench size {BENCH[args.kernel]}",
             "parallelism": f"row-shard x{world}, exchange: {suite.exchange_kind}" if world > 1
                            else "single GPU",
