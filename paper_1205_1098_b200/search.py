@@ -29,7 +29,8 @@ from pathlib import Path
 from .cost import CachedFitness, CostReport, GpuVariant, cached, variant_space
 from .spec import match_corpus
 
-__all__ = ["SearchConfig", "LogEntry", "SearchResult", "run_strategy", "write_run", "STRATEGIES"]
+__all__ = ["SearchConfig", "LogEntry", "SearchResult", "run_strategy", "write_run", "STRATEGIES",
+           "Autotuner"]
 
 STRATEGIES = ("default", "exhaustive", "random", "ga")
 
@@ -218,3 +219,70 @@ def write_run(outdir, graph, result: SearchResult, cfg: SearchConfig, fitness_so
     }
     (outdir / "summary.json").write_text(json.dumps(summary, indent=2) + "\n")
     return summary
+
+
+# ---------------------------------------------------------------------------
+# persistent tuning: search once per (kernel, extents), reuse afterwards
+
+class Autotuner:
+    """BTO's thesis -- pick the variant by measuring -- as a cache in front of the
+    library: `best(graph, extents)` searches the launch variants once (empirical
+    fitness by default), stores the winner in a JSON file keyed by kernel, extents and
+    device, and returns it from the file afterwards; `applied(variant)` is a context
+    manager that installs the variant's tunables for the duration of a call and
+    restores the previous ones."""
+
+    def __init__(self, path, strategy: str = "exhaustive", cfg: SearchConfig | None = None,
+                 fitness_factory=None, device_tag: str | None = None):
+        self.path = Path(path)
+        self.strategy, self.cfg = strategy, cfg or SearchConfig()
+        self.fitness_factory = fitness_factory
+        self.device_tag = device_tag
+        self._table = json.loads(self.path.read_text()) if self.path.exists() else {}
+
+    def _key(self, kernel: str, extents: dict) -> str:
+        if self.device_tag is None:
+            try:
+                from ._native import device_info
+                info = device_info()
+                self.device_tag = f"sm{info['sm_count']}"
+            except Exception:           # no device: analytic tuning only
+                self.device_tag = "nodevice"
+        ext = ",".join(f"{k}={int(v)}" for k, v in sorted(extents.items()))
+        return f"{kernel}|{ext}|{self.device_tag}"
+
+    def best(self, graph, extents: dict) -> GpuVariant:
+        kernel = match_corpus(graph.spec)
+        key = self._key(kernel, extents)
+        if key in self._table:
+            entry = self._table[key]
+            return GpuVariant(kernel, tuple((k, int(v)) for k, v in entry["tuning"]))
+        if self.fitness_factory is not None:
+            fitness = self.fitness_factory(graph, extents)
+        else:
+            from .cost import GpuEmpiricalTimer
+            fitness = cached(GpuEmpiricalTimer(graph, extents))
+        result = run_strategy(self.strategy, graph, self.cfg, fitness)
+        self._table[key] = {"tuning": [list(kv) for kv in result.best.tuning],
+                            "fitness": result.best_fitness, "strategy": self.strategy,
+                            "evaluations": result.evaluations}
+        self.path.parent.mkdir(parents=True, exist_ok=True)
+        self.path.write_text(json.dumps(self._table, indent=1, sort_keys=True) + "\n")
+        return result.best
+
+    @staticmethod
+    def applied(variant: GpuVariant):
+        from contextlib import contextmanager
+
+        from . import _native
+
+        @contextmanager
+        def scope():
+            saved = {k: _native.get_tuning(k) for k, _ in variant.tuning}
+            _native.set_tuning(**dict(variant.tuning))
+            try:
+                yield variant
+            finally:
+                _native.set_tuning(**saved)
+
+        return scope()

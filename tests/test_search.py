@@ -91,3 +91,46 @@ def test_empirical_search_on_device():
     res = S.run_strategy("exhaustive", g, S.SearchConfig(), timer, space=space)
     assert res.evaluations == 3 and not res.best_report.failed
     assert all(e.elapsed_s > 0 for e in res.log)
+
+
+def test_autotuner_searches_once_and_persists(tmp_path):
+    calls = []
+
+    def factory(graph, extents):
+        calls.append(dict(extents))
+        m = C.GpuMachineModel(extents=tuple(sorted(extents.items())))
+        return C.cached(C.AnalyticGpuCost(graph, m))
+
+    g = bto.load_graph("atax")
+    path = tmp_path / "cache" / "tuned.json"
+    tuner = S.Autotuner(path, fitness_factory=factory, device_tag="test")
+    a = tuner.best(g, {"M": 4096, "N": 4096})
+    b = tuner.best(g, {"M": 4096, "N": 4096})
+    assert a == b and len(calls) == 1                     # second lookup is served from the table
+    tuner.best(g, {"M": 8192, "N": 4096})
+    assert len(calls) == 2                                 # another shape is another search
+    again = S.Autotuner(path, fitness_factory=factory, device_tag="test")
+    assert again.best(g, {"M": 4096, "N": 4096}) == a and len(calls) == 2     # persisted
+    table = json.loads(path.read_text())
+    assert set(table) == {"atax|M=4096,N=4096|test", "atax|M=8192,N=4096|test"}
+    assert set(next(iter(table.values()))) == {"tuning", "fitness", "strategy", "evaluations"}
+
+
+def test_applied_variant_is_restored():
+    from paper_1205_1098_b200 import _native
+    before = _native.get_tuning("mv_rows")
+    with S.Autotuner.applied(C.GpuVariant("bicgk", (("mv_rows", 16),))):
+        assert _native.get_tuning("mv_rows") == 16
+    assert _native.get_tuning("mv_rows") == before
+
+
+@pytest.mark.gpu
+def test_autotuner_with_the_empirical_timer(tmp_path):
+    g = bto.load_graph("gesummv")
+    tuner = S.Autotuner(tmp_path / "tuned.json", strategy="random", cfg=S.SearchConfig(budget=4, seed=1))
+    best = tuner.best(g, {"M": 4096, "N": 4096})
+    assert best.kernel == "gesummv"
+    with S.Autotuner.applied(best):
+        inputs = bto.gen_inputs(g, {"M": 64, "N": 64}, seed=1)
+        out = bto.run_kernel(bto.library_path(), bto.gpu_kernel(g), g, inputs, {"M": 64, "N": 64})
+    assert out["y"].shape == (64,)
