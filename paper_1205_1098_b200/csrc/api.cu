@@ -37,8 +37,10 @@ void axpydot(const double *w, const double *v, const double *u, double alpha,
     Call c;
     if (!extents_ok(c, M, 1)) return;
     const long P = panel_count(8.0 * (double)M);
+    // duplex panel pipeline for pinned buffers; pageable ones go through the bounce slots
     const bool stream_it = g_tuning.host_pipeline && M >= (1L << 22) && host_memory(w) &&
-                           host_memory(v) && host_memory(u) && host_memory(z);
+                           host_memory(v) && host_memory(u) && host_memory(z) &&
+                           !(g_tuning.host_bounce && (pageable_memory(w) || pageable_memory(z)));
     if (stream_it) {
         double *dots = nullptr;
         c.in_streamed(&w, M); c.in_streamed(&v, M); c.in_streamed(&u, M);
@@ -500,6 +502,9 @@ static long *tuning_slot(const char *key)
     if (!strcmp(key, "debug")) return &g_tuning.debug;
     if (!strcmp(key, "pdl")) return &g_tuning.pdl;
     if (!strcmp(key, "exchange_phases")) return &g_tuning.exchange_phases;
+    if (!strcmp(key, "host_bounce")) return &g_tuning.host_bounce;
+    if (!strcmp(key, "host_threads")) return &g_tuning.host_threads;
+    if (!strcmp(key, "host_nt")) return &g_tuning.host_nt;
     if (!strcmp(key, "host_pipeline")) return &g_tuning.host_pipeline;
     if (!strcmp(key, "host_panel_mib")) return &g_tuning.host_panel_mib;
     return nullptr;
@@ -515,7 +520,8 @@ int bto_set_tuning(const char *key, long value)
     if (slot == &g_tuning.mv_minb) ok = value == 0 || value == 1 || value == 2 || value == 3 || value == 4 || value == 6;
     if (slot == &g_tuning.mv_vec) ok = value == 0 || value == 1 || value == 2;
     if (slot == &g_tuning.vec_unroll) ok = value == 1 || value == 2 || value == 4;
-    if (slot == &g_tuning.atax_fused || slot == &g_tuning.host_pipeline) ok = value == 0 || value == 1;
+    if (slot == &g_tuning.atax_fused || slot == &g_tuning.host_pipeline || slot == &g_tuning.host_bounce || slot == &g_tuning.host_nt) ok = value == 0 || value == 1;
+    if (slot == &g_tuning.host_threads) ok = value >= 0 && value <= 64;
     if (slot == &g_tuning.host_panel_mib) ok = value >= 1 && value <= 4096;
     if (slot == &g_tuning.exchange_phases) ok = value >= 1 && value <= 3;
     if (slot == &g_tuning.atax_cluster) ok = value == 0 || value == 1 || value == 2 || value == 4 || value == 8 || value == 16;
@@ -583,6 +589,10 @@ int bto_release_workspace(void)
     if (c.arena) CUDA_TRY(cudaFree(c.arena));
     c.ws = nullptr; c.ws_bytes = 0;
     c.arena = nullptr; c.arena_bytes = 0;
+    for (int i = 0; i < 6; ++i) {
+        if (c.bounce[i]) CUDA_TRY(cudaFreeHost(c.bounce[i]));
+        c.bounce[i] = nullptr;
+    }
     return BTO_OK;
 }
 

@@ -7,6 +7,11 @@
 #include <cstring>
 #include <map>
 #include <mutex>
+#include <thread>
+#include <condition_variable>
+#if defined(__SSE2__)
+#include <emmintrin.h>
+#endif
 #include <vector>
 
 #include "bto_b200.h"
@@ -65,6 +70,9 @@ struct Tuning {
     long pdl = 1;            // joins launched as programmatic dependents of their producer
     long debug = 0;          // print launch plans to stderr
     long exchange_phases = 3;    // bit 0 publish, bit 1 wait+reduce (tests emulate ranks with 1, 2)
+    long host_bounce = 1;        // pageable operands >= 16 MiB go through pinned bounce slots
+    long host_nt = 1;            // non-temporal stores in the host-side bounce copies
+    long host_threads = 0;       // host threads copying into / out of the bounce slots (0 = auto)
     long host_pipeline = 1;  // overlap H2D / compute / D2H in row panels for host operands
     long host_panel_mib = 256;   // panel size of that pipeline
 };
@@ -92,6 +100,10 @@ struct DeviceCtx {
     double **exch_bufs = nullptr;      // device array [world] of peer-mapped buffers
     unsigned int **exch_flags = nullptr;
     unsigned int exch_epoch = 0;
+    // pageable host operands: pinned bounce slots filled / drained by host threads
+    // (slots 0-2 carry host->device traffic, 3-5 device->host, so both directions can run at once)
+    char *bounce[6] = {};
+    cudaEvent_t bounce_ev[6] = {};
     // host-pointer pipeline: copy-in and copy-out streams, reusable events
     cudaStream_t copy_in = nullptr, copy_out = nullptr;
     std::vector<cudaEvent_t> events;

@@ -22,6 +22,227 @@ bool host_memory(const void *p)
     return !(attr.type == cudaMemoryTypeDevice || attr.type == cudaMemoryTypeManaged);
 }
 
+// true for ordinary (pageable, unregistered) host memory
+bool pageable_memory(const void *p)
+{
+    cudaPointerAttributes attr;
+    if (cudaPointerGetAttributes(&attr, p) != cudaSuccess) {
+        cudaGetLastError();
+        return true;
+    }
+    return attr.type == cudaMemoryTypeUnregistered;
+}
+
+// ---------------------------------------------------------------------------
+// Pageable host operands.  cudaMemcpyAsync from pageable memory runs at
+// ~11 GB/s on this platform (the driver bounces it through a small pinned
+// buffer on one thread); the reference's own caller passes exactly such
+// buffers (numpy arrays, runtime.py:99-150).  Large pageable operands are
+// therefore copied by several host threads into three pinned 64 MiB slots
+// that the copy engine drains (or fills, for outputs) concurrently.
+
+constexpr size_t kBounceBytes = 64u << 20;
+constexpr size_t kBounceMin = 16u << 20;       // smaller copies are not worth the threads
+
+// slots [base, base+3)
+cudaError_t bounce_setup(DeviceCtx &c, int base)
+{
+    for (int i = base; i < base + 3; ++i) {
+        cudaError_t e = cudaSuccess;
+        if (!c.bounce[i]) e = cudaHostAlloc(reinterpret_cast<void **>(&c.bounce[i]), kBounceBytes, cudaHostAllocDefault);
+        if (e == cudaSuccess && !c.bounce_ev[i]) e = cudaEventCreateWithFlags(&c.bounce_ev[i], cudaEventDisableTiming);
+        if (e != cudaSuccess) return e;
+    }
+    return cudaSuccess;
+}
+
+int host_copy_threads()
+{
+    if (g_tuning.host_threads > 0) return (int)g_tuning.host_threads;
+    unsigned hw = std::thread::hardware_concurrency();
+    int t = hw ? (int)hw : 4;
+    if (t > 16) t = 16;
+    return t;
+}
+
+// memcpy with non-temporal stores: the destination (a bounce slot the copy engine
+// reads next, or a result the caller reads later) is not wanted in this core's cache,
+// and skipping the read-for-ownership saves a third of the host memory traffic.
+void stream_copy(char *dst, const char *src, size_t bytes)
+{
+#if defined(__SSE2__)
+    if (g_tuning.host_nt && bytes >= 4096) {
+        const size_t head = (16 - (reinterpret_cast<uintptr_t>(dst) & 15)) & 15;
+        memcpy(dst, src, head);
+        dst += head; src += head; bytes -= head;
+        const size_t blocks = bytes / 64;
+        for (size_t b = 0; b < blocks; ++b, dst += 64, src += 64) {
+            const __m128i r0 = _mm_loadu_si128(reinterpret_cast<const __m128i *>(src));
+            const __m128i r1 = _mm_loadu_si128(reinterpret_cast<const __m128i *>(src + 16));
+            const __m128i r2 = _mm_loadu_si128(reinterpret_cast<const __m128i *>(src + 32));
+            const __m128i r3 = _mm_loadu_si128(reinterpret_cast<const __m128i *>(src + 48));
+            _mm_stream_si128(reinterpret_cast<__m128i *>(dst), r0);
+            _mm_stream_si128(reinterpret_cast<__m128i *>(dst + 16), r1);
+            _mm_stream_si128(reinterpret_cast<__m128i *>(dst + 32), r2);
+            _mm_stream_si128(reinterpret_cast<__m128i *>(dst + 48), r3);
+        }
+        _mm_sfence();
+        memcpy(dst, src, bytes - blocks * 64);
+        return;
+    }
+#endif
+    memcpy(dst, src, bytes);
+}
+
+void parallel_memcpy(char *dst, const char *src, size_t bytes, int nt)
+{
+    if (nt <= 1 || bytes < (4u << 20)) {
+        stream_copy(dst, src, bytes);
+        return;
+    }
+    std::vector<std::thread> pool;
+    const size_t piece = ((bytes / nt) + 4095) & ~size_t(4095);
+    for (int t = 1; t < nt; ++t) {
+        const size_t lo = piece * t;
+        if (lo >= bytes) break;
+        const size_t len = lo + piece < bytes ? piece : bytes - lo;
+        pool.emplace_back([=] { stream_copy(dst + lo, src + lo, len); });
+    }
+    stream_copy(dst, src, piece < bytes ? piece : bytes);
+    for (std::thread &th : pool) th.join();
+}
+
+// host (pageable) -> device, enqueued on `s`; returns once `src` has been read.
+// (cudaError_t, no fail(): the device->host twin also runs on a helper thread.)
+cudaError_t h2d_bounced(DeviceCtx &c, void *dst, const void *src, size_t bytes, cudaStream_t s,
+                        int nt)
+{
+    cudaError_t e = bounce_setup(c, 0);
+    size_t off = 0;
+    for (int i = 0; off < bytes && e == cudaSuccess; ++i, off += kBounceBytes) {
+        const int slot = i % 3;
+        const size_t len = bytes - off < kBounceBytes ? bytes - off : kBounceBytes;
+        e = cudaEventSynchronize(c.bounce_ev[slot]);              // slot drained by its last copy
+        if (e != cudaSuccess) break;
+        parallel_memcpy(c.bounce[slot], static_cast<const char *>(src) + off, len, nt);
+        e = cudaMemcpyAsync(static_cast<char *>(dst) + off, c.bounce[slot], len,
+                            cudaMemcpyHostToDevice, s);
+        if (e == cudaSuccess) e = cudaEventRecord(c.bounce_ev[slot], s);
+    }
+    return e;
+}
+
+// device -> host (pageable); everything queued on `s` before the call is waited for
+cudaError_t d2h_bounced(DeviceCtx &c, void *dst, const void *src, size_t bytes, cudaStream_t s,
+                        int nt)
+{
+    cudaError_t e = bounce_setup(c, 3);
+    if (e != cudaSuccess) return e;
+    const size_t nchunks = (bytes + kBounceBytes - 1) / kBounceBytes;
+    auto issue = [&](size_t i) -> cudaError_t {
+        const int slot = 3 + (int)(i % 3);
+        const size_t off = i * kBounceBytes;
+        const size_t len = bytes - off < kBounceBytes ? bytes - off : kBounceBytes;
+        cudaError_t r = cudaMemcpyAsync(c.bounce[slot], static_cast<const char *>(src) + off, len,
+                                        cudaMemcpyDeviceToHost, s);
+        return r == cudaSuccess ? cudaEventRecord(c.bounce_ev[slot], s) : r;
+    };
+    // two copies in flight while the third slot is emptied by the host threads
+    for (size_t i = 0; i < nchunks && i < 2 && e == cudaSuccess; ++i) e = issue(i);
+    for (size_t i = 0; i < nchunks && e == cudaSuccess; ++i) {
+        const int slot = 3 + (int)(i % 3);
+        const size_t off = i * kBounceBytes;
+        const size_t len = bytes - off < kBounceBytes ? bytes - off : kBounceBytes;
+        if (i + 2 < nchunks) e = issue(i + 2);                    // its slot was emptied at i-1
+        if (e == cudaSuccess) e = cudaEventSynchronize(c.bounce_ev[slot]);
+        if (e != cudaSuccess) break;
+        parallel_memcpy(static_cast<char *>(dst) + off, c.bounce[slot], len, nt);
+    }
+    return e;
+}
+
+bool bounce_wanted(const void *host, size_t bytes)
+{
+    return g_tuning.host_bounce && bytes >= kBounceMin && pageable_memory(host);
+}
+
+// one host <-> device transfer on `s`, through the bounce slots when that pays
+int copy_in(DeviceCtx &c, void *dst, const void *src, size_t bytes, cudaStream_t s, int nt = 0)
+{
+    if (bounce_wanted(src, bytes)) {
+        CUDA_TRY(h2d_bounced(c, dst, src, bytes, s, nt ? nt : host_copy_threads()));
+        return BTO_OK;
+    }
+    CUDA_TRY(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, s));
+    return BTO_OK;
+}
+
+int copy_out(DeviceCtx &c, void *dst, const void *src, size_t bytes, cudaStream_t s, int nt = 0)
+{
+    if (bounce_wanted(dst, bytes)) {
+        CUDA_TRY(d2h_bounced(c, dst, src, bytes, s, nt ? nt : host_copy_threads()));
+        return BTO_OK;
+    }
+    CUDA_TRY(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, s));
+    return BTO_OK;
+}
+
+// Drains finished device panels into pageable host memory on a helper thread while the
+// calling thread keeps feeding the other direction.  post() hands over a panel whose
+// producer event has ALREADY been recorded; close() waits for the last one.
+class PanelDrain {
+public:
+    PanelDrain(DeviceCtx &c, cudaStream_t s, int nt) : c_(c), s_(s), nt_(nt) {}
+    ~PanelDrain() { close(); }
+    void post(void *dst, const void *src, size_t bytes, cudaEvent_t produced)
+    {
+        if (!worker_.joinable()) worker_ = std::thread([this] { run(); });
+        std::lock_guard<std::mutex> g(mu_);
+        jobs_.push_back({dst, src, bytes, produced});
+        cv_.notify_one();
+    }
+    cudaError_t close()
+    {
+        if (worker_.joinable()) {
+            {
+                std::lock_guard<std::mutex> g(mu_);
+                closed_ = true;
+                cv_.notify_one();
+            }
+            worker_.join();
+        }
+        return err_;
+    }
+
+private:
+    struct Job { void *dst; const void *src; size_t bytes; cudaEvent_t produced; };
+    void run()
+    {
+        err_ = cudaSetDevice(c_.device);
+        for (size_t next = 0;; ++next) {
+            Job j;
+            {
+                std::unique_lock<std::mutex> g(mu_);
+                cv_.wait(g, [&] { return next < jobs_.size() || closed_; });
+                if (next >= jobs_.size()) return;
+                j = jobs_[next];
+            }
+            if (err_ != cudaSuccess) continue;                    // keep consuming, copy nothing
+            err_ = cudaStreamWaitEvent(s_, j.produced, 0);
+            if (err_ == cudaSuccess) err_ = d2h_bounced(c_, j.dst, j.src, j.bytes, s_, nt_);
+        }
+    }
+    DeviceCtx &c_;
+    cudaStream_t s_;
+    int nt_;
+    std::thread worker_;
+    std::mutex mu_;
+    std::condition_variable cv_;
+    std::vector<Job> jobs_;
+    bool closed_ = false;
+    cudaError_t err_ = cudaSuccess;
+};
+
 class Call {
 public:
     Call() : lock_(g_mu)
@@ -104,13 +325,8 @@ public:
             a.host = *a.slot;
             *a.slot = reinterpret_cast<double *>(ctx_->arena + a.offset);
             if (!a.is_out && !a.streamed) {
-                cudaError_t e = cudaMemcpyAsync(*a.slot, a.host, (size_t)a.count * sizeof(double),
-                                                cudaMemcpyHostToDevice, stream());
-                if (e != cudaSuccess) {
-                    status(fail(BTO_ERR_CUDA, "host->device copy failed: %s",
-                                cudaGetErrorString(e)));
-                    return;
-                }
+                status(copy_in(*ctx_, *a.slot, a.host, (size_t)a.count * sizeof(double), stream()));
+                if (!ok()) return;
             }
         }
     }
@@ -122,13 +338,8 @@ public:
         if (ok()) {
             for (Arg &a : args_) {
                 if (!a.on_host || !a.is_out || a.streamed || a.scratch) continue;
-                cudaError_t e = cudaMemcpyAsync(a.host, *a.slot, (size_t)a.count * sizeof(double),
-                                                cudaMemcpyDeviceToHost, stream());
-                if (e != cudaSuccess) {
-                    status(fail(BTO_ERR_CUDA, "device->host copy failed: %s",
-                                cudaGetErrorString(e)));
-                    break;
-                }
+                status(copy_out(*ctx_, a.host, *a.slot, (size_t)a.count * sizeof(double), stream()));
+                if (!ok()) break;
             }
         }
         cudaError_t e = cudaStreamSynchronize(stream());
@@ -226,6 +437,12 @@ int gemver_streamed(DeviceCtx &c, cudaStream_t main, const double *hA, double *d
     CUDA_TRY(cudaEventRecord(ready, main));
     CUDA_TRY(cudaStreamWaitEvent(c.copy_in, ready, 0));
     CUDA_TRY(cudaStreamWaitEvent(c.copy_out, ready, 0));
+    // pageable A / B: this thread fills the inbound bounce slots, a helper drains B
+    const size_t panel_bytes = (size_t)(M / P) * N * sizeof(double);
+    const bool drain_b = bounce_wanted(hB, panel_bytes);
+    const int nt = host_copy_threads();
+    const int nt_in = drain_b && bounce_wanted(hA, panel_bytes) ? (nt + 1) / 2 : nt;
+    PanelDrain drain(c, c.copy_out, nt_in < nt ? nt - nt_in : nt);
     for (long p = 0; p < P; ++p) {
         const long r0 = (M * p) / P, r1 = (M * (p + 1)) / P;
         if (r1 == r0) {
@@ -233,7 +450,7 @@ int gemver_streamed(DeviceCtx &c, cudaStream_t main, const double *hA, double *d
             continue;
         }
         const size_t off = (size_t)r0 * N, bytes = (size_t)(r1 - r0) * N * sizeof(double);
-        CUDA_TRY(cudaMemcpyAsync(dA + off, hA + off, bytes, cudaMemcpyHostToDevice, c.copy_in));
+        BTO_TRY(copy_in(c, dA + off, hA + off, bytes, c.copy_in, nt_in));
         CUDA_TRY(cudaEventRecord(c.events[2 * p], c.copy_in));
         CUDA_TRY(cudaStreamWaitEvent(main, c.events[2 * p], 0));
         FinArgs f{};
@@ -242,11 +459,16 @@ int gemver_streamed(DeviceCtx &c, cudaStream_t main, const double *hA, double *d
         BTO_TRY(seq_pass1(c, dA + off, u1 + r0, v1, u2 + r0, v2, y + r0, dB + off, f, r1 - r0, N,
                           main));
         CUDA_TRY(cudaEventRecord(c.events[2 * p + 1], main));
-        CUDA_TRY(cudaStreamWaitEvent(c.copy_out, c.events[2 * p + 1], 0));
-        CUDA_TRY(cudaMemcpyAsync(hB + off, dB + off, bytes, cudaMemcpyDeviceToHost, c.copy_out));
+        if (drain_b) {
+            drain.post(hB + off, dB + off, bytes, c.events[2 * p + 1]);
+        } else {
+            CUDA_TRY(cudaStreamWaitEvent(c.copy_out, c.events[2 * p + 1], 0));
+            CUDA_TRY(cudaMemcpyAsync(hB + off, dB + off, bytes, cudaMemcpyDeviceToHost, c.copy_out));
+        }
     }
     BTO_TRY(join_partials(panel_sums, P, N, kColAxpz, beta, z, x, main));
     BTO_TRY(seq_pass2(c, dB, x, alpha, w, M, N, main));
+    CUDA_TRY(drain.close());
     // the caller's finish() copies x and w on `main`; B must have landed too
     CUDA_TRY(cudaEventRecord(done, c.copy_out));
     CUDA_TRY(cudaStreamWaitEvent(main, done, 0));

@@ -258,6 +258,31 @@ def test_host_operand_pipeline(bto_lib, oracle):
         _native.set_tuning(host_pipeline=1, host_panel_mib=256)
 
 
+def test_pageable_host_operands_bounce(bto_lib, oracle):
+    """Pageable (numpy) operands of 16 MiB and more travel through the pinned bounce
+    slots, filled and drained by host threads: one chunk, several chunks, more chunks
+    than slots, every thread count, and the direct path with the slots switched off."""
+    try:
+        for threads, panel_mib, (m, n) in ((0, 256, (1500, 1450)), (1, 256, (3100, 3000)),
+                                           (5, 32, (5300, 5200)), (12, 16, (2048, 4096)),
+                                           (3, 256, (5300, 5200))):
+            _native.set_tuning(host_bounce=1, host_threads=threads, host_panel_mib=panel_mib)
+            ext = {"M": m, "N": n}
+            for name in ("gemver", "bicgk", "gesummv"):
+                g = bto.load_graph(name)
+                inputs = bto.gen_inputs(g, ext, seed=n)
+                want = oracle.oracle_run(name, inputs, ext, threads=8)
+                assert_matches(name, run_host(name, inputs, ext), want, ext, f"bounce, {threads} threads")
+        _native.set_tuning(host_bounce=0)
+        ext = {"M": 3100, "N": 3000}
+        g = bto.load_graph("gemver")
+        inputs = bto.gen_inputs(g, ext, seed=2)
+        assert_matches("gemver", run_host("gemver", inputs, ext),
+                       oracle.oracle_run("gemver", inputs, ext, threads=8), ext, "no bounce")
+    finally:
+        _native.set_tuning(host_bounce=1, host_threads=0, host_panel_mib=256)
+
+
 def test_reference_style_ctypes_binding(bto_lib, oracle):
     """Bind the library the way the reference's loader does (runtime.py:99-150):
     raw CDLL, symbol by kernel name, POINTER(c_double) numpy buffers, c_double
