@@ -80,6 +80,9 @@ __device__ __forceinline__ double ld_cg(const double *p)
 // its predecessor in the stream is still running and waits here, before it
 // touches memory, until that grid has completed and flushed; the launch latency
 // hides under the predecessor's tail.  A no-op for a normally launched kernel.
+// (An explicit griddepcontrol.launch_dependents right after the wait was measured:
+// no gain at any size, profiles/r01/midsize_probe.md -- the implicit trigger at
+// grid completion already hides the launch.)
 __device__ __forceinline__ void wait_for_producer_grid()
 {
     asm volatile("griddepcontrol.wait;" ::: "memory");

@@ -143,10 +143,15 @@ int plan_mv(DeviceCtx &c, long M, long N, bool aligned, MvPlan *p)
     long per_sm = g_tuning.grid_per_sm > 0 ? g_tuning.grid_per_sm : dflt.grid_per_sm;
     if (per_sm <= 0) per_sm = occ;
     long grid = (long)c.sm_count * per_sm;
-    // small matrices: at least 4 units per CTA, so that few CTAs share a strip and
-    // the join (one partial per CTA and strip) stays short
-    const long by_work = (p->total_units + 3) / 4;
-    if (grid > by_work) grid = by_work;
+    // small matrices: about 3 units or more per CTA (the prologue and the partial a CTA
+    // writes per strip are fixed costs), in whole multiples of the SM count so that every
+    // SM carries the same number of CTAs; below one CTA per SM, 2 units per CTA
+    const long per_cta = 3;
+    if (grid * per_cta > p->total_units) {
+        const long waves = p->total_units / (per_cta * c.sm_count);
+        grid = waves >= 1 ? waves * c.sm_count : (p->total_units + 1) / 2;
+        if (grid > c.sm_count && waves < 1) grid = c.sm_count;
+    }
     if (grid < 1) grid = 1;
     p->grid = grid;
     long slots = 1;
@@ -197,7 +202,7 @@ int launch_join(DeviceCtx &c, FinArgs f, cudaStream_t stream)
         return launch_dependent(join_exchange_kernel, (unsigned)(kExchCtas + rb), e, stream,
                                 "join_exchange_kernel");
     }
-    const long cb = f.cmode != kColNone ? (f.N + kThreads - 1) / kThreads : 0;
+    const long cb = f.cmode != kColNone ? (f.N + kJoinCols - 1) / kJoinCols : 0;
     f.col_blocks = (int)cb;
     return launch_dependent(finalize_kernel, (unsigned)(cb + rb), f, stream, "finalize_kernel");
 }

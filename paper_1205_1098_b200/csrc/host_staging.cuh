@@ -420,7 +420,7 @@ int join_partials(const double *parts, long count, long n, int cmode, double sca
     f.total_units = count;
     f.grid = count;
     f.rmode = kRowNone;
-    f.col_blocks = (int)((n + kThreads - 1) / kThreads);
+    f.col_blocks = (int)((n + kJoinCols - 1) / kJoinCols);
     return launch_dependent(finalize_kernel, (unsigned)f.col_blocks, f, st, "finalize_kernel");
 }
 

@@ -309,6 +309,8 @@ struct FinArgs {
     int col_blocks;           // CTAs [0, col_blocks) do columns, the rest rows
 };
 
+constexpr int kJoinCols = 32;  // columns per column CTA of finalize_kernel
+
 // Sum of `count` partials `stride` apart in a FIXED order that exposes 8
 // independent load/add chains (the partials sit in L2; a single dependent chain
 // would pay the L2 latency `count` times): lane k takes partials k, k+8, ..;
@@ -347,6 +349,35 @@ __device__ __forceinline__ double column_epilogue(const FinArgs &f, long j, doub
     return s;
 }
 
+// The same join done by a whole CTA for kJoinCols adjacent columns: lane = column,
+// warp w sums the w-th eighth of the partials (strided_sum order inside), the eight
+// warp sums are added pairwise by warp 0.  A fixed order again, but the dependent
+// L2 round trips per thread drop from count/8 to count/64 -- what a mid-size call
+// (n ~ 2-8 K, 100+ partials per column, a 20 us tile kernel) spends its time on.
+__device__ __forceinline__ void join_columns_cta(const FinArgs &f, long j0)
+{
+    __shared__ double warp_part[kWarps][kJoinCols];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const long j = j0 + lane;
+    if (j < f.N) {
+        const long strip = j / f.strip_width;
+        const long first = split_owner(f.total_units, f.grid, strip * f.units_per_strip);
+        const long last = split_owner(f.total_units, f.grid, (strip + 1) * f.units_per_strip - 1);
+        const long count = last - first + 1;
+        const long k0 = (count * warp) / kWarps, k1 = (count * (warp + 1)) / kWarps;
+        warp_part[warp][lane] = strided_sum(f.colpart + j + k0 * f.N, k1 - k0, f.N);
+    }
+    __syncthreads();
+    if (warp == 0 && j < f.N) {
+        static_assert(kWarps == 8, "pairwise tree below is written for 8 warps");
+        const double s = ((warp_part[0][lane] + warp_part[1][lane]) +
+                          (warp_part[2][lane] + warp_part[3][lane])) +
+                         ((warp_part[4][lane] + warp_part[5][lane]) +
+                          (warp_part[6][lane] + warp_part[7][lane]));
+        f.colout[j] = column_epilogue(f, j, s);
+    }
+}
+
 // join + epilogue of row i
 __device__ __forceinline__ void finalize_row(const FinArgs &f, long i)
 {
@@ -367,8 +398,7 @@ finalize_kernel(const FinArgs f)
 {
     wait_for_producer_grid();
     if ((int)blockIdx.x < f.col_blocks) {
-        const long j = (long)blockIdx.x * kThreads + threadIdx.x;
-        if (j < f.N) f.colout[j] = column_epilogue(f, j, join_column(f, j));
+        join_columns_cta(f, (long)blockIdx.x * kJoinCols);
     } else {
         const long i = (long)(blockIdx.x - f.col_blocks) * kThreads + threadIdx.x;
         if (i < f.M) finalize_row(f, i);
