@@ -46,7 +46,7 @@ from pathlib import Path
 from .runtime import GeneratedKernel, ToolchainError
 
 __all__ = ["ir_from_matfuse", "emit_cuda", "NvccToolchain", "run_emitted", "DEFAULT_BLOCKS",
-           "measure_empirical_ir", "OrganismTimer", "EmitModel", "estimate_cost_ir",
+           "EMIT_VARIANTS", "time_emitted", "measure_empirical_ir", "OrganismTimer", "EmitModel", "estimate_cost_ir",
            "AnalyticOrganismCost"]
 
 DEFAULT_BLOCKS = 592          # 4 CTAs per SM on a 148-SM part
@@ -102,7 +102,7 @@ class _Writer:
         self.lines.append("    " * self.depth + text if text else "")
 
     def open(self, text: str):
-        self.put(text + " {")
+        self.put(text + " {" if text else "{")
         self.depth += 1
 
     def close(self, suffix: str = ""):
@@ -110,9 +110,25 @@ class _Writer:
         self.put("}" + suffix)
 
 
-_PRELUDE = r'''#include <cuda_runtime.h>
+_PRELUDE = r"""#include <cuda_runtime.h>
 
 namespace {
+// Batched loads of read-only operands.  `asm volatile` keeps them in program order ahead of
+// the arithmetic (left to itself the compiler sinks each load to its use and the thread has
+// one or two requests in flight instead of a whole batch).  Streamed-once data bypasses L1.
+__device__ __forceinline__ double ld_stream(const double *p)
+{
+    double v;
+    asm volatile("ld.global.nc.L1::no_allocate.f64 %0, [%1];" : "=d"(v) : "l"(p));
+    return v;
+}
+__device__ __forceinline__ double ld_keep(const double *p)
+{
+    double v;
+    asm volatile("ld.global.nc.f64 %0, [%1];" : "=d"(v) : "l"(p));
+    return v;
+}
+
 // fixed-order CTA reduction, result broadcast to every thread
 __device__ __forceinline__ double cta_allreduce(double v, double *scratch)
 {
@@ -126,16 +142,52 @@ __device__ __forceinline__ double cta_allreduce(double v, double *scratch)
     for (int w = 1; w < nwarps; ++w) total += scratch[w];
     return total;
 }
+
+// the same for R values at once (R rows of an unrolled-and-jammed loop): one pair of
+// barriers instead of R, every value summed in exactly the order cta_allreduce uses
+template <int R>
+__device__ __forceinline__ void cta_allreduce_n(double (&v)[R], double *scratch)
+{
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = (blockDim.x + 31) >> 5;
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+#pragma unroll
+        for (int off = 16; off >= 1; off >>= 1) v[r] += __shfl_xor_sync(0xffffffffu, v[r], off);
+    }
+    __syncthreads();
+    if (lane == 0) {
+#pragma unroll
+        for (int r = 0; r < R; ++r) scratch[warp * R + r] = v[r];
+    }
+    __syncthreads();
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+        double total = scratch[r];
+        for (int w = 1; w < nwarps; ++w) total += scratch[w * R + r];
+        v[r] = total;
+    }
+}
 }  // namespace
-'''
+"""
+
+JAM = 4                       # rows of an outer loop processed together (unroll-and-jam)
+# Launch-shape variants an empirical timer may try per organism (B200 sweep at n = 8192,
+# profiles/r01/emit_sweep.md): the first is the default of emit_cuda.
+EMIT_VARIANTS = ({"jam": 4, "unroll": 4, "minb": 2}, {"jam": 2, "unroll": 4, "minb": 2},
+                 {"jam": 8, "unroll": 2, "minb": 2})
+SMEM_ACC_BYTES = 192 * 1024   # per-CTA budget for block partials promoted to shared memory
+JOIN_COLS = 32                # columns per CTA of a join kernel
 
 
 class _Emitter:
-    def __init__(self, ir: dict, blocks: int):
+    def __init__(self, ir: dict, blocks: int, optimize: bool = True, jam: int = JAM,
+                 unroll: int = 4, threads: int = CTA_THREADS, minb: int = 2):
+        self.jam, self.unroll, self.threads, self.minb = int(jam), int(unroll), int(threads), int(minb)
         self.ir = ir
         self.st = ir["storage"]
         self.ops = ir["ops"]
         self.blocks = blocks
+        self.optimize = optimize
         self.w = _Writer()
         self.scalar_names = {}
         for name, s in self.st.items():
@@ -145,6 +197,13 @@ class _Emitter:
                     local += "_"
                 self.scalar_names[name] = local
         self.acc_counter = 0
+        # per launch: access table, whether every barrier of the plain scheme is kept,
+        # and the block partials that live in shared memory
+        self.access: dict = {}
+        self.conservative = True
+        self.promoted: dict = {}
+        self.preloaded: dict = {}      # operand -> register holding it (inside a load/compute batch)
+        self.cur_threads = self.threads
 
     # -- names and references (cemit.py:54-110) ----------------------------------
     def index(self, s: dict, block: str | None = None) -> str:
@@ -162,7 +221,14 @@ class _Emitter:
         size = " * ".join(exts) if exts else "1"
         return block if core is None else f"{block} * ({size}) + {core}"
 
+    def partial_ref(self, name: str, block: str | None) -> str:
+        if name in self.promoted:
+            return f"{name}_l[{self.st[name]['labels'][0]}]"
+        return f"{name}[{self.index(self.st[name], block)}]"
+
     def ref(self, name: str, block: str | None = None) -> str:
+        if name in self.preloaded:
+            return self.preloaded[name]
         s = self.st[name]
         if s["cls"] == "contracted":
             return self.scalar_names[name]
@@ -171,7 +237,7 @@ class _Emitter:
                 return name                       # by-value kernel parameter
             return f"{name}[0]"                   # scalar output / scalar temp in device memory
         if s["cls"] == "partial":
-            return f"{name}[{self.index(s, block)}]"
+            return self.partial_ref(name, block)
         return f"{name}[{self.index(s)}]"
 
     def partial_for(self, result: str) -> str | None:
@@ -180,13 +246,25 @@ class _Emitter:
                 return name
         return None
 
-    def target(self, op: dict, block: str | None, in_region: bool) -> tuple[str, str]:
-        """(C lvalue, storage name) of the op's destination."""
+    def target_name(self, op: dict, in_region: bool) -> str:
         if in_region:
             p = self.partial_for(op["result"])
             if p is not None:
-                return f"{p}[{self.index(self.st[p], block)}]", p
-        return self.ref(op["result"]), op["result"]
+                return p
+        return op["result"]
+
+    def target(self, op: dict, block: str | None, in_region: bool) -> tuple[str, str]:
+        """(C lvalue, storage name) of the op's destination."""
+        name = self.target_name(op, in_region)
+        if self.st[name]["cls"] == "partial":
+            return self.partial_ref(name, block), name
+        return self.ref(name), name
+
+    def init_lvalue(self, name: str, block: str | None) -> str:
+        s = self.st[name]
+        if s["cls"] == "contracted":
+            return self.scalar_names[name]
+        return self.partial_ref(name, block) if s["cls"] == "partial" else self.ref(name)
 
     def expr(self, op: dict) -> str:
         a = [self.ref(n) for n in op["operands"]]
@@ -217,18 +295,112 @@ class _Emitter:
         s = self.st[storage_name]
         return s["cls"] != "contracted" and axis in s["labels"]
 
-    def emit_uniform_stmt(self, stmt: dict, block: str | None, in_region: bool):
+    # -- who touches what, and from which threads ---------------------------------------
+    # Context of an access: "u0" a uniform statement with a memory target (thread 0 only),
+    # "u" a uniform statement executed by every thread, ("l", axis, sliced) a strided loop
+    # where thread k owns the elements lo + k, lo + k + blockDim.x, ...
+    def analyse(self, items: list, in_region: bool) -> dict:
+        table: dict = {}
+
+        def note(name, ctx, mode):
+            if self.st[name]["cls"] != "contracted":
+                table.setdefault(name, []).append((ctx, mode))
+
+        def stmt(it, lane):
+            if it["role"] == "init":
+                name = it["target"]
+                if lane is None:
+                    note(name, "u0", "w")
+                else:
+                    note(name, lane if self.indexed_by(name, lane[1]) else "u", "w")
+                return
+            op = self.ops[str(it["op"])]
+            tname = self.target_name(op, in_region)
+            contracted = self.st[tname]["cls"] == "contracted"
+            if lane is None:
+                ctx = "u" if contracted else "u0"
+                for n in op["operands"]:
+                    note(n, ctx, "r")
+                note(tname, ctx, "w")
+                return
+            for n in op["operands"]:
+                note(n, lane if self.indexed_by(n, lane[1]) else "u", "r")
+            if op["reduction"] and not self.indexed_by(tname, lane[1]):
+                note(tname, "u0", "w")            # accumulator: thread 0 adds the CTA sum
+            else:
+                ctx = lane if self.indexed_by(tname, lane[1]) else "u"
+                note(tname, ctx, "w")
+                if op["reduction"]:
+                    note(tname, ctx, "r")
+
+        def walk(items, lane):
+            for it in items:
+                if it["t"] == "stmt":
+                    stmt(it, lane)
+                elif it["t"] == "loop":
+                    walk(it["body"], ("l", it["axis"], bool(it["sliced"])) if self.is_innermost(it) else lane)
+
+        walk(items, None)
+        return table
+
+    def begin_launch(self, items: list, in_region: bool):
+        """Set up barrier policy and shared-memory promotion for one kernel."""
+        self.cur_threads = self.threads if in_region else SERIAL_THREADS
+        self.access = self.analyse(items, in_region)
+        self.promoted = {}
+        if not self.optimize:
+            self.conservative = True
+            return
+        # a value written by thread 0 and read by other threads needs the full barrier
+        # scheme (write -> barrier -> reads -> barrier -> next write)
+        self.conservative = any(
+            any(c == "u0" and m == "w" for c, m in acc) and any(c != "u0" and m == "r" for c, m in acc)
+            for acc in self.access.values())
+        if in_region:
+            for name, acc in self.access.items():
+                s = self.st[name]
+                if s["cls"] == "partial" and s["order"] == "vec" and \
+                        all(c == ("l", s["labels"][0], False) for c, _ in acc):
+                    self.promoted[name] = s["extents"][0]
+
+    def lane_private(self, name: str, key: tuple) -> bool:
+        return all(c == key for c, _ in self.access.get(name, ()))
+
+    def written(self, name: str) -> bool:
+        return any(m == "w" for _, m in self.access.get(name, ()))
+
+    def loop_needs_barrier(self, loop: dict, in_region: bool) -> bool:
+        """After a strided loop: only when something it touches element-wise is written in
+        this launch and also touched with a different thread mapping."""
+        if self.conservative:
+            return True
+        key = ("l", loop["axis"], bool(loop["sliced"]))
+        names = set()
+        for it in loop["body"]:
+            if it["role"] == "init":
+                names.add(it["target"])
+                continue
+            op = self.ops[str(it["op"])]
+            names.update(op["operands"])
+            tname = self.target_name(op, in_region)
+            if not (op["reduction"] and not self.indexed_by(tname, loop["axis"])):
+                names.add(tname)
+        return any(self.st[n]["cls"] != "contracted" and self.written(n) and not self.lane_private(n, key)
+                   for n in names)
+
+    # -- plain emission ------------------------------------------------------------------
+    def emit_uniform_stmt(self, stmt: dict, block: str | None, in_region: bool, barrier: bool = True):
         """A statement outside any strided loop: same value in every thread."""
         w = self.w
+        barrier = barrier and self.conservative
         if stmt["role"] == "init":
             name = stmt["target"]
-            s = self.st[name]
-            if s["cls"] == "contracted":
+            if self.st[name]["cls"] == "contracted":
                 w.put(f"{self.scalar_names[name]} = 0.0;")
                 return
-            lhs = f"{name}[{self.index(s, block)}]" if s["cls"] == "partial" else self.ref(name)
-            w.put(f"if (threadIdx.x == 0) {lhs} = 0.0;")
-            w.put("__syncthreads();")
+            w.put(f"if (threadIdx.x == 0) {self.init_lvalue(name, block)} = 0.0;")
+            if barrier:
+                w.put("__syncthreads();")
             return
         op = self.ops[str(stmt["op"])]
         lhs, sname = self.target(op, block, in_region)
@@ -237,42 +409,40 @@ class _Emitter:
             w.put(f"{lhs} {assign} {self.expr(op)};")
         else:
             w.put(f"if (threadIdx.x == 0) {lhs} {assign} {self.expr(op)};")
-            w.put("__syncthreads();")
+            if barrier:
+                w.put("__syncthreads();")
 
-    def emit_lane_loop(self, loop: dict, block: str | None, in_region: bool):
-        """The innermost loop of a nest, strided across the CTA's threads."""
-        w = self.w
-        v = loop["axis"]
-        lo, hi = (f"{v}_lo", f"{v}_hi") if loop["sliced"] else ("0", loop["extent"])
-        # reductions whose destination does not move with this loop -> thread accumulators
+    def lane_accumulators(self, loop: dict, block: str | None, in_region: bool) -> dict:
+        """Reductions whose destination does not move with the strided loop."""
         accs = {}
         for it in loop["body"]:
             if it["t"] == "stmt" and it["role"] == "compute":
                 op = self.ops[str(it["op"])]
                 if op["reduction"]:
                     lhs, sname = self.target(op, block, in_region)
-                    if not self.indexed_by(sname, v):
+                    if not self.indexed_by(sname, loop["axis"]):
                         self.acc_counter += 1
                         accs[it["op"]] = (f"lacc{self.acc_counter}", lhs, sname)
-        for acc, _, _ in accs.values():
-            w.put(f"double {acc} = 0.0;")
-        # loops that only load, compute and store to their own elements are unrolled so
-        # several loads are in flight per thread; read-modify-write loops are not (measured:
-        # unrolling those serialises on the memory dependences and is ~10x slower)
-        rmw = any(it["role"] == "compute" and self.ops[str(it["op"])]["reduction"]
-                  and it["op"] not in accs for it in loop["body"])
-        if not rmw:
-            w.put("#pragma unroll 4")
-        w.open(f"for (long {v} = {lo} + threadIdx.x; {v} < {hi}; {v} += blockDim.x)")
+        return accs
+
+    def lane_header(self, loop: dict) -> str:
+        v = loop["axis"]
+        lo, hi = (f"{v}_lo", f"{v}_hi") if loop["sliced"] else ("0", loop["extent"])
+        return f"for (long {v} = {lo} + threadIdx.x; {v} < {hi}; {v} += blockDim.x)"
+
+    def is_global_rmw(self, loop: dict, accs: dict, in_region: bool) -> bool:
+        for it in loop["body"]:
+            if it["role"] == "compute" and it["op"] not in accs:
+                op = self.ops[str(it["op"])]
+                if op["reduction"] and self.target_name(op, in_region) not in self.promoted:
+                    return True
+        return False
+
+    def emit_lane_body(self, loop: dict, accs: dict, block: str | None, in_region: bool):
+        w = self.w
         for it in loop["body"]:
             if it["role"] == "init":
-                name = it["target"]
-                s = self.st[name]
-                if s["cls"] == "contracted":
-                    w.put(f"{self.scalar_names[name]} = 0.0;")
-                else:
-                    lhs = f"{name}[{self.index(s, block)}]" if s["cls"] == "partial" else self.ref(name)
-                    w.put(f"{lhs} = 0.0;")
+                w.put(f"{self.init_lvalue(it['target'], block)} = 0.0;")
                 continue
             op = self.ops[str(it["op"])]
             if it["op"] in accs:
@@ -280,6 +450,23 @@ class _Emitter:
                 continue
             lhs, _ = self.target(op, block, in_region)
             w.put(f"{lhs} {'+=' if op['reduction'] else '='} {self.expr(op)};")
+
+    def emit_lane_loop(self, loop: dict, block: str | None, in_region: bool):
+        """The innermost loop of a nest, strided across the CTA's threads."""
+        if self.optimize:
+            self.emit_batched_lane(loop, block, in_region, None)
+            return
+        w = self.w
+        accs = self.lane_accumulators(loop, block, in_region)
+        for acc, _, _ in accs.values():
+            w.put(f"double {acc} = 0.0;")
+        # loops that only load, compute and store to their own elements are unrolled so
+        # several loads are in flight per thread; loops that read-modify-write global memory
+        # are not (measured: unrolling those serialises on the memory dependences, ~10x slower)
+        if not self.is_global_rmw(loop, accs, in_region):
+            w.put("#pragma unroll 4")
+        w.open(self.lane_header(loop))
+        self.emit_lane_body(loop, accs, block, in_region)
         w.close()
         for acc, lhs, sname in accs.values():
             w.put(f"{acc} = cta_allreduce({acc}, scratch_);")
@@ -287,7 +474,200 @@ class _Emitter:
                 w.put(f"{lhs} += {acc};")
             else:
                 w.put(f"if (threadIdx.x == 0) {lhs} += {acc};")
-        w.put("__syncthreads();")
+        if self.loop_needs_barrier(loop, in_region):
+            w.put("__syncthreads();")
+
+    def streamed_operands(self, loop: dict) -> list:
+        """Operands of the strided loop that move with it and are read-only in this launch:
+        these are loaded in batches ahead of the arithmetic."""
+        names = []
+        for it in loop["body"]:
+            if it["role"] != "compute":
+                continue
+            for n in self.ops[str(it["op"])]["operands"]:
+                if n not in names and self.indexed_by(n, loop["axis"]) and not self.written(n):
+                    names.append(n)
+        return names
+
+    def load_of(self, name: str, loop: dict) -> str:
+        """Batched load of a read-only operand: 2-D operands pass once (no L1 allocation),
+        vectors are reused by the next rows and stay cached."""
+        once = len(self.st[name]["labels"]) == 2
+        return f"{'ld_stream' if once else 'ld_keep'}(&{self.ref(name)})"
+
+    def emit_batched_lane(self, loop: dict, block: str | None, in_region: bool, rows):
+        """Strided loop as explicit load / compute batches.  `rows` = (axis, scalars) when
+        the surrounding loop is jammed: every statement then runs for `jam` rows.
+
+        Per thread and batch: U elements of the strided axis (stride = CTA size, a literal, so
+        the compiler sees that they are distinct) times R rows; all loads of the read-only
+        operands are issued first, then the statements run in the reference's order (row by
+        row for one element, so an element's `+=` chain keeps its ascending-row order)."""
+        w = self.w
+        v, T = loop["axis"], self.cur_threads
+        lo, hi = (f"{v}_lo", f"{v}_hi") if loop["sliced"] else ("0", loop["extent"])
+        accs = self.lane_accumulators(loop, block, in_region)
+        R = self.jam if rows else 1
+        U = 1 if self.is_global_rmw(loop, accs, in_region) else self.unroll
+        a, scalars = rows if rows else (None, [])
+        for acc, _, _ in accs.values():
+            w.put(f"double {acc}_a[{R}] = {{}};" if rows else f"double {acc} = 0.0;")
+        streamed = self.streamed_operands(loop)
+        per_row = {n: bool(rows) and a in self.st[n]["labels"] for n in streamed}
+
+        def open_rows(aliases=True):
+            if not rows:
+                return
+            w.put("#pragma unroll")
+            w.open(f"for (int r_ = 0; r_ < {R}; ++r_)")
+            w.put(f"const long {a} = {a}_b_ + r_; (void){a};")
+            if aliases:
+                for name in scalars:
+                    local = self.scalar_names[name]
+                    w.put(f"double &{local} = {local}_a[r_]; (void){local};")
+                for acc, _, _ in accs.values():
+                    w.put(f"double &{acc} = {acc}_a[r_];")
+
+        def close_rows():
+            if rows:
+                w.close()
+
+        w.open("")
+        w.put(f"long {v}_b_ = {lo} + threadIdx.x;")
+        if U > 1 or streamed:
+            w.open(f"for (; {v}_b_ + {(U - 1) * T} < {hi}; {v}_b_ += {U * T})")
+            for n in streamed:
+                w.put(f"double {n}_v[{R}][{U}];" if per_row[n] else f"double {n}_v[{U}];")
+            if streamed:
+                w.put("#pragma unroll")
+                w.open(f"for (int u_ = 0; u_ < {U}; ++u_)")
+                w.put(f"const long {v} = {v}_b_ + u_ * {T};")
+                for n in streamed:
+                    if not per_row[n]:
+                        w.put(f"{n}_v[u_] = {self.load_of(n, loop)};")
+                if any(per_row.values()):
+                    open_rows(aliases=False)
+                    for n in streamed:
+                        if per_row[n]:
+                            w.put(f"{n}_v[r_][u_] = {self.load_of(n, loop)};")
+                    close_rows()
+                w.close()
+            w.put("#pragma unroll")
+            w.open(f"for (int u_ = 0; u_ < {U}; ++u_)")
+            w.put(f"const long {v} = {v}_b_ + u_ * {T}; (void){v};")
+            open_rows()
+            self.preloaded = {n: (f"{n}_v[r_][u_]" if per_row[n] else f"{n}_v[u_]") for n in streamed}
+            self.emit_lane_body(loop, accs, block, in_region)
+            self.preloaded = {}
+            close_rows()
+            w.close()
+            w.close()
+        w.open(f"for (; {v}_b_ < {hi}; {v}_b_ += {T})")           # what is left of the range
+        w.put(f"const long {v} = {v}_b_;")
+        open_rows()
+        self.emit_lane_body(loop, accs, block, in_region)
+        close_rows()
+        w.close()
+        w.close()
+        for acc, lhs, sname in accs.values():
+            if rows:
+                w.put(f"cta_allreduce_n<{R}>({acc}_a, scratch_);")
+                open_rows()
+            else:
+                w.put(f"{acc} = cta_allreduce({acc}, scratch_);")
+            if self.st[sname]["cls"] == "contracted":
+                w.put(f"{lhs} += {acc};")
+            else:
+                w.put(f"if (threadIdx.x == 0) {lhs} += {acc};")
+            close_rows()
+        if self.loop_needs_barrier(loop, in_region):
+            w.put("__syncthreads();")
+
+    # -- unroll-and-jam of a loop around strided loops ----------------------------------------
+    def jam_legal(self, loop: dict, in_region: bool) -> bool:
+        """Iterations of `loop` may be processed JAM at a time when they only meet in
+        accumulations: everything written is either private to the iteration (indexed by the
+        loop's axis, or a contracted scalar labelled by it) or the target of exactly one
+        `+=` statement that nothing else in the body reads."""
+        if not self.optimize or self.conservative:
+            return False
+        a = loop["axis"]
+        stmts = []
+        lanes = 0
+        for it in loop["body"]:
+            if it["t"] == "stmt":
+                stmts.append(it)
+            elif it["t"] == "loop" and self.is_innermost(it) and it["axis"] != a:
+                lanes += 1
+                stmts.extend(it["body"])
+            else:
+                return False
+        if lanes == 0:
+            return False
+        reads, shared_writes = set(), {}
+        for it in stmts:
+            if it["role"] == "init":
+                if a not in self.st[it["target"]]["labels"]:
+                    return False
+                continue
+            op = self.ops[str(it["op"])]
+            reads.update(op["operands"])
+            tname = self.target_name(op, in_region)
+            if a in self.st[tname]["labels"]:
+                continue
+            if self.st[tname]["cls"] == "contracted" or not op["reduction"]:
+                return False
+            shared_writes[tname] = shared_writes.get(tname, 0) + 1
+        return all(n == 1 for n in shared_writes.values()) and not (reads & set(shared_writes))
+
+    def jam_written_scalars(self, loop: dict) -> list:
+        names = []
+        def visit(items):
+            for it in items:
+                if it["t"] == "loop":
+                    visit(it["body"])
+                    continue
+                name = it["target"] if it["role"] == "init" else self.ops[str(it["op"])]["result"]
+                if self.st[name]["cls"] == "contracted" and name not in names:
+                    names.append(name)
+        visit(loop["body"])
+        return names
+
+    def emit_jammed_loop(self, loop: dict, block: str | None, in_region: bool):
+        w = self.w
+        a = loop["axis"]
+        lo, hi = (f"{a}_lo", f"{a}_hi") if loop["sliced"] else ("0", loop["extent"])
+        scalars = self.jam_written_scalars(loop)
+        w.open("")                               # scope: the same axis may head several nests
+        w.put(f"long {a}_b_ = {lo};")
+        w.open(f"for (; {a}_b_ + {self.jam} <= {hi}; {a}_b_ += {self.jam})")
+        for name in scalars:
+            w.put(f"double {self.scalar_names[name]}_a[{self.jam}];")
+
+        def rows(extra_alias=()):
+            """open the per-row loop: row index and the row's private scalars under their usual names"""
+            w.put("#pragma unroll")
+            w.open(f"for (int r_ = 0; r_ < {self.jam}; ++r_)")
+            w.put(f"const long {a} = {a}_b_ + r_; (void){a};")
+            for name in scalars:
+                local = self.scalar_names[name]
+                w.put(f"double &{local} = {local}_a[r_]; (void){local};")
+            for acc in extra_alias:
+                w.put(f"double &{acc} = {acc}_a[r_];")
+
+        for it in loop["body"]:
+            if it["t"] == "stmt":
+                rows()
+                self.emit_uniform_stmt(it, block, in_region, barrier=False)
+                w.close()
+            else:
+                self.emit_batched_lane(it, block, in_region, (a, scalars))
+        w.close()
+        # remaining rows one at a time
+        w.open(f"for (long {a} = {a}_b_; {a} < {hi}; ++{a})")
+        self.emit_items(loop["body"], block, in_region)
+        w.close()
+        w.close()
 
     def emit_items(self, items: list, block: str | None, in_region: bool):
         for it in items:
@@ -296,6 +676,8 @@ class _Emitter:
             elif it["t"] == "loop":
                 if self.is_innermost(it):
                     self.emit_lane_loop(it, block, in_region)
+                elif self.jam_legal(it, in_region):
+                    self.emit_jammed_loop(it, block, in_region)
                 else:
                     v = it["axis"]
                     rng = (f"long {v} = {v}_lo; {v} < {v}_hi; ++{v}" if it["sliced"]
@@ -320,6 +702,50 @@ class _Emitter:
         out += [(f"long {e}", e) for e in self.ir["extents"]]
         return out
 
+    def emit_join(self, jname: str, decl: str, pname: str, result: str):
+        """Ascending join of the block partials (cemit.py:204-222) as its own kernel."""
+        w = self.w
+        ps = self.st[pname]
+        if not ps["extents"]:
+            # scalar: thread k adds blocks k, k + 256, ..; then the fixed-order CTA reduction
+            w.open(f"__global__ void __launch_bounds__(256) {jname}({decl}, long nblocks_)")
+            w.put("__shared__ double scratch_[32];")
+            w.put("double acc = 0.0;")
+            w.put(f"for (long b = threadIdx.x; b < nblocks_; b += 256) acc += {pname}[b];")
+            w.put("acc = cta_allreduce(acc, scratch_);")
+            w.put(f"if (threadIdx.x == 0) {self.ref(result)} = acc;")
+            w.close()
+            w.put()
+            return "1"
+        lab, e0 = ps["labels"][0], ps["extents"][0]
+        w.open(f"__global__ void __launch_bounds__(256) {jname}({decl}, long nblocks_)")
+        # a CTA joins JOIN_COLS adjacent elements: lane = element, warp w adds the w-th
+        # eighth of the blocks in 8 independent chains (the partials sit in L2; one dependent
+        # chain per element would pay its latency nblocks times); fixed order throughout
+        w.put(f"__shared__ double part_[8][{JOIN_COLS}];")
+        w.put("const int lane_ = threadIdx.x & 31, warp_ = threadIdx.x >> 5;")
+        w.put(f"const long {lab} = (long)blockIdx.x * {JOIN_COLS} + lane_;")
+        w.open(f"if ({lab} < {e0})")
+        w.put("const long b0_ = (nblocks_ * warp_) / 8, b1_ = (nblocks_ * (warp_ + 1)) / 8;")
+        w.put("double a_[8] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};")
+        w.put("long b = b0_;")
+        w.open("for (; b + 8 <= b1_; b += 8)")
+        w.put("#pragma unroll")
+        w.put(f"for (int u = 0; u < 8; ++u) a_[u] += {pname}[(b + u) * ({e0}) + {lab}];")
+        w.close()
+        w.put("#pragma unroll")
+        w.put(f"for (int u = 0; u < 8; ++u) if (b + u < b1_) a_[u] += {pname}[(b + u) * ({e0}) + {lab}];")
+        w.put("part_[warp_][lane_] = ((a_[0] + a_[1]) + (a_[2] + a_[3])) + ((a_[4] + a_[5]) + (a_[6] + a_[7]));")
+        w.close()
+        w.put("__syncthreads();")
+        w.open(f"if (warp_ == 0 && {lab} < {e0})")
+        w.put(f"{self.ref(result)} = ((part_[0][lane_] + part_[1][lane_]) + (part_[2][lane_] + part_[3][lane_])) + "
+              f"((part_[4][lane_] + part_[5][lane_]) + (part_[6][lane_] + part_[7][lane_]));")
+        w.close()
+        w.close()
+        w.put()
+        return f"(unsigned)(({e0} + {JOIN_COLS - 1}) / {JOIN_COLS})"
+
     def emit(self) -> str:
         ir, w = self.ir, self.w
         kname = ir["name"].lower()
@@ -332,11 +758,12 @@ class _Emitter:
         launches = []          # host-side launch statements
         regions = 0
         serial_group: list = []
+        uses_smem = False
 
         def scalars_decl():
             for local in self.scalar_names.values():
                 w.put(f"double {local} = 0.0;")
-            w.put("__shared__ double scratch_[32];")
+            w.put(f"__shared__ double scratch_[{32 * self.jam}];")
             w.put("(void)scratch_;")
 
         def flush_serial():
@@ -345,6 +772,7 @@ class _Emitter:
                 return
             fname = f"{kname}_serial{regions}"
             regions += 1
+            self.begin_launch(serial_group, False)
             w.open(f"__global__ void __launch_bounds__({SERIAL_THREADS}) {fname}({decl})")
             scalars_decl()
             self.emit_items(serial_group, None, False)
@@ -363,57 +791,66 @@ class _Emitter:
             fname = f"{kname}_region{regions}"
             nb = f"nb{regions}_"
             regions += 1
+            self.begin_launch(root["body"], True)
             # When the strided (innermost) loops run over the block's own slice, a
             # slice narrower than the CTA leaves threads idle: cap the block count
             # so every CTA gets at least a CTA-width of the axis (never below the
             # organism's own count).  Any count is legal for the block formula.
             if self.has_sliced_lane_loop(root["body"]):
-                launches.append(f"long {nb} = {root['extent']} / {CTA_THREADS}; "
+                launches.append(f"long {nb} = {root['extent']} / {self.threads}; "
                                 f"if ({nb} < {org_t}) {nb} = {org_t}; if ({nb} > {t}) {nb} = {t};")
             else:
                 launches.append(f"long {nb} = {t};")
             ax, ext = root["axis"], root["extent"]
-            w.open(f"__global__ void __launch_bounds__({CTA_THREADS}) {fname}({decl}, long nblocks_)")
+            smem_args = ""
+            if self.promoted:
+                # block partials indexed by the strided axis only: each thread owns its
+                # elements for the whole launch, so they accumulate in shared memory and
+                # reach the partial buffer once, at the end (when they fit; else in place)
+                uses_smem = True
+                total = " + ".join(f"(size_t){e}" for e in self.promoted.values())
+                launches.append(f"const size_t smb{regions}_ = sizeof(double) * ({total});")
+                launches.append(f"const int sm_ok{regions}_ = smb{regions}_ <= {SMEM_ACC_BYTES};")
+                launches.append(f"if (sm_ok{regions}_) {{ long fit_ = (long)sms_ * (long)((227 * 1024) / (smb{regions}_ + 2048)); "
+                                f"if (fit_ < {org_t}) fit_ = {org_t}; if ({nb} > fit_) {nb} = fit_; }}")
+                launches.append(f"static bool attr{regions}_ = false; if (!attr{regions}_) {{ cudaFuncSetAttribute({fname}, "
+                                f"cudaFuncAttributeMaxDynamicSharedMemorySize, {SMEM_ACC_BYTES}); attr{regions}_ = true; }}")
+                smem_args = f", sm_ok{regions}_"
+            # min-blocks in the launch bounds: without it ptxas aims for full occupancy, keeps the
+            # register count low and sinks every batched load down to its use
+            bounds = f"{self.threads}, {self.minb}" if self.optimize else f"{self.threads}"
+            w.open(f"__global__ void __launch_bounds__({bounds}) {fname}({decl}, long nblocks_"
+                   + (", int sm_ok_" if self.promoted else "") + ")")
             scalars_decl()
             w.put("const long p_ = blockIdx.x;")
             w.put(f"const long {ax}_lo = ({ext} * p_) / nblocks_;")
             w.put(f"const long {ax}_hi = ({ext} * (p_ + 1)) / nblocks_;")
             w.put(f"(void){ax}_lo; (void){ax}_hi;")
+            if self.promoted:
+                w.put("extern __shared__ double dyn_[];")
+                offset = "0"
+                for name, e in self.promoted.items():
+                    size = self.st[name]["extents"][0]
+                    w.put(f"double *{name}_l = sm_ok_ ? dyn_ + ({offset}) : {name} + p_ * ({size});")
+                    offset += f" + {e}"
             self.emit_items(root["body"], "p_", True)
+            if self.promoted:
+                w.open("if (sm_ok_)")
+                for name in self.promoted:
+                    s = self.st[name]
+                    lab, size = s["labels"][0], s["extents"][0]
+                    w.put(f"for (long {lab} = threadIdx.x; {lab} < {size}; {lab} += blockDim.x) "
+                          f"{name}[p_ * ({size}) + {lab}] = {name}_l[{lab}];")
+                w.close()
             w.close()
             w.put()
-            launches.append(f"{fname}<<<(unsigned){nb}, {CTA_THREADS}, 0, 0>>>({call}, {nb});")
+            dyn = f"sm_ok{regions}_ ? smb{regions}_ : 0" if self.promoted else "0"
+            launches.append(f"{fname}<<<(unsigned){nb}, {self.threads}, {dyn}, 0>>>({call}, {nb}{smem_args});")
+            self.promoted = {}
             for result in root["partials"]:
                 pname = self.partial_for(result)
-                ps = self.st[pname]
                 jname = f"{kname}_join{regions}_{result}"
-                w.open(f"__global__ void {jname}({decl}, long nblocks_)")
-                if not ps["extents"]:
-                    w.open("if (blockIdx.x == 0 && threadIdx.x == 0)")
-                    w.put(f"double acc = {pname}[0];")
-                    w.put(f"for (long b = 1; b < nblocks_; ++b) acc += {pname}[b];")
-                    w.put(f"{self.ref(result)} = acc;")
-                    w.close()
-                    grid = "1"
-                else:
-                    lab, e0 = ps["labels"][0], ps["extents"][0]
-                    w.put(f"const long {lab} = (long)blockIdx.x * blockDim.x + threadIdx.x;")
-                    w.open(f"if ({lab} < {e0})")
-                    # ascending blocks dealt to 8 independent chains (fixed order): the
-                    # partials sit in L2 and one dependent chain would pay its latency nblocks times
-                    w.put("double a_[8] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};")
-                    w.put("long b = 0;")
-                    w.open("for (; b + 8 <= nblocks_; b += 8)")
-                    w.put("#pragma unroll")
-                    w.put(f"for (int u = 0; u < 8; ++u) a_[u] += {pname}[(b + u) * ({e0}) + {lab}];")
-                    w.close()
-                    w.put("#pragma unroll")
-                    w.put(f"for (int u = 0; u < 8; ++u) if (b + u < nblocks_) a_[u] += {pname}[(b + u) * ({e0}) + {lab}];")
-                    w.put(f"{self.ref(result)} = ((a_[0] + a_[1]) + (a_[2] + a_[3])) + ((a_[4] + a_[5]) + (a_[6] + a_[7]));")
-                    w.close()
-                    grid = f"(unsigned)(({e0} + 255) / 256)"
-                w.close()
-                w.put()
+                grid = self.emit_join(jname, decl, pname, result)
                 launches.append(f"{jname}<<<{grid}, 256, 0, 0>>>({call}, {nb});")
         flush_serial()
 
@@ -425,6 +862,12 @@ class _Emitter:
             hparams.append(f"double *{name}")
         hparams += [f"long {e}" for e in ir["extents"]]
         w.open(f'extern "C" void {kname}({", ".join(hparams)})')
+        if uses_smem:
+            w.put("static int sms_ = 0;")
+            w.open("if (!sms_)")
+            w.put("int dev_ = 0; cudaGetDevice(&dev_);")
+            w.put("cudaDeviceGetAttribute(&sms_, cudaDevAttrMultiProcessorCount, dev_);")
+            w.close()
         temps = []
         for name, s in self.st.items():
             if s["cls"] == "temp":
@@ -462,10 +905,14 @@ class _Emitter:
         return "\n".join(w.lines) + "\n"
 
 
-def emit_cuda(ir: dict, blocks: int = DEFAULT_BLOCKS) -> GeneratedKernel:
+def emit_cuda(ir: dict, blocks: int = DEFAULT_BLOCKS, optimize: bool = True, **tune) -> GeneratedKernel:
     """Render a loop-IR snapshot as a standalone CUDA translation unit.
-    Deterministic: the same IR and `blocks` always yield byte-identical source."""
-    em = _Emitter(ir, int(blocks))
+    Deterministic: the same IR, `blocks` and `optimize` always yield byte-identical source.
+    `optimize=False` prints the plain mapping only (every barrier, no unroll-and-jam, block
+    partials accumulated in global memory).  `tune`: jam (rows per batch), unroll (of the
+    strided loop under a batch), threads (per CTA of a parallel region), minb (CTAs per SM the
+    register budget is sized for)."""
+    em = _Emitter(ir, int(blocks), bool(optimize), **tune)
     source = em.emit()
     params = []
     for name, kind in ir["inputs"]:
@@ -570,18 +1017,66 @@ def run_emitted(binary, kernel: GeneratedKernel, ir: dict, inputs: dict, extents
     return result
 
 
+def time_emitted(binary, kernel: GeneratedKernel, ir: dict, dev_inputs: dict, extents: dict,
+                 reps: int = 5) -> float:
+    """Best-of-`reps` seconds of the emitted entry point alone (its launches, joins,
+    temporaries and final sync) on device-resident operands, outputs preallocated."""
+    import math
+
+    import torch
+
+    lib = ctypes.CDLL(str(binary))
+    fn = getattr(lib, kernel.kernel_name)
+    fn.restype = None
+    st = ir["storage"]
+    args, keep = [], []
+    for name, kind in ir["inputs"]:
+        if kind == "scalar":
+            args.append(ctypes.c_double(float(dev_inputs[name])))
+            continue
+        t = dev_inputs[name]
+        if st[name]["order"] == "col":
+            t = t.t()
+        t = t.contiguous()
+        keep.append(t)
+        args.append(ctypes.c_void_p(t.data_ptr()))
+    for name, kind in ir["outputs"]:
+        size = 1
+        for e in st[name]["extents"]:
+            size *= int(extents[e])
+        buf = torch.empty((size,), dtype=torch.float64, device="cuda")
+        keep.append(buf)
+        args.append(ctypes.c_void_p(buf.data_ptr()))
+    args += [ctypes.c_long(int(extents[e])) for e in ir["extents"]]
+    torch.cuda.synchronize()
+    fn(*args)                                                      # warm-up
+    best = math.inf
+    for _ in range(reps):
+        start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        start.record()
+        fn(*args)
+        stop.record()
+        stop.synchronize()
+        best = min(best, start.elapsed_time(stop) * 1e-3)
+    if getattr(lib, kernel.kernel_name + "_last_cuda_error")():
+        raise ToolchainError("emitted kernel failed while being timed")
+    return best
+
+
 # ---------------------------------------------------------------------------
 # empirical fitness for organisms (cost.py:124-208 with a GPU back end)
 
 def measure_empirical_ir(ir: dict, graph, extents: dict, reps: int = 5,
                          validate_extents: dict | None = None, blocks: int = DEFAULT_BLOCKS,
                          toolchain: NvccToolchain | None = None, source_filter=None,
-                         tolerance: float = 1e-10):
+                         tolerance: float = 1e-10, optimize: bool = True, variants=None):
     """Emit, compile, validate, then time one lowered organism; +inf with the
     reference's diagnostics on any failure (cost.py:176-207).  `graph` is this
     package's TypedSpec of the same kernel; validation compares against the
     independent spec evaluator (cost.evaluate_spec).  `source_filter` is the
-    reference's fault-injection hook (cost.py:148,186)."""
+    reference's fault-injection hook (cost.py:148,186).  `variants`: launch-shape settings
+    (dicts of emit_cuda's tunables, e.g. EMIT_VARIANTS) to try after the default one has
+    validated; the best time is reported."""
     import math
 
     import torch
@@ -592,7 +1087,7 @@ def measure_empirical_ir(ir: dict, graph, extents: dict, reps: int = 5,
     def failure(kind: str, detail: str) -> CostReport:
         return CostReport(total=math.inf, source="empirical", diagnostic=f"{kind}: {detail}")
 
-    kernel = emit_cuda(ir, blocks=blocks)
+    kernel = emit_cuda(ir, blocks=blocks, optimize=optimize)
     source = source_filter(kernel.source) if source_filter is not None else kernel.source
     try:
         lib = (toolchain or NvccToolchain()).compile(source, workdir(), name="kernel", shared=True)
@@ -613,15 +1108,14 @@ def measure_empirical_ir(ir: dict, graph, extents: dict, reps: int = 5,
     try:
         inputs = gen_inputs(graph, extents, seed=7)
         dev = {k: (torch.from_numpy(v).cuda() if hasattr(v, "shape") else v) for k, v in inputs.items()}
-        run_emitted(lib, kernel, ir, dev, extents)                 # warm-up, untimed
-        best = math.inf
-        for _ in range(reps):
-            start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            start.record()
-            run_emitted(lib, kernel, ir, dev, extents)
-            stop.record()
-            stop.synchronize()
-            best = min(best, start.elapsed_time(stop) * 1e-3)
+        best = time_emitted(lib, kernel, ir, dev, extents, reps=reps)
+        for idx, tune in enumerate(variants or ()):
+            alt = emit_cuda(ir, blocks=blocks, optimize=optimize, **tune)
+            if alt.source == kernel.source:
+                continue
+            alt_lib = (toolchain or NvccToolchain()).compile(alt.source, workdir(), name=f"kernel_v{idx}",
+                                                             shared=True)
+            best = min(best, time_emitted(alt_lib, alt, ir, dev, extents, reps=reps))
     except Exception as exc:  # noqa: BLE001
         return failure("runtime-crash", repr(exc))
     return CostReport(total=best, source="empirical")
@@ -637,7 +1131,7 @@ class OrganismTimer:
 
     def __init__(self, ref_graph, extents: dict | None = None, reps: int = 5,
                  validate_extents: dict | None = None, blocks: int = DEFAULT_BLOCKS,
-                 source_filter=None):
+                 source_filter=None, optimize: bool = True, variants=None):
         from .runtime import _convert_expr
         from .spec import Decl, KernelSpec, infer_shapes
         spec = ref_graph.spec
@@ -650,16 +1144,18 @@ class OrganismTimer:
         self.extents = extents or {n: 1000 for n in ref_graph.extent_names}
         self.reps, self.validate_extents, self.blocks = reps, validate_extents, blocks
         self.source_filter = source_filter
+        self.optimize, self.variants = optimize, variants
 
     def key_salt(self) -> str:
-        return "empirical-cuda:" + ",".join(f"{k}={v}" for k, v in sorted(self.extents.items()))
+        return ("empirical-cuda:" if self.optimize else "empirical-cuda-plain:") + ",".join(f"{k}={v}" for k, v in sorted(self.extents.items()))
 
     def __call__(self, organism):
         from matfuse import contract_arrays, lower
         ir = ir_from_matfuse(contract_arrays(lower(organism, self.ref_graph)))
         return measure_empirical_ir(ir, self.graph, self.extents, self.reps,
                                     validate_extents=self.validate_extents, blocks=self.blocks,
-                                    source_filter=self.source_filter)
+                                    source_filter=self.source_filter, optimize=self.optimize,
+                                    variants=self.variants)
 
 
 # ---------------------------------------------------------------------------
@@ -669,15 +1165,20 @@ class OrganismTimer:
 @dataclass(frozen=True)
 class EmitModel:
     """Coefficients of `estimate_cost_ir`, fitted on the 360 timings of
-    profiles/r01/organism_times.json (120 organisms x n = 1024, 2048, 4096)."""
+    profiles/r01/organism_times.json (120 organisms x n = 1024, 2048, 4096) by
+    scripts/fit_emit_model.py."""
     peak_gbs: float = 6500.0        # HBM ceiling of a full grid
-    cta_gbs: float = 100.0          # what one CTA streams on its own
-    launch_us: float = 20.0         # per kernel launch (incl. its share of the final sync)
-    step_us: float = 0.4            # one strided-loop execution: barriers + CTA reduction
-    trip_us: float = 0.06           # one trip of a thread through a strided loop
-    rmw_trip_us: float = 0.25       # the same when the trip read-modify-writes global memory
-    stmt_us: float = 0.6            # a uniform statement that writes memory (thread 0 + barrier)
-    alloc_us: float = 30.0          # stream-ordered malloc + free of one temporary / partial per call
+    cta_gbs: float = 96.0          # what one CTA streams on its own
+    launch_us: float = 11.0         # per kernel launch (incl. its share of the final sync)
+    step_us: float = 0.13           # one strided-loop execution that ends in a barrier / CTA reduction
+    free_step_us: float = 0.0       # ... that ends in neither (barrier analysis removed them)
+    trip_us: float = 0.17           # one trip of a thread through a strided loop
+    jam_trip_us: float = 0.30       # the same per row when rows are batched (unroll-and-jam; a trip then
+                                    # carries `unroll` elements per row, hence the larger figure)
+    rmw_trip_us: float = 0.15       # a trip that read-modify-writes global memory
+    stmt_us: float = 1.27           # a uniform statement that writes memory and needs its barrier
+    free_stmt_us: float = 0.15      # ... and does not
+    alloc_us: float = 0.0           # stream-ordered malloc + free of one temporary / partial per call
                                     # (the reference pays malloc/free per call too, cemit.py:183-202)
     sm_count: int = 148
 
@@ -692,10 +1193,13 @@ def estimate_cost_ir(ir: dict, extents: dict, model: EmitModel | None = None,
                  count, unlike cost.py:80-86); vectors indexed by the strided
                  axis stay cache-resident per CTA and count once per block;
     * bandwidth grows with the number of CTAs up to the HBM ceiling (a serial
-      root runs in ONE CTA -- the GPU analogue of an unpartitioned CPU loop);
+      root runs in ONE CTA -- the GPU analogue of an unpartitioned CPU loop;
+      shared-memory accumulators cap the CTAs per SM);
     * steps   -- the longest block's chain of strided-loop executions (barriers,
                  CTA reductions, read-modify-write trips) and uniform memory
-                 writes, which bounds latency-dominated organisms.
+                 writes, which bounds latency-dominated organisms.  The emitter's own
+                 decisions are asked for, not guessed: whether a loop is jammed, which
+                 barriers its analysis removes, which partials live in shared memory.
     Returns cost.CostReport(source="analytic")."""
     from .cost import CostReport
 
@@ -704,64 +1208,82 @@ def estimate_cost_ir(ir: dict, extents: dict, model: EmitModel | None = None,
     ext = {k: float(v) for k, v in extents.items()}
     per_launch = []
     launches = 0
+    em = _Emitter(ir, blocks)
 
     def has_loop(items):
         return any(it["t"] == "loop" for it in items)
 
-    def walk(items, trips, nb, threads, acc):
-        """acc: dict(bytes=, steps=) for one launch; `trips` executions per block."""
+    def walk(items, trips, nb, threads, acc, in_region, batch):
+        """acc: dict(bytes=, steps=) for one launch; `trips` executions per block, `batch`
+        rows handled per execution (1 unless the enclosing loop is jammed)."""
         for it in items:
             if it["t"] == "stmt":
                 target = it["target"] if it["role"] == "init" else ops[str(it["op"])]["result"]
                 if st[target]["cls"] != "contracted":
-                    acc["steps"] += trips * m.stmt_us
+                    acc["steps"] += trips * batch * (m.stmt_us if em.conservative else m.free_stmt_us)
                 continue
             rng = ext[it["extent"]] / nb if it["sliced"] else ext[it["extent"]]
             if has_loop(it["body"]):
-                walk(it["body"], trips * max(rng, 1.0), nb, threads, acc)
+                jam = em.jam if em.jam_legal(it, in_region) else 1
+                walk(it["body"], trips * max(rng / jam, 1.0), nb, threads, acc, in_region, jam)
                 continue
             # strided (innermost) loop
             per_thread = max(1.0, rng / threads)
             mats, vecs, rmw = set(), set(), False
+            accs = em.lane_accumulators(it, "p_" if in_region else None, in_region)
             for s in it["body"]:
                 if s["role"] == "init":
-                    names, target, red = [s["target"]], s["target"], False
+                    names = [s["target"]]
                 else:
                     op = ops[str(s["op"])]
-                    names, target, red = list(op["operands"]) + [op["result"]], op["result"], op["reduction"]
-                    if red and it["axis"] in st[target]["labels"] and st[target]["cls"] != "contracted":
-                        rmw = True
+                    names = list(op["operands"]) + [op["result"]]
                 for n in names:
                     s_ = st[n]
                     if s_["cls"] == "contracted" or it["axis"] not in s_["labels"]:
                         continue
                     (mats if len(s_["labels"]) == 2 else vecs).add(n)
-            acc["bytes"] += 8.0 * len(mats) * rng * trips * nb + 8.0 * len(vecs) * rng * nb
-            acc["steps"] += trips * (m.step_us + per_thread * (m.rmw_trip_us if rmw else m.trip_us))
+            rmw = em.is_global_rmw(it, accs, in_region)
+            acc["bytes"] += 8.0 * len(mats) * rng * trips * batch * nb + 8.0 * len(vecs) * rng * nb
+            ends_in_sync = bool(accs) or em.loop_needs_barrier(it, in_region)
+            trip = m.rmw_trip_us if rmw else (m.jam_trip_us if batch > 1 else m.trip_us)
+            acc["steps"] += trips * ((m.step_us if ends_in_sync else m.free_step_us) + per_thread * batch * trip)
 
     def close(acc, nb):
         bw = min(m.peak_gbs, m.cta_gbs * min(nb, 4 * m.sm_count)) * 1e9
         per_launch.append((m.launch_us + max(acc["bytes"] / bw * 1e6, acc["steps"])) * 1e-6)
 
-    serial = None
+    serial_items, serial = [], None
+
+    def flush_serial():
+        nonlocal serial, launches
+        if not serial_items:
+            return
+        em.begin_launch(serial_items, False)
+        serial = {"bytes": 0.0, "steps": 0.0}
+        walk(serial_items, 1.0, 1.0, float(SERIAL_THREADS), serial, False, 1)
+        close(serial, 1.0)
+        launches += 1
+        serial_items.clear()
+
     for root in ir["roots"]:
         if root["t"] != "par":
-            if serial is None:
-                serial = {"bytes": 0.0, "steps": 0.0}
-                launches += 1
-            walk([root], 1.0, 1.0, float(SERIAL_THREADS), serial)
+            serial_items.append(root)
             continue
-        if serial is not None:
-            close(serial, 1.0)
-            serial = None
+        flush_serial()
         org_t = float(ir["threads"][root["slot"]])
         nb = max(org_t, float(blocks))
-        em = _Emitter(ir, blocks)
+        em.begin_launch(root["body"], True)
         if em.has_sliced_lane_loop(root["body"]):
-            nb = min(nb, max(org_t, float(int(ext[root["extent"]]) // CTA_THREADS)))
+            nb = min(nb, max(org_t, float(int(ext[root["extent"]]) // em.threads)))
+        if em.promoted:
+            smem = 8.0 * sum(ext[e] for e in em.promoted.values())
+            if smem <= SMEM_ACC_BYTES:
+                nb = min(nb, max(org_t, m.sm_count * float(int(227 * 1024 // (smem + 2048)))))
+            else:
+                em.promoted = {}                       # too long: they stay in the partial buffer
         nb = max(1.0, min(nb, ext[root["extent"]]))
         acc = {"bytes": 0.0, "steps": 0.0}
-        walk(root["body"], 1.0, nb, float(CTA_THREADS), acc)
+        walk(root["body"], 1.0, nb, float(em.threads), acc, True, 1)
         close(acc, nb)
         launches += 1
         for result in root["partials"]:          # join: read nb partial rows, write the result
@@ -769,11 +1291,9 @@ def estimate_cost_ir(ir: dict, extents: dict, model: EmitModel | None = None,
             size = 1.0
             for e in p["extents"]:
                 size *= ext[e]
-            per_launch.append((m.launch_us + 8.0 * size * (nb + 1) / (m.peak_gbs * 1e9) * 1e6
-                               + (nb * 0.01 if not p["extents"] else 0.0)) * 1e-6)
+            per_launch.append((m.launch_us + 8.0 * size * (nb + 1) / (m.peak_gbs * 1e9) * 1e6) * 1e-6)
             launches += 1
-    if serial is not None:
-        close(serial, 1.0)
+    flush_serial()
     nalloc = sum(1 for s in st.values() if s["cls"] in ("temp", "partial"))
     per_launch.append(nalloc * m.alloc_us * 1e-6)
     contracted = tuple(sorted(n for n, s in st.items() if s["cls"] == "contracted"))

@@ -14,8 +14,23 @@ for name in bto.HOT_PATH:
     ext = {"M": n * n} if typed.extent_names == ("M",) else {"M": n, "N": n}
     fused = cost.measure_empirical(cost.GpuVariant(name), typed, ext, reps=5)
     emitted = cuemit.measure_empirical_ir(irs[name][0], typed, ext, reps=3)
+    plain = cuemit.measure_empirical_ir(irs[name][0], typed, ext, reps=3, optimize=False)
     unf = cuemit.measure_empirical_ir(irs[name][1], typed, ext, reps=1)
     nbytes = bto._native.bytes_min(name, ext["M"], ext.get("N", 1))
     print(f"{name:8s} n={n}: hand-written {fused.total*1e3:8.3f} ms ({nbytes/fused.total/1e9:6.0f} GB/s)   "
           f"emitted max-fuse {emitted.total*1e3:8.3f} ms ({nbytes/emitted.total/1e9:6.0f} GB/s)   "
+          f"plain mapping {plain.total*1e3:8.3f} ms   "
           f"emitted unfused {unf.total*1e3:9.3f} ms  {emitted.diagnostic or ''} {unf.diagnostic or ''}", flush=True)
+
+# GEMVER: the CPU max-fuse organism partitions columns; the row-partitioned ones the GA finds on
+# the GPU model (profiles/r01/ga_best_irs.json) are the fair comparison
+best = json.loads((REPO / "profiles/r01/ga_best_irs.json").read_text())
+typed = bto.load_graph("gemver")
+ext = {"M": n, "N": n}
+nbytes = bto._native.bytes_min("gemver", n, n)
+for entry in best["gemver"]["alternatives"]:
+    ir = entry["ir"]
+    e = cuemit.measure_empirical_ir(ir, typed, ext, reps=3)
+    p = cuemit.measure_empirical_ir(ir, typed, ext, reps=3, optimize=False)
+    print(f"gemver {ir['organism']}: emitted {e.total*1e3:8.3f} ms ({nbytes/e.total/1e9:6.0f} GB/s)  "
+          f"plain {p.total*1e3:8.3f} ms {e.diagnostic or ''}", flush=True)

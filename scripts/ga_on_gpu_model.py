@@ -30,4 +30,11 @@ for name in ("axpydot", "bicgk", "atax", "gesummv", "gemver"):
     }
     print(f"{name:8s} evals {res.evaluations:4d}  GA best {res.best_fitness*1e3:8.3f} ms {canonical_key(res.best)}")
     print(f"{'':8s}            max-fuse {out[name]['max_fuse']['model_ms']:8.3f} ms {canonical_key(seed_org)}")
-(REPO / "profiles" / "r01" / "ga_best_irs.json").write_text(json.dumps(out, separators=(",", ":")))
+# hand-picked alternatives recorded earlier (GEMVER's row-partitioned organisms) stay, re-priced
+path = REPO / "profiles" / "r01" / "ga_best_irs.json"
+if path.exists():
+    for name, entry in json.loads(path.read_text()).items():
+        for alt in entry.get("alternatives", []):
+            alt["model_ms"] = cuemit.estimate_cost_ir(alt["ir"], out[name]["extents"]).total * 1e3
+            out[name].setdefault("alternatives", []).append(alt)
+path.write_text(json.dumps(out, separators=(",", ":")))

@@ -27,12 +27,7 @@ for n in sizes:
         ext = {"M": n * n} if typed.extent_names == ("M",) else {"M": n, "N": n}
         inputs = bto.gen_inputs(typed, ext, seed=1)
         dev = {k: (torch.from_numpy(v).cuda() if hasattr(v, "shape") else v) for k, v in inputs.items()}
-        cuemit.run_emitted(path, kernel, ir, dev, ext)
-        best = 1e9
-        for _ in range(3):
-            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            a.record(); cuemit.run_emitted(path, kernel, ir, dev, ext); b.record(); b.synchronize()
-            best = min(best, a.elapsed_time(b) * 1e-3)
+        best = cuemit.time_emitted(path, kernel, ir, dev, ext, reps=3)
         rows.append({"kernel": name, "index": i, "organism": ir["organism"], "M": ext["M"],
                      "N": ext.get("N", 1), "seconds": best})
         print(f"n={n} {name:8s} #{i:2d} {best*1e3:9.3f} ms  {ir['organism'][:70]}", flush=True)

@@ -44,7 +44,7 @@ def test_emission_is_deterministic_and_keeps_the_reference_signature():
 
 def test_structure_of_the_bicgk_max_fuse_kernel():
     ir = next(ir for ir in IRS["bicgk"] if ir["organism"].startswith("{_{p(i)}{_i{_j 1 2}}}"))
-    src = cuemit.emit_cuda(ir, blocks=64).source
+    src = cuemit.emit_cuda(ir, blocks=64, optimize=False).source         # the plain mapping
     assert "for (long i = i_lo; i < i_hi; ++i)" in src                  # block's rows, uniform
     assert "for (long j = 0 + threadIdx.x; j < N; j += blockDim.x)" in src   # innermost: strided
     assert "lacc1 += __dmul_rn(A[i * N + j], p[j]);" in src            # row dot -> thread accumulator
@@ -52,17 +52,37 @@ def test_structure_of_the_bicgk_max_fuse_kernel():
     assert "cta_allreduce(lacc1, scratch_)" in src
     assert "long nb0_ = 64;" in src and "bicgk_region0<<<(unsigned)nb0_, 256, 0, 0>>>" in src
     assert "bicgk_join1_s" in src
+    # optimised: rows four at a time, column partial in shared memory, one batched reduction,
+    # no barrier besides the reduction's own (q is only ever touched by thread 0)
+    opt = cuemit.emit_cuda(ir, blocks=64).source
+    assert "for (; i_b_ + 4 <= i_hi; i_b_ += 4)" in opt and "for (long i = i_b_; i < i_hi; ++i)" in opt
+    assert "double *s_part_l = sm_ok_ ? dyn_ + (0) : s_part + p_ * (N);" in opt
+    # explicit load / compute batches with a literal stride: all loads first, then the statements
+    assert "for (; j_b_ + 768 < N; j_b_ += 1024)" in opt and "double A_v[4][4];" in opt
+    assert "A_v[r_][u_] = ld_stream(&A[i * N + j]);" in opt and "p_v[u_] = ld_keep(&p[j]);" in opt
+    assert "__launch_bounds__(256, 2) bicgk_region0" in opt
+    assert "s_part_l[j] += __dmul_rn(A_v[r_][u_], r[i]);" in opt
+    assert "cta_allreduce_n<4>(lacc1_a, scratch_);" in opt
+    assert "s_part[p_ * (N) + j] = s_part_l[j];" in opt
+    body = opt[opt.index("bicgk_region0("):opt.index("bicgk_join1_s")]
+    assert "__syncthreads" not in body
+    # ATAX: the contracted row value is an array over the jammed rows
+    atax = cuemit.emit_cuda(next(i for i in IRS["atax"] if i["organism"].startswith("{_{p(i)}{_i{_j 1}{_j 2}}}"))).source
+    assert "double t0_s_a[4];" in atax and "double &t0_s = t0_s_a[r_];" in atax
+    # a value written by thread 0 and read by every thread keeps all barriers and is not jammed
+    plain = cuemit.emit_cuda(next(i for i in IRS["gesummv"] if i["organism"].startswith("{_i{_j 1}}{_i 2}"))).source
+    assert "cta_allreduce_n<" not in plain and "__syncthreads();" in plain
     # a region whose strided loops run over its own slice gets at least a CTA-width per block
     gem = cuemit.emit_cuda(IRS["gemver"][0], blocks=592).source
     assert "long nb0_ = N / 256; if (nb0_ < 8) nb0_ = 8; if (nb0_ > 592) nb0_ = 592;" in gem
 
 
-def _compile_all(irs, workdir, blocks=cuemit.DEFAULT_BLOCKS):
+def _compile_all(irs, workdir, blocks=cuemit.DEFAULT_BLOCKS, optimize=True):
     tc = cuemit.NvccToolchain()
 
     def job(args):
         idx, ir = args
-        k = cuemit.emit_cuda(ir, blocks=blocks)
+        k = cuemit.emit_cuda(ir, blocks=blocks, optimize=optimize)
         return idx, k, tc.compile(k.source, workdir, name=f"{ir['name'].lower()}_{idx}")
 
     with ThreadPoolExecutor(max_workers=8) as pool:
@@ -87,14 +107,17 @@ def test_compile_failure_is_reported(tmp_path):
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("optimize", [True, False], ids=["optimised", "plain"])
 @pytest.mark.parametrize("name", sorted(IRS))
-def test_every_organism_matches_the_oracle(bto_lib, oracle, tmp_path, name):
+def test_every_organism_matches_the_oracle(bto_lib, oracle, tmp_path, name, optimize):
     typed = bto.load_graph(name)
-    built = _compile_all(IRS[name], tmp_path, blocks=37)       # odd block count: ragged slices
+    built = _compile_all(IRS[name], tmp_path, blocks=37, optimize=optimize)   # odd block count: ragged slices
     worst = 0.0
+    # (6, 24700): a row too long for the shared-memory accumulators -> they stay in the partial buffer
+    sizes = [(1, 1), (7, 50), (200, 200), (513, 1030)] + ([(6, 24700)] if optimize else [])
     for idx, kernel, path in built:
         ir = IRS[name][idx]
-        for (m, n) in [(1, 1), (7, 50), (200, 200), (513, 1030)]:
+        for (m, n) in sizes:
             ext = {"M": m * n} if typed.extent_names == ("M",) else {"M": m, "N": n}
             inputs = bto.random_inputs(typed, ext, seed=idx)
             want = oracle.oracle_run(name, inputs, ext, threads=8)
@@ -186,8 +209,8 @@ class TestOrganismCostModel:
             meas.append(r["seconds"])
         rho = spearmanr(pred, meas).correlation
         logerr = np.abs(np.log(np.array(pred) / np.array(meas)))
-        assert rho > 0.9, rho
-        assert np.median(logerr) < 0.35 and np.sqrt(np.mean(logerr ** 2)) < 0.6
+        assert rho > 0.95, rho
+        assert np.median(logerr) < 0.25 and np.sqrt(np.mean(logerr ** 2)) < 0.4
 
     def test_fusion_and_partitioning_pay_off(self):
         ext = {"M": 4096, "N": 4096}
@@ -203,8 +226,8 @@ class TestOrganismCostModel:
         # GEMVER max-fuse reads B a second time inside the same root: the reference's
         # distinct-array rule counts it once (cost.py:80-86), the GPU model twice
         ir = IRS["gemver"][0]
-        model = cuemit.EmitModel(step_us=0.0, trip_us=0.0, rmw_trip_us=0.0, stmt_us=0.0,
-                                 launch_us=0.0, alloc_us=0.0, cta_gbs=1e9)
+        model = cuemit.EmitModel(step_us=0.0, free_step_us=0.0, trip_us=0.0, jam_trip_us=0.0, rmw_trip_us=0.0,
+                                 stmt_us=0.0, free_stmt_us=0.0, launch_us=0.0, alloc_us=0.0, cta_gbs=1e9)
         n = 8192
         rep = cuemit.estimate_cost_ir(ir, {"M": n, "N": n}, model)
         streamed = rep.total * model.peak_gbs * 1e9
