@@ -383,6 +383,82 @@ def test_bench_size_cross_kernel_identities(bto_lib):
     assert _err(y, 0.75 * torch.mv(A, x)) <= 1e-12 * math.log2(m)
 
 
+def test_more_than_2_to_the_32_elements(bto_lib):
+    """Matrices of 4.3e9 and more elements (32-36 GiB each): every index computation has to
+    be 64-bit.  Rank-1 matrices A = a b' give closed forms at any size:
+    A p = a (b.p), A' r = b (a.r), A'(A x) = b (a.a)(b.x)."""
+    free, _ = torch.cuda.mem_get_info()
+    if free < 100 * 2 ** 30:
+        pytest.skip("needs ~80 GiB of free HBM")
+
+    def rank1(m, n, seed):
+        a, b = _rand((m,), seed), _rand((n,), seed + 1)
+        A = torch.empty((m, n), dtype=torch.float64, device="cuda")
+        torch.outer(a, b, out=A)
+        return A, a, b
+
+    def close(got, want, scale, tol):
+        return float(torch.max(torch.abs(got - want))) <= tol * scale
+
+    for m, n in ((65536, 65536), (36000, 120000)):
+        ext = {"M": m, "N": n}
+        A, a, b = rank1(m, n, m % 97)
+        p, r = _rand((n,), 3), _rand((m,), 4)
+        bp, ar, aa = float(torch.dot(b, p)), float(torch.dot(a, r)), float(torch.dot(a, a))
+        scale = math.sqrt(max(m, n))                     # size of a length-n dot of U[-1,1) terms
+        out = _run("bicgk", {"A": A, "p": p, "r": r}, ext)
+        assert close(out["q"], a * bp, scale, 1e-12) and close(out["s"], b * ar, scale, 1e-12)
+        y = _run("atax", {"A": A, "x": p}, ext)["y"]
+        want = b * (aa * bp)
+        assert close(y, want, float(torch.max(torch.abs(want))), 1e-11)
+        # the last row / column really were read: perturb one corner element
+        A[m - 1, n - 1] += 1.0
+        out2 = _run("bicgk", {"A": A, "p": p, "r": r}, ext)
+        assert abs(float(out2["q"][m - 1] - out["q"][m - 1]) - float(p[n - 1])) <= 1e-9
+        assert abs(float(out2["s"][n - 1] - out["s"][n - 1]) - float(r[m - 1])) <= 1e-9
+        assert torch.equal(out2["q"][: m - 1], out["q"][: m - 1])
+        del out, out2, y
+        if m == n:
+            # GEMVER with A and B of 32 GiB each: sampled rows of B bit-exact, x and w closed-form
+            u1, v1, u2, v2, yv, z = (_rand((n,), sd) for sd in (5, 6, 7, 8, 9, 10))
+            A[m - 1, n - 1] -= 1.0
+            ge = _run("gemver", {"A": A, "u1": u1, "v1": v1, "u2": u2, "v2": v2,
+                                 "alpha": 0.7, "beta": 0.3, "y": yv, "z": z}, ext)
+            rows = torch.tensor([0, 1, 32767, 32768, m - 1], device="cuda")
+            want = (A[rows] + u1[rows, None] * v1[None, :]) + u2[rows, None] * v2[None, :]
+            assert torch.equal(ge["B"][rows], want)
+            bty = b * float(torch.dot(a, yv)) + v1 * float(torch.dot(u1, yv)) + v2 * float(torch.dot(u2, yv))
+            assert close(ge["x"], 0.3 * bty + z, scale, 1e-11)
+            x = ge["x"]
+            bx = a * float(torch.dot(b, x)) + u1 * float(torch.dot(v1, x)) + u2 * float(torch.dot(v2, x))
+            assert close(ge["w"], 0.7 * bx, float(torch.max(torch.abs(bx))), 1e-11)
+            del ge, want
+        del A
+        torch.cuda.empty_cache()
+    # GESUMMV: two matrices of 2^32 + elements would need 69 GiB; 50000^2 x 2 = 40 GB is the same code path
+    m = 50000
+    A, a, b = rank1(m, m, 11)
+    B, c, d = rank1(m, m, 13)
+    x = _rand((m,), 15)
+    y = _run("gesummv", {"alpha": 0.375, "beta": -0.5, "A": A, "B": B, "x": x}, {"M": m, "N": m})["y"]
+    want = 0.375 * a * float(torch.dot(b, x)) - 0.5 * c * float(torch.dot(d, x))
+    assert close(y, want, math.sqrt(m), 1e-12)
+    # AXPYDOT on 2^32 + 5 elements (4 vectors of 32 GiB)
+    del A, B
+    torch.cuda.empty_cache()
+    k = (1 << 32) + 5
+    w = torch.empty(k, dtype=torch.float64, device="cuda")
+    w[: 1 << 31] = _rand((1 << 31,), 17)
+    w[1 << 31: 1 << 32] = w[: 1 << 31]
+    w[1 << 32:] = 3.0
+    out = _run("axpydot", {"w": w, "v": w, "u": w, "alpha": 0.5}, {"M": k})
+    assert torch.equal(out["z"][-5:], torch.full((5,), 1.5, dtype=torch.float64, device="cuda"))
+    assert torch.equal(out["z"][: 1 << 20], w[: 1 << 20] - w[: 1 << 20] * 0.5)
+    q4 = 1 << 30                                              # (torch.dot takes < 2^31 elements)
+    half = float(torch.dot(w[:q4], w[:q4])) + float(torch.dot(w[q4: 2 * q4], w[q4: 2 * q4]))  # beta = 0.5 * sum w^2
+    assert abs(out["beta"] - (0.5 * (2 * half + 45.0))) <= 1e-10 * half
+
+
 def test_bench_size_axpydot_properties(bto_lib):
     n = 1 << 27
     w, v, u = _rand((n,), 1), _rand((n,), 2), _rand((n,), 3)
