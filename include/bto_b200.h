@@ -178,6 +178,23 @@ int bto_prim_outer_async(const double *u, const double *v, double *out, long M, 
 int bto_prim_dot_async(const double *x, const double *y, double *out, long n,
                        bto_stream_t stream);
 
+/* ---- 3d. fused passes for column-major operands -----------------------------
+ * A `matrix(column)` operand (lang.py:17-31, runtime.py:92-95) reaches the
+ * library as the row-major buffer S of its TRANSPOSE.  Every corpus sequence
+ * then maps onto the row-major passes with the roles of the two products
+ * swapped (A x = S' x is a column sum, A' r = S r a row dot); the two shapes
+ * the row-major entry points do not offer are these (device pointers):
+ *   colsum_axpz : out[c] = (sum_r S[r,c]*y[r])*scale (+ z[c] when z != NULL)
+ *   rank2_rowdot: Sout[r,c] = (S[r,c] + a1[r]*b1[c]) + a2[r]*b2[c];
+ *                 out[r] = (sum_c Sout[r,c]*wgt[c])*scale + add[r]
+ * each product and sum rounded as in cemit.py:112-136; S is rows x cols.      */
+int bto_colsum_axpz_async(const double *S, const double *y, double scale, const double *z,
+                          double *out, long rows, long cols, bto_stream_t stream);
+int bto_rank2_rowdot_async(const double *S, const double *a1, const double *b1,
+                           const double *a2, const double *b2, const double *wgt,
+                           double scale, const double *add, double *Sout, double *out,
+                           long rows, long cols, bto_stream_t stream);
+
 /* ---- 4. runtime control and introspection --------------------------------- */
 int   bto_abi_version(void);
 int   bto_set_stream(bto_stream_t stream);      /* stream for section-1 calls */

@@ -55,6 +55,7 @@ EXPORTED = tuple(SIGNATURES) + tuple(f"bto_{k}_async" for k in SIGNATURES) + (
     "bto_axpydot_sharded_async", "bto_bicgk_sharded_async", "bto_atax_sharded_async",
     "bto_gemver_sharded_async",
     "bto_prim_matvec_async", "bto_prim_axpby_async", "bto_prim_outer_async", "bto_prim_dot_async",
+    "bto_colsum_axpz_async", "bto_rank2_rowdot_async",
     "bto_last_error", "bto_last_error_string", "bto_clear_error",
     "bto_abi_version", "bto_set_stream", "bto_set_tuning", "bto_get_tuning",
     "bto_kernel_launches", "bto_bytes_min", "bto_device_info",
@@ -105,6 +106,10 @@ def load() -> ctypes.CDLL:
     lib.bto_prim_outer_async.argtypes = [_P, _P, _P, _L, _L, _S]
     lib.bto_prim_dot_async.restype = c_int
     lib.bto_prim_dot_async.argtypes = [_P, _P, _P, _L, _S]
+    lib.bto_colsum_axpz_async.restype = c_int
+    lib.bto_colsum_axpz_async.argtypes = [_P, _P, _D, _P, _P, _L, _L, _S]
+    lib.bto_rank2_rowdot_async.restype = c_int
+    lib.bto_rank2_rowdot_async.argtypes = [_P, _P, _P, _P, _P, _P, _D, _P, _P, _P, _L, _L, _S]
     lib.bto_exchange_init.restype = c_int
     lib.bto_exchange_init.argtypes = [c_int, c_int, POINTER(c_void_p), POINTER(c_void_p), _L,
                                       ctypes.c_uint]

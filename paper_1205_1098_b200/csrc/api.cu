@@ -476,6 +476,41 @@ int bto_prim_dot_async(const double *x, const double *y, double *out, long n, bt
     return check_launch("prim_dot_kernel");
 }
 
+// ---- section 3d: fused passes over a transposed (column-major) operand --------------
+
+int bto_colsum_axpz_async(const double *S, const double *y, double scale, const double *z,
+                          double *out, long rows, long cols, bto_stream_t stream)
+{
+    ASYNC_PROLOGUE();
+    BTO_TRY(check_mn(rows, cols));
+    FinArgs f{};
+    f.cmode = z ? kColAxpz : kColScale;
+    f.cscale = scale;
+    f.colz = z;
+    f.colout = out;
+    return seq_pass1(*ac.ctx, S, nullptr, nullptr, nullptr, nullptr, y, nullptr, f, rows, cols, st);
+}
+
+int bto_rank2_rowdot_async(const double *S, const double *a1, const double *b1, const double *a2,
+                           const double *b2, const double *wgt, double scale, const double *add,
+                           double *Sout, double *out, long rows, long cols, bto_stream_t stream)
+{
+    ASYNC_PROLOGUE();
+    BTO_TRY(check_mn(rows, cols));
+    if (!a1 || !b1 || !a2 || !b2 || !add) return fail(BTO_ERR_INVALID, "rank2_rowdot: null vector");
+    DeviceCtx &c = *ac.ctx;
+    WsLayout lay;
+    Pass<kFlagN | kFlagRank2> pass;
+    BTO_TRY(pass.prepare(c, rows, cols, mat_aligned(cols, S, Sout), &lay));
+    BTO_TRY(size_ws(c, lay));
+    MvArgs a{};
+    a.A = S; a.colw = wgt;
+    a.u1 = a1; a.v1 = b1; a.u2 = a2; a.v2 = b2; a.Bout = Sout;
+    FinArgs f{};
+    f.rmode = kRowDgemv; f.ralpha = scale; f.rbeta = 1.0; f.rowy = add; f.rowout = out;
+    return pass.run(c, a, f, st);
+}
+
 // ---- section 4: control ----------------------------------------------------------
 
 int bto_set_stream(bto_stream_t stream)

@@ -118,6 +118,7 @@ constexpr MvDefault mv_default()
     if (FLAGS == (kFlagN | kFlagT)) return {8, 1, 8, 4};        // BiCGK         7.10 TB/s
     if (FLAGS == (kFlagN | kFlagN2)) return {8, 1, 4, 4};       // GESUMMV       7.04 TB/s
     if (FLAGS == (kFlagT | kFlagRank2)) return {16, 1, 2, 1};   // GEMVER pass 1 6.29 TB/s (r+w)
+    if (FLAGS == (kFlagN | kFlagRank2)) return {8, 1, 4, 2};    // column-major GEMVER pass 1 6.38 TB/s (r+w)
     if (FLAGS == kFlagT) return {32, 1, 2, 1};                  // A' y          7.17 TB/s
     return {8, 2, 8, 2};                                        // A x           7.20 TB/s
 }

@@ -108,6 +108,13 @@ def gpu_kernel(graph, allow_generic: bool = True) -> GeneratedKernel:
         try:
             name = match_corpus(spec)
         except UnsupportedKernelError:
+            from .colmajor import column_major_variant
+            cm = column_major_variant(spec)
+            if cm is not None:      # a corpus kernel on column-major matrices: fused, roles swapped
+                return GeneratedKernel(
+                    source=f"libbto_b200:colmajor:{cm}", kernel_name=spec.name.lower(),
+                    params=_c_params(spec.inputs, spec.outputs, typed.extent_names),
+                    organism_key="colmajor " + _SEQUENCES[cm])
             if not allow_generic:
                 raise
             return GeneratedKernel(
@@ -258,6 +265,9 @@ def run_kernel(binary, kernel: GeneratedKernel, graph, inputs: dict,
     if kernel.source.endswith(":generic"):
         from .generic import run_generic
         return run_generic(_as_typed(graph), inputs, extents)
+    if ":colmajor:" in kernel.source:
+        from .colmajor import run_colmajor
+        return run_colmajor(kernel.source.rsplit(":", 1)[1], _as_typed(graph), inputs, extents)
     lib, args, out_bufs, keep, on_gpu = _marshal(binary, kernel, graph, inputs, extents)
     fn = getattr(lib, kernel.kernel_name)
     if on_gpu:

@@ -36,7 +36,7 @@ SPECS = {
              "x : vector(column) out: C : matrix(row), y : vector(column) "
              "{ C = A + u * v'  y = C * x }",
     "colmajor": "COLMAJOR in: A : matrix(column), x : vector(column), w : vector(column) "
-                "out: y : vector(column), z : vector(column) { y = A * x  z = A' * w }",
+                "out: y : vector(column), z : vector(column) { y = A * x  z = A' * w + x }",
     "mixed": "MIXED in: A : matrix(row), B : matrix(column), x : vector(column), gamma : scalar "
              "out: C : matrix(row), y : vector(column) { C = A - gamma * B  y = gamma * C * x }",
     "gram": "GRAM in: A : matrix(row), x : vector(column), lam : scalar out: y : vector(column) "

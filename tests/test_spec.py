@@ -111,3 +111,26 @@ def test_generated_kernel_handle():
     assert k.kernel_name == "gesummv"
     assert [n for _, n in k.params] == ["alpha", "beta", "A", "B", "x", "y", "M", "N"]
     assert k.params[0][0] == "double alpha" and k.params[2][0] == "const double *A"
+
+
+def test_column_major_variants_of_the_corpus_are_recognised():
+    """All matrices `matrix(column)` -> the fused column-major mapping (colmajor.py);
+    mixed orientations and non-corpus structures are left to the generic executor."""
+    from paper_1205_1098_b200 import spec as S
+    from paper_1205_1098_b200.colmajor import COLMAJOR_SEQUENCES, column_major_variant
+    for name in S.CORPUS:
+        text = S.CORPUS[name]
+        assert column_major_variant(S.parse_kernel(text)) is None              # row-major: not ours
+        col = S.parse_kernel(text.replace("matrix(row)", "matrix(column)"))
+        assert column_major_variant(col) == (name if name in COLMAJOR_SEQUENCES else None)
+    mixed = S.parse_kernel(S.CORPUS["gesummv"].replace("A : matrix(row)", "A : matrix(column)"))
+    assert column_major_variant(mixed) is None
+    other = S.parse_kernel("K in: A : matrix(column), x : vector(column) out: y : vector(column) "
+                           "{ y = A * x }")
+    assert column_major_variant(other) is None
+    # gpu_kernel: fused handle with the caller's kernel name and the corpus argument order
+    import paper_1205_1098_b200 as bto
+    g = S.infer_shapes(S.parse_kernel(S.CORPUS["gemver"].replace("matrix(row)", "matrix(column)")))
+    k = bto.gpu_kernel(g, allow_generic=False)
+    assert k.source == "libbto_b200:colmajor:gemver" and k.organism_key.startswith("colmajor ")
+    assert [n for _, n in k.params][:3] == ["A", "u1", "v1"]
