@@ -3,6 +3,7 @@
 #pragma once
 #include "host_context.cuh"
 #include "mv_kernels.cuh"
+#include "skinny_kernels.cuh"
 #include "vec_kernels.cuh"
 
 namespace bto_host {
@@ -185,7 +186,10 @@ int launch_mv(const MvPlan &p, const MvArgs &a, cudaStream_t stream)
 // is fused into it (join_exchange_kernel); otherwise the plain local join runs.
 int launch_join(DeviceCtx &c, FinArgs f, cudaStream_t stream)
 {
-    const long rb = f.rmode != kRowNone ? (f.M + kThreads - 1) / kThreads : 0;
+    // threads per row of the row-side join (finalize_rows_cta)
+    f.row_group = f.nstrips <= 128 ? 1 : (f.nstrips <= 4096 ? 32 : kThreads);
+    const long rows_per_cta = kThreads / f.row_group;
+    const long rb = f.rmode != kRowNone ? (f.M + rows_per_cta - 1) / rows_per_cta : 0;
     if (c.exch_active && f.cmode != kColNone) {
         if (2 * f.N > c.exch_capacity) {
             return fail(BTO_ERR_INVALID, "exchange buffer holds %ld doubles, need %ld",
@@ -203,7 +207,11 @@ int launch_join(DeviceCtx &c, FinArgs f, cudaStream_t stream)
         return launch_dependent(join_exchange_kernel, (unsigned)(kExchCtas + rb), e, stream,
                                 "join_exchange_kernel");
     }
-    const long cb = f.cmode != kColNone ? (f.N + kJoinCols - 1) / kJoinCols : 0;
+    // few partials per column (a short, wide matrix: about grid / nstrips of them): a thread per
+    // column; otherwise 8 warps share the partials of 32 columns
+    const long per_col = f.nstrips > 0 ? f.grid / f.nstrips + 2 : f.grid;
+    f.col_cols = per_col <= 8 ? kThreads : kJoinCols;
+    const long cb = f.cmode != kColNone ? (f.N + f.col_cols - 1) / f.col_cols : 0;
     f.col_blocks = (int)cb;
     return launch_dependent(finalize_kernel, (unsigned)(cb + rb), f, stream, "finalize_kernel");
 }
@@ -237,9 +245,82 @@ bool mat_aligned(long N, const void *a, const void *b = nullptr, const void *c =
 // prepare() plans the launch and books its partial buffers in the sequence's
 // workspace layout; run() launches after the workspace has been sized once,
 // so no pointer handed out earlier in the sequence can move.
+// ---- narrow matrices (skinny_kernels.cuh) --------------------------------------------
+
+struct SkinnyPlan {
+    bool pair = true;          // column pairs (double2) or single columns per thread
+    int V = 1;                 // column slots per thread
+    int L = 1;                 // threads per row (<= 32)
+    long grid = 0;             // 0: not in use
+    long rows_per_cta = 0;
+};
+
+// column pairs cover N <= 512; single columns (odd N or unaligned operands) N <= 256
+bool skinny_applies(long N, bool aligned)
+{
+    return g_tuning.skinny != 0 && (N <= 256 || (N <= kSkinnyMaxN && aligned));
+}
+
+SkinnyPlan plan_skinny(DeviceCtx &c, long M, long N, bool aligned)
+{
+    SkinnyPlan p;
+    p.pair = aligned && (N % 2 == 0);
+    const long width = p.pair ? N / 2 : N;                        // column slots in a row
+    p.V = 1;
+    while (32L * p.V < width && p.V < 8) p.V *= 2;                // 8 slots x 32 lanes x 2 = 512 columns
+    if (!p.pair && p.V == 2) p.V = 4;                             // (singles are built for V = 1, 4, 8)
+    p.L = 1;
+    while ((long)p.L * p.V < width) p.L *= 2;
+    const long unit = (long)(kSkinnyRows / p.V) * (kThreads / p.L);   // rows one CTA covers per step
+    const long per_sm = g_tuning.grid_per_sm > 0 ? g_tuning.grid_per_sm : 4;
+    const long target = (long)c.sm_count * per_sm;
+    long rows = (M + target - 1) / target;
+    rows = ((rows + unit - 1) / unit) * unit;
+    // a few units per CTA at least: the fold of the column sums and the partial row are per CTA
+    if (rows < 4 * unit) rows = 4 * unit;
+    p.rows_per_cta = rows;
+    p.grid = (M + rows - 1) / rows;
+    return p;
+}
+
+// the join of the per-CTA column partials of a skinny pass (and its sharded exchange)
+int launch_join(DeviceCtx &c, FinArgs f, cudaStream_t stream);
+
+template <int FLAGS>
+int run_skinny(DeviceCtx &c, const SkinnyPlan &p, const MvArgs &a, FinArgs f, cudaStream_t stream)
+{
+    SkinnyArgs s{};
+    s.mv = a;
+    s.fin = f;
+    s.L = p.L;
+    s.rows_per_cta = p.rows_per_cta;
+    void (*fn)(const SkinnyArgs) = nullptr;
+    if (p.pair) {
+        fn = p.V == 1 ? mv_skinny_kernel<FLAGS, true, 1>
+                      : (p.V == 2 ? mv_skinny_kernel<FLAGS, true, 2>
+                                  : (p.V == 4 ? mv_skinny_kernel<FLAGS, true, 4> : mv_skinny_kernel<FLAGS, true, 8>));
+    } else {
+        fn = p.V == 1 ? mv_skinny_kernel<FLAGS, false, 1>
+                      : (p.V == 4 ? mv_skinny_kernel<FLAGS, false, 4> : mv_skinny_kernel<FLAGS, false, 8>);
+    }
+    BTO_TRY(launch_dependent(fn, (unsigned)p.grid, s, stream, "mv_skinny_kernel"));
+    if (f.cmode == kColNone) return BTO_OK;
+    f.colpart = a.colpart;
+    f.M = a.M;
+    f.N = a.N;
+    f.strip_width = a.N;               // one "strip": every column has the same contributors
+    f.units_per_strip = p.grid;        // owner(u) = u when units == CTAs
+    f.total_units = p.grid;
+    f.grid = p.grid;
+    f.nstrips = 1;
+    f.rmode = kRowNone;
+    return launch_join(c, f, stream);
+}
+
 template <int FLAGS>
 struct Pass {
     MvPlan plan;
+    SkinnyPlan skinny;             // used instead of `plan` for narrow matrices
     size_t off_row = 0, off_row2 = 0, off_col = 0;
     long M = 0, N = 0;
 
@@ -247,6 +328,12 @@ struct Pass {
     {
         M = m;
         N = n;
+        // (a full 512-column strip of a rank-2 pass is mv_tile_kernel's best case: 5.9 vs 4.9 TB/s)
+        if (skinny_applies(N, aligned) && !((FLAGS & kFlagRank2) && N == kSkinnyMaxN)) {
+            skinny = plan_skinny(c, M, N, aligned);
+            if (FLAGS & kFlagT) off_col = lay->take((size_t)skinny.grid * N);
+            return BTO_OK;
+        }
         BTO_TRY(plan_mv<FLAGS>(c, M, N, aligned, &plan));
         if (FLAGS & kFlagN) off_row = lay->take((size_t)plan.nstrips * M);
         if (FLAGS & kFlagN2) off_row2 = lay->take((size_t)plan.nstrips * M);
@@ -258,6 +345,14 @@ struct Pass {
     // through f.cmode.
     int run(DeviceCtx &c, MvArgs a, FinArgs f, cudaStream_t stream) const
     {
+        if (skinny.grid > 0) {
+            a.M = M;
+            a.N = N;
+            a.colpart = reinterpret_cast<double *>(c.ws + off_col);
+            if (!(FLAGS & kFlagN)) f.rmode = kRowNone;
+            if (!(FLAGS & kFlagT)) f.cmode = kColNone;
+            return run_skinny<FLAGS>(c, skinny, a, f, stream);
+        }
         fill_geometry(plan, &a, M, N);
         a.rowpart = reinterpret_cast<double *>(c.ws + off_row);
         a.rowpart2 = reinterpret_cast<double *>(c.ws + off_row2);

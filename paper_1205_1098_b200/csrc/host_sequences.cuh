@@ -229,6 +229,21 @@ int seq_atax(DeviceCtx &c, const double *A, const double *x, double *y, long M,
              long N, bool scaled, double beta, cudaStream_t st)
 {
     BTO_TRY(check_mn(M, N));
+    if (skinny_applies(N, mat_aligned(N, A))) {
+        // a row lives inside one CTA segment: t_i = A_i . x is complete before A_i leaves the
+        // registers, so y = A' t needs no second pass
+        WsLayout lay;
+        const SkinnyPlan sp = plan_skinny(c, M, N, mat_aligned(N, A));
+        const size_t off = lay.take((size_t)sp.grid * N);
+        BTO_TRY(size_ws(c, lay));
+        MvArgs a{};
+        a.A = A; a.colw = x; a.M = M; a.N = N;
+        a.colpart = reinterpret_cast<double *>(c.ws + off);
+        FinArgs f{};
+        f.rmode = kRowNone;
+        f.cmode = scaled ? kColScale : kColPlain; f.cscale = beta; f.colout = y;
+        return run_skinny<kFlagN | kFlagT | kFlagAtax>(c, sp, a, f, st);
+    }
     AtaxPlan fused;
     BTO_TRY(plan_atax(c, A, x, M, N, &fused));
     if (fused.fn) return seq_atax_fused(c, fused, A, x, y, M, N, scaled, beta, st);

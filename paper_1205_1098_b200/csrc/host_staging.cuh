@@ -420,6 +420,7 @@ int join_partials(const double *parts, long count, long n, int cmode, double sca
     f.total_units = count;
     f.grid = count;
     f.rmode = kRowNone;
+    f.col_cols = kJoinCols;
     f.col_blocks = (int)((n + kJoinCols - 1) / kJoinCols);
     return launch_dependent(finalize_kernel, (unsigned)f.col_blocks, f, st, "finalize_kernel");
 }

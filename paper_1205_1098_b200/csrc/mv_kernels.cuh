@@ -307,6 +307,9 @@ struct FinArgs {
     long M;
     int nstrips;
     int col_blocks;           // CTAs [0, col_blocks) do columns, the rest rows
+    int row_group;            // threads that share one row's join: 1, 32 (a warp) or 256 (the CTA)
+    int col_cols;             // columns per column CTA: kJoinCols (8 warps share a column's partials)
+                              // or kThreads (a thread per column: few partials, very many columns)
 };
 
 constexpr int kJoinCols = 32;  // columns per column CTA of finalize_kernel
@@ -378,12 +381,10 @@ __device__ __forceinline__ void join_columns_cta(const FinArgs &f, long j0)
     }
 }
 
-// join + epilogue of row i
-__device__ __forceinline__ void finalize_row(const FinArgs &f, long i)
+// epilogue of row i given its joined sum(s)
+__device__ __forceinline__ void row_epilogue(const FinArgs &f, long i, double s, double s2)
 {
-    double s = strided_sum(f.rowpart + i, f.nstrips, f.M);
     if (f.rmode == kRowGesummv) {         // t1 = t0*alpha ; t3 = t2*beta ; y = t1 + t3
-        const double s2 = strided_sum(f.rowpart2 + i, f.nstrips, f.M);
         s = __dadd_rn(__dmul_rn(s, f.ralpha), __dmul_rn(s2, f.rbeta));
     } else if (f.rmode == kRowScale) {    // w = t5*alpha
         s = __dmul_rn(s, f.ralpha);
@@ -393,15 +394,54 @@ __device__ __forceinline__ void finalize_row(const FinArgs &f, long i)
     f.rowout[i] = s;
 }
 
+// Row side of the join for row CTA `rblock`.  One partial per strip and row: a square
+// matrix has 64 strips and a thread per row is right; a short, very wide one has thousands
+// (N / 512) and few rows, so a warp or the whole CTA shares a row -- thread k adds strips
+// k, k + G, .. in strided_sum order, then the fixed-order warp / CTA reduction.
+__device__ __forceinline__ void finalize_rows_cta(const FinArgs &f, long rblock)
+{
+    const bool two = f.rmode == kRowGesummv;
+    if (f.row_group <= 1) {
+        const long i = rblock * kThreads + threadIdx.x;
+        if (i < f.M) {
+            const double s = strided_sum(f.rowpart + i, f.nstrips, f.M);
+            const double s2 = two ? strided_sum(f.rowpart2 + i, f.nstrips, f.M) : 0.0;
+            row_epilogue(f, i, s, s2);
+        }
+        return;
+    }
+    const int G = f.row_group;
+    const int k = G == 32 ? (threadIdx.x & 31) : threadIdx.x;
+    const long i = G == 32 ? rblock * kWarps + (threadIdx.x >> 5) : rblock;
+    const bool live = i < f.M;                                    // uniform per warp (G = 32) / CTA
+    const long mine = live && k < f.nstrips ? (f.nstrips - k + G - 1) / G : 0;
+    double s = strided_sum(f.rowpart + (live ? i : 0) + (long)k * f.M, mine, (long)G * f.M);
+    double s2 = two ? strided_sum(f.rowpart2 + (live ? i : 0) + (long)k * f.M, mine, (long)G * f.M) : 0.0;
+    if (G == 32) {
+        s = warp_sum(s);
+        if (two) s2 = warp_sum(s2);
+        if (live && k == 0) row_epilogue(f, i, s, s2);
+    } else {
+        __shared__ double scratch[kWarps];
+        s = block_sum(s, scratch);
+        if (two) s2 = block_sum(s2, scratch);
+        if (live && threadIdx.x == 0) row_epilogue(f, i, s, s2);
+    }
+}
+
 __global__ void __launch_bounds__(kThreads)
 finalize_kernel(const FinArgs f)
 {
     wait_for_producer_grid();
     if ((int)blockIdx.x < f.col_blocks) {
-        join_columns_cta(f, (long)blockIdx.x * kJoinCols);
+        if (f.col_cols == kThreads) {
+            const long j = (long)blockIdx.x * kThreads + threadIdx.x;
+            if (j < f.N) f.colout[j] = column_epilogue(f, j, join_column(f, j));
+        } else {
+            join_columns_cta(f, (long)blockIdx.x * kJoinCols);
+        }
     } else {
-        const long i = (long)(blockIdx.x - f.col_blocks) * kThreads + threadIdx.x;
-        if (i < f.M) finalize_row(f, i);
+        finalize_rows_cta(f, (long)blockIdx.x - f.col_blocks);
     }
 }
 
@@ -462,8 +502,7 @@ join_exchange_kernel(const ExchArgs e)
     wait_for_producer_grid();
     const FinArgs &f = e.fin;
     if ((int)blockIdx.x >= kExchCtas) {          // row side: purely local
-        const long i = (long)(blockIdx.x - kExchCtas) * kThreads + threadIdx.x;
-        if (i < f.M) finalize_row(f, i);
+        finalize_rows_cta(f, (long)blockIdx.x - kExchCtas);
         return;
     }
     const int cta = blockIdx.x;

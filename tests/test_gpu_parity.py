@@ -383,6 +383,28 @@ def test_bench_size_cross_kernel_identities(bto_lib):
     assert _err(y, 0.75 * torch.mv(A, x)) <= 1e-12 * math.log2(m)
 
 
+@pytest.mark.parametrize("shape", [(3, 200001), (2, 2200000), (9, 70000), (300000, 6), (70001, 33), (1, 600000),
+                                   (500000, 1), (100000, 2), (40000, 64), (30011, 100), (20000, 255),
+                                   (20000, 256), (20000, 257), (5, 256), (77, 130), (9000, 17), (9000, 300), (8000, 511),
+                                   (8000, 512), (4000, 514), (3000, 390)])
+def test_extreme_aspect_ratios(bto_lib, oracle, shape):
+    """Short-wide matrices have thousands of column strips (the row-side join then shares a
+    row between a warp or a whole CTA); tall-skinny ones (N <= 256) take skinny_kernels.cuh,
+    where L threads share a row -- checked with that path on and off."""
+    m, n = shape
+    try:
+        for skinny in ((1, 0) if n <= 512 else (1,)):
+            _native.set_tuning(skinny=skinny)
+            for name in ("bicgk", "atax", "gesummv", "gemver", "dgemv", "dgemvt", "batax"):
+                ext = ext_of(name, m, n)
+                graph = bto.load_graph(name)
+                inputs = bto.random_inputs(graph, ext, seed=m % 13)
+                want = oracle.oracle_run(name, inputs, ext, threads=4)
+                assert_matches(name, run_device(name, inputs, ext), want, ext, f"aspect ratio, skinny={skinny}")
+    finally:
+        _native.set_tuning(skinny=1)
+
+
 def test_column_major_corpus_kernels_stay_fused(bto_lib, oracle):
     """`matrix(column)` operands: the same logical kernel, the
     buffers are F-ordered.  The library maps every corpus sequence onto its row-major fused
