@@ -132,6 +132,9 @@ int plan_mv(DeviceCtx &c, long M, long N, bool aligned, MvPlan *p)
     int V = g_tuning.mv_vec ? (int)g_tuning.mv_vec : dflt.vec;
     int minb = g_tuning.mv_minb ? (int)g_tuning.mv_minb : dflt.minb;
     if (!aligned || !mv_shape_ok<FLAGS>(R, V)) { R = 8; V = 1; }
+    // A ragged last strip takes the guarded (predicated) unit, which is slow for tall tiles; when
+    // it is a large share of the matrix (N = 1000: half of it) 8-row tiles win (GEMVER 3.9 -> 5.3 TB/s)
+    if (!g_tuning.mv_rows && R > 8 && N % ((long)kThreads * 2 * V) != 0 && N < 4L * kThreads * 2 * V) R = 8;
     p->R = R;
     p->V = V;
     p->aligned = aligned;
@@ -186,10 +189,18 @@ int launch_mv(const MvPlan &p, const MvArgs &a, cudaStream_t stream)
 // is fused into it (join_exchange_kernel); otherwise the plain local join runs.
 int launch_join(DeviceCtx &c, FinArgs f, cudaStream_t stream)
 {
-    // threads per row of the row-side join (finalize_rows_cta)
+    // threads per row of the row-side join: a thread (in the join kernel itself), or a warp /
+    // the whole CTA in finalize_rows_wide_kernel when a row has hundreds of strip partials
     f.row_group = f.nstrips <= 128 ? 1 : (f.nstrips <= 4096 ? 32 : kThreads);
-    const long rows_per_cta = kThreads / f.row_group;
-    const long rb = f.rmode != kRowNone ? (f.M + rows_per_cta - 1) / rows_per_cta : 0;
+    if (f.rmode != kRowNone && f.row_group > 1) {
+        const long rows_per_cta = kThreads / f.row_group;
+        const long rb = (f.M + rows_per_cta - 1) / rows_per_cta;
+        BTO_TRY(launch_dependent(finalize_rows_wide_kernel, (unsigned)rb, f, stream,
+                                 "finalize_rows_wide_kernel"));
+        f.rmode = kRowNone;
+        if (f.cmode == kColNone) return BTO_OK;
+    }
+    const long rb = f.rmode != kRowNone ? (f.M + kThreads - 1) / kThreads : 0;
     if (c.exch_active && f.cmode != kColNone) {
         if (2 * f.N > c.exch_capacity) {
             return fail(BTO_ERR_INVALID, "exchange buffer holds %ld doubles, need %ld",

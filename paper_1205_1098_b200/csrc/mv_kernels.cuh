@@ -70,16 +70,20 @@ __device__ __forceinline__ double2 mv_load(const double *base, long row, long N,
 // Per-thread view of the strip the CTA is walking down.
 template <int V>
 struct StripState {
-    long jcol[V];                     // first of the two columns of each double2
+    long jcol[V];                     // first of the two columns of each double2; 0 for a thread
+                                      // whose columns are outside the matrix (its loads stay
+                                      // unconditional and in bounds, the values are dropped)
     bool ok0[V], ok1[V];              // column j / j+1 inside the matrix
     double2 cw[V], cv1[V], cv2[V];    // colw, v1, v2 at those columns
     double2 csum[V];                  // running column sums (T-product)
 };
 
-// One unit = R rows of the strip.  INTERIOR units (all rows and the whole strip
-// inside the matrix) are predicate-free so every load is issued before the
-// first use; edge units are guarded.
-template <int FLAGS, int R, int V, bool ALIGNED, bool INTERIOR>
+// One unit = R rows of the strip.  INTERIOR units (all R rows inside the matrix)
+// load without predicates, so every load is issued before the first use -- in a
+// ragged last strip the threads beyond column N read column 0 instead and drop
+// the values; units that run past row M are guarded.
+// MODE: 0 guarded, 1 interior (rows and strip inside), 2 interior rows of a ragged strip
+template <int FLAGS, int R, int V, bool ALIGNED, int MODE>
 __device__ __forceinline__ void mv_unit(const MvArgs &a, StripState<V> &st, long r0,
                                         double (&rp)[R],
                                         double (&rp2)[(FLAGS & kFlagN2) ? R : 1])
@@ -88,7 +92,8 @@ __device__ __forceinline__ void mv_unit(const MvArgs &a, StripState<V> &st, long
     constexpr bool kN2 = (FLAGS & kFlagN2) != 0;
     constexpr bool kT = (FLAGS & kFlagT) != 0;
     constexpr bool kRank2 = (FLAGS & kFlagRank2) != 0;
-    constexpr bool kInterior = INTERIOR;
+    constexpr bool kInterior = MODE != 0;
+    constexpr bool kRagged = MODE == 2;
     const long M = a.M, N = a.N;
     long (&jcol)[V] = st.jcol;
     bool (&ok0)[V] = st.ok0;
@@ -112,6 +117,18 @@ __device__ __forceinline__ void mv_unit(const MvArgs &a, StripState<V> &st, long
                 if constexpr (kN2) {
                     t2[i][v] = mv_load<ALIGNED>(a.A2, r0 + i, N, jcol[v],
                                                 rv && ok0[v], rv && ok1[v]);
+                }
+            }
+        }
+    }
+    if constexpr (kRagged) {              // drop what the threads outside the matrix loaded
+#pragma unroll
+        for (int i = 0; i < R; ++i) {
+#pragma unroll
+            for (int v = 0; v < V; ++v) {
+                if (!ok0[v]) {
+                    t[i][v] = make_double2(0.0, 0.0);
+                    if constexpr (kN2) t2[i][v] = make_double2(0.0, 0.0);
                 }
             }
         }
@@ -142,7 +159,7 @@ __device__ __forceinline__ void mv_unit(const MvArgs &a, StripState<V> &st, long
                                 __dmul_rn(ru2[i], cv2[v].y));
                 double *dst = a.Bout + row * N + jcol[v];
                 if constexpr (ALIGNED) {
-                    if (kInterior || (rv && ok0[v])) st_stream2(dst, e);
+                    if (MODE == 1 || (rv && ok0[v])) st_stream2(dst, e);
                 } else {
                     if (rv && ok0[v]) st_stream1(dst, e.x);
                     if (rv && ok1[v]) st_stream1(dst + 1, e.y);
@@ -181,6 +198,11 @@ mv_tile_kernel(const MvArgs a)
     constexpr int kRowSets = kN2 ? 2 : 1;
     constexpr int kLanesPerRow = 32 / R;
     constexpr long kStripWidth = (long)kThreads * 2 * V;
+    // Ragged last strip, rows inside: unconditional loads with clamped columns (mv_unit MODE 2).
+    // Tall tiles only: their guarded unit is the slow one -- GEMVER pass 1 at N = 2500 ran at
+    // 3.8 TB/s, 5.8 with this; in the 8-row kernels the extra path costs more than it gives
+    // (GESUMMV spills at its 64-register budget, -2.5 %; BiCGK -0.6 % at bench size).
+    constexpr bool kRaggedMode = ALIGNED && !kN2 && R >= 16;
 
     __shared__ double red[2][kRowSets][kWarps][R];
 
@@ -228,7 +250,7 @@ mv_tile_kernel(const MvArgs a)
 #pragma unroll
             for (int v = 0; v < V; ++v) {
                 const long j = c * kStripWidth + (long)v * (kThreads * 2) + 2 * tid;
-                jcol[v] = j;
+                jcol[v] = (kRaggedMode && j >= N) ? 0 : j;
                 ok0[v] = j < N;
                 ok1[v] = j + 1 < N;
                 csum[v] = make_double2(0.0, 0.0);
@@ -250,9 +272,11 @@ mv_tile_kernel(const MvArgs a)
         // a predicate-free path so that every load of the unit is issued before
         // the first use; edge units take the guarded path.
         if (strip_inside && r0 + R <= M) {
-            mv_unit<FLAGS, R, V, ALIGNED, true>(a, st, r0, rp, rp2);
+            mv_unit<FLAGS, R, V, ALIGNED, 1>(a, st, r0, rp, rp2);
+        } else if (kRaggedMode && r0 + R <= M) {
+            mv_unit<FLAGS, R, V, ALIGNED, kRaggedMode ? 2 : 0>(a, st, r0, rp, rp2);
         } else {
-            mv_unit<FLAGS, R, V, ALIGNED, false>(a, st, r0, rp, rp2);
+            mv_unit<FLAGS, R, V, ALIGNED, 0>(a, st, r0, rp, rp2);
         }
 
         if constexpr (kN) {
@@ -398,34 +422,40 @@ __device__ __forceinline__ void row_epilogue(const FinArgs &f, long i, double s,
 // matrix has 64 strips and a thread per row is right; a short, very wide one has thousands
 // (N / 512) and few rows, so a warp or the whole CTA shares a row -- thread k adds strips
 // k, k + G, .. in strided_sum order, then the fixed-order warp / CTA reduction.
-__device__ __forceinline__ void finalize_rows_cta(const FinArgs &f, long rblock)
+// (its own kernel: the wide variant is the rare one and must not set the register count of the
+// join every square matrix runs)
+__global__ void __launch_bounds__(kThreads)
+finalize_rows_wide_kernel(const FinArgs f)
 {
+    wait_for_producer_grid();
+    const long rblock = blockIdx.x;
     const bool two = f.rmode == kRowGesummv;
-    if (f.row_group <= 1) {
-        const long i = rblock * kThreads + threadIdx.x;
-        if (i < f.M) {
-            const double s = strided_sum(f.rowpart + i, f.nstrips, f.M);
-            const double s2 = two ? strided_sum(f.rowpart2 + i, f.nstrips, f.M) : 0.0;
-            row_epilogue(f, i, s, s2);
-        }
-        return;
-    }
     const int G = f.row_group;
-    const int k = G == 32 ? (threadIdx.x & 31) : threadIdx.x;
+    const int k = G == 32 ? (int)(threadIdx.x & 31) : (int)threadIdx.x;
     const long i = G == 32 ? rblock * kWarps + (threadIdx.x >> 5) : rblock;
     const bool live = i < f.M;                                    // uniform per warp (G = 32) / CTA
     const long mine = live && k < f.nstrips ? (f.nstrips - k + G - 1) / G : 0;
-    double s = strided_sum(f.rowpart + (live ? i : 0) + (long)k * f.M, mine, (long)G * f.M);
-    double s2 = two ? strided_sum(f.rowpart2 + (live ? i : 0) + (long)k * f.M, mine, (long)G * f.M) : 0.0;
+    const long first = (live ? i : 0) + (long)k * f.M;
+    double s = strided_sum(f.rowpart + first, mine, (long)G * f.M);
+    double s2 = two ? strided_sum(f.rowpart2 + first, mine, (long)G * f.M) : 0.0;
     if (G == 32) {
         s = warp_sum(s);
         if (two) s2 = warp_sum(s2);
-        if (live && k == 0) row_epilogue(f, i, s, s2);
     } else {
         __shared__ double scratch[kWarps];
         s = block_sum(s, scratch);
         if (two) s2 = block_sum(s2, scratch);
-        if (live && threadIdx.x == 0) row_epilogue(f, i, s, s2);
+    }
+    if (live && k == 0) row_epilogue(f, i, s, s2);
+}
+
+__device__ __forceinline__ void finalize_rows_cta(const FinArgs &f, long rblock)
+{
+    const long i = rblock * kThreads + threadIdx.x;
+    if (i < f.M) {
+        const double s = strided_sum(f.rowpart + i, f.nstrips, f.M);
+        const double s2 = f.rmode == kRowGesummv ? strided_sum(f.rowpart2 + i, f.nstrips, f.M) : 0.0;
+        row_epilogue(f, i, s, s2);
     }
 }
 
