@@ -580,8 +580,9 @@ def test_cuda_graph_capture_and_replay(bto_lib, oracle):
     assert_matches("gemver", got, want, {"M": m, "N": n}, "graph replay")
 
 
+@pytest.mark.parametrize("shape", [(1030, 2050), (4001, 130)], ids=["tiles", "shared-rows"])
 @pytest.mark.parametrize("world", [2, 3, 8])
-def test_join_fused_exchange_emulated_ranks(bto_lib, oracle, world):
+def test_join_fused_exchange_emulated_ranks(bto_lib, oracle, world, shape):
     """The join kernel that does the cross-GPU all-reduce itself (peer-memory one-shot,
     include/bto_b200.h 3b), with ONE GPU standing in for all ranks: the exchange
     buffers and flag arrays of every "rank" live on this device; first every rank
@@ -594,7 +595,7 @@ def test_join_fused_exchange_emulated_ranks(bto_lib, oracle, world):
     from paper_1205_1098_b200.sharded import GpuShardOps, row_block, shard_inputs
     lib = _native.load()
     ops = GpuShardOps()
-    m, n = 1030, 2050
+    m, n = shape
     capacity = 2 * max(m, n)
     exch = [torch.zeros(capacity, dtype=torch.float64, device="cuda") for _ in range(world)]
     flags = [torch.zeros(lib.bto_exchange_flag_bytes(world) // 4, dtype=torch.int32, device="cuda")
