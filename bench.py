@@ -506,9 +506,15 @@ def main() -> int:
                     help="N > 1: NCCL all-reduce after the join, or the exchange fused into the join")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--tune", action="append", default=[], metavar="KEY=VALUE",
+                    help="experiments only: a bto_set_tuning key (include/bto_b200.h section 4)")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference_arm(args)
+    for kv in args.tune:
+        from paper_1205_1098_b200 import _native
+        key, value = kv.split("=")
+        _native.set_tuning(**{key: int(value)})
     return run_gpu_arm(args)
 
 
