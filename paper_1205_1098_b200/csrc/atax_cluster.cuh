@@ -319,7 +319,7 @@ atax_cluster_kernel(const AtaxArgs a)
 #pragma unroll
         for (int k = 0; k < KMAX; ++k) {
             const int j = 2 * tid + 2 * kThreads * k;
-            if (j < wlen) *reinterpret_cast<double2 *>(dst + j) = ysum[k];
+            if (j < wlen) st_partial2(dst + j, ysum[k]);
         }
     }
     __syncwarp();

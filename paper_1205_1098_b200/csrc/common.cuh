@@ -18,29 +18,34 @@ constexpr int kWarps = kThreads / 32;
 constexpr unsigned kFullMask = 0xffffffffu;
 
 // ---- streaming global loads / stores ---------------------------------------
-// .nc + L1::no_allocate: read-once data must not evict the small vectors
-// (weights, x) that do get re-used from L1.
-#ifndef BTO_LOAD_POLICY
-#define BTO_LOAD_POLICY 0
-#endif
+// Read-once operands come through the non-coherent path.  BYPASS_L1 adds
+// L1::no_allocate, which keeps them from evicting the small vectors (weights, x)
+// that are re-used from L1 -- but measured on B200 it makes a streaming kernel
+// bistable: AXPYDOT runs at 7.0 TB/s until any other large kernel has run, then at
+// 6.3 TB/s for good (profiles/r01/axpydot_state_probe.log); with plain .nc loads it
+// stays at 7.0, BiCGK and GEMVER gain 1-2 %, only the two-matrix GESUMMV pass is
+// faster (3 %) with the bypass.  So the bypass is a per-kernel choice.
+template <bool BYPASS_L1 = false>
 __device__ __forceinline__ double2 ld_stream2(const double *p)   // 16 B aligned
 {
     double2 v;
-#if BTO_LOAD_POLICY == 0
-    asm("ld.global.nc.L1::no_allocate.v2.f64 {%0, %1}, [%2];"
-#elif BTO_LOAD_POLICY == 1
-    asm("ld.global.nc.L1::no_allocate.L2::evict_first.v2.f64 {%0, %1}, [%2];"
-#else
-    asm("ld.global.nc.v2.f64 {%0, %1}, [%2];"
-#endif
-        : "=d"(v.x), "=d"(v.y) : "l"(p));
+    if constexpr (BYPASS_L1) {
+        asm("ld.global.nc.L1::no_allocate.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "l"(p));
+    } else {
+        asm("ld.global.nc.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "l"(p));
+    }
     return v;
 }
 
+template <bool BYPASS_L1 = false>
 __device__ __forceinline__ double ld_stream1(const double *p)
 {
     double v;
-    asm("ld.global.nc.L1::no_allocate.f64 %0, [%1];" : "=d"(v) : "l"(p));
+    if constexpr (BYPASS_L1) {
+        asm("ld.global.nc.L1::no_allocate.f64 %0, [%1];" : "=d"(v) : "l"(p));
+    } else {
+        asm("ld.global.nc.f64 %0, [%1];" : "=d"(v) : "l"(p));
+    }
     return v;
 }
 
@@ -61,6 +66,33 @@ __device__ __forceinline__ void st_stream2(double *p, double2 v)   // 16 B align
     asm volatile("st.global.cg.v2.f64 [%0], {%1, %2};"
 #endif
                  :: "l"(p), "d"(v.x), "d"(v.y) : "memory");
+}
+
+// Stores of partial results (workspace rows the join kernel reads next) and of the small
+// result vectors.  BTO_PARTIAL_POLICY: 0 = default write-back, 1 = .wt (write-through: the
+// line stays in L2 for the join but is clean), 2 = .cs
+#ifndef BTO_PARTIAL_POLICY
+#define BTO_PARTIAL_POLICY 0
+#endif
+__device__ __forceinline__ void st_partial1(double *p, double v)
+{
+#if BTO_PARTIAL_POLICY == 1
+    asm volatile("st.global.wt.f64 [%0], %1;" :: "l"(p), "d"(v) : "memory");
+#elif BTO_PARTIAL_POLICY == 2
+    asm volatile("st.global.cs.f64 [%0], %1;" :: "l"(p), "d"(v) : "memory");
+#else
+    *p = v;
+#endif
+}
+__device__ __forceinline__ void st_partial2(double *p, double2 v)   // 16 B aligned
+{
+#if BTO_PARTIAL_POLICY == 1
+    asm volatile("st.global.wt.v2.f64 [%0], {%1, %2};" :: "l"(p), "d"(v.x), "d"(v.y) : "memory");
+#elif BTO_PARTIAL_POLICY == 2
+    asm volatile("st.global.cs.v2.f64 [%0], {%1, %2};" :: "l"(p), "d"(v.x), "d"(v.y) : "memory");
+#else
+    *reinterpret_cast<double2 *>(p) = v;
+#endif
 }
 
 __device__ __forceinline__ void st_stream1(double *p, double v)

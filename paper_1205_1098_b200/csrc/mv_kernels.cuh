@@ -53,17 +53,17 @@ struct MvArgs {
     int nstrips;
 };
 
-template <bool ALIGNED>
+template <bool ALIGNED, bool BYPASS_L1>
 __device__ __forceinline__ double2 mv_load(const double *base, long row, long N,
                                            long j, bool ok0, bool ok1)
 {
     const double *p = base + row * N + j;
     if constexpr (ALIGNED) {
-        return ok0 ? ld_stream2(p) : make_double2(0.0, 0.0);
+        return ok0 ? ld_stream2<BYPASS_L1>(p) : make_double2(0.0, 0.0);
     }
     double2 v;
-    v.x = ok0 ? ld_stream1(p) : 0.0;
-    v.y = ok1 ? ld_stream1(p + 1) : 0.0;
+    v.x = ok0 ? ld_stream1<BYPASS_L1>(p) : 0.0;
+    v.y = ok1 ? ld_stream1<BYPASS_L1>(p + 1) : 0.0;
     return v;
 }
 
@@ -92,6 +92,7 @@ __device__ __forceinline__ void mv_unit(const MvArgs &a, StripState<V> &st, long
     constexpr bool kN2 = (FLAGS & kFlagN2) != 0;
     constexpr bool kT = (FLAGS & kFlagT) != 0;
     constexpr bool kRank2 = (FLAGS & kFlagRank2) != 0;
+    constexpr bool kBypass = kN2;        // L1 bypass only for the two-matrix pass (common.cuh)
     constexpr bool kInterior = MODE != 0;
     constexpr bool kRagged = MODE == 2;
     const long M = a.M, N = a.N;
@@ -109,13 +110,13 @@ __device__ __forceinline__ void mv_unit(const MvArgs &a, StripState<V> &st, long
 #pragma unroll
         for (int v = 0; v < V; ++v) {
             if constexpr (kInterior && ALIGNED) {
-                t[i][v] = ld_stream2(a.A + (r0 + i) * N + jcol[v]);
-                if constexpr (kN2) t2[i][v] = ld_stream2(a.A2 + (r0 + i) * N + jcol[v]);
+                t[i][v] = ld_stream2<kBypass>(a.A + (r0 + i) * N + jcol[v]);
+                if constexpr (kN2) t2[i][v] = ld_stream2<kBypass>(a.A2 + (r0 + i) * N + jcol[v]);
             } else {
-                t[i][v] = mv_load<ALIGNED>(a.A, r0 + i, N, jcol[v],
+                t[i][v] = mv_load<ALIGNED, kBypass>(a.A, r0 + i, N, jcol[v],
                                            rv && ok0[v], rv && ok1[v]);
                 if constexpr (kN2) {
-                    t2[i][v] = mv_load<ALIGNED>(a.A2, r0 + i, N, jcol[v],
+                    t2[i][v] = mv_load<ALIGNED, kBypass>(a.A2, r0 + i, N, jcol[v],
                                                 rv && ok0[v], rv && ok1[v]);
                 }
             }
@@ -232,10 +233,10 @@ mv_tile_kernel(const MvArgs a)
 #pragma unroll
         for (int v = 0; v < V; ++v) {
             if constexpr (ALIGNED) {
-                if (ok0[v]) *reinterpret_cast<double2 *>(dst + jcol[v]) = csum[v];
+                if (ok0[v]) st_partial2(dst + jcol[v], csum[v]);
             } else {
-                if (ok0[v]) dst[jcol[v]] = csum[v].x;
-                if (ok1[v]) dst[jcol[v] + 1] = csum[v].y;
+                if (ok0[v]) st_partial1(dst + jcol[v], csum[v].x);
+                if (ok1[v]) st_partial1(dst + jcol[v] + 1, csum[v].y);
             }
         }
     };
@@ -296,7 +297,7 @@ mv_tile_kernel(const MvArgs a)
                 for (int w = 1; w < kWarps; ++w) s += red[buf][set][w][i];
                 if (r0 + i < M) {
                     double *dst = set == 1 ? a.rowpart2 : a.rowpart;
-                    dst[strip * M + r0 + i] = s;
+                    st_partial1(dst + strip * M + r0 + i, s);
                 }
             }
             // red[] is double-buffered: the next unit writes the other half and
@@ -401,7 +402,7 @@ __device__ __forceinline__ void join_columns_cta(const FinArgs &f, long j0)
                           (warp_part[2][lane] + warp_part[3][lane])) +
                          ((warp_part[4][lane] + warp_part[5][lane]) +
                           (warp_part[6][lane] + warp_part[7][lane]));
-        f.colout[j] = column_epilogue(f, j, s);
+        st_partial1(f.colout + j, column_epilogue(f, j, s));
     }
 }
 
@@ -415,7 +416,7 @@ __device__ __forceinline__ void row_epilogue(const FinArgs &f, long i, double s,
     } else if (f.rmode == kRowDgemv) {    // t1 = t0*alpha ; t2 = y*beta ; z = t1 + t2
         s = __dadd_rn(__dmul_rn(s, f.ralpha), __dmul_rn(f.rowy[i], f.rbeta));
     }
-    f.rowout[i] = s;
+    st_partial1(f.rowout + i, s);
 }
 
 // Row side of the join for row CTA `rblock`.  One partial per strip and row: a square
@@ -466,7 +467,7 @@ finalize_kernel(const FinArgs f)
     if ((int)blockIdx.x < f.col_blocks) {
         if (f.col_cols == kThreads) {
             const long j = (long)blockIdx.x * kThreads + threadIdx.x;
-            if (j < f.N) f.colout[j] = column_epilogue(f, j, join_column(f, j));
+            if (j < f.N) st_partial1(f.colout + j, column_epilogue(f, j, join_column(f, j)));
         } else {
             join_columns_cta(f, (long)blockIdx.x * kJoinCols);
         }

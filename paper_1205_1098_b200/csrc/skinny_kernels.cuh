@@ -48,6 +48,7 @@ mv_skinny_kernel(const SkinnyArgs s)
     static_assert(V == 1 || V == 2 || V == 4 || V == 8, "slots per thread");
     constexpr int R = kSkinnyRows / V;
     constexpr int W = PAIR ? 2 : 1;
+    // loads bypass L1 here (measured: 4M x 32 BiCGK 4.8 TB/s with the bypass, 4.4 without)
 
     __shared__ double fold[V][kThreads][2];
 
@@ -93,14 +94,14 @@ mv_skinny_kernel(const SkinnyArgs s)
                 const bool ld = rv && ok0[v];
                 const double *p = a.A + row * N + col[v];
                 if constexpr (PAIR) {
-                    e[i][v] = ld ? ld_stream2(p) : make_double2(0.0, 0.0);
+                    e[i][v] = ld ? ld_stream2<true>(p) : make_double2(0.0, 0.0);
                     if constexpr (kN2) {
-                        e2[i][v] = ld ? ld_stream2(a.A2 + row * N + col[v]) : make_double2(0.0, 0.0);
+                        e2[i][v] = ld ? ld_stream2<true>(a.A2 + row * N + col[v]) : make_double2(0.0, 0.0);
                     }
                 } else {
-                    e[i][v] = make_double2(ld ? ld_stream1(p) : 0.0, 0.0);
+                    e[i][v] = make_double2(ld ? ld_stream1<true>(p) : 0.0, 0.0);
                     if constexpr (kN2) {
-                        e2[i][v] = make_double2(ld ? ld_stream1(a.A2 + row * N + col[v]) : 0.0, 0.0);
+                        e2[i][v] = make_double2(ld ? ld_stream1<true>(a.A2 + row * N + col[v]) : 0.0, 0.0);
                     }
                 }
             }
@@ -196,8 +197,8 @@ mv_skinny_kernel(const SkinnyArgs s)
                     t1 += fold[v][gg * L + cp][1];
                 }
                 double *dst = a.colpart + (long)blockIdx.x * N + col[v];
-                if (ok0[v]) dst[0] = t0;
-                if (ok1[v]) dst[1] = t1;
+                if (ok0[v]) st_partial1(dst, t0);
+                if (ok1[v]) st_partial1(dst + 1, t1);
             }
         }
     }
