@@ -91,13 +91,32 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity)
 }
 
 // TMA 1-D bulk copy global -> shared, completion counted in bytes on `bar`
+// BTO_TMA_POLICY: 0 = no L2 hint, 1 = evict_first, 2 = evict_last, 3 = evict_normal (explicit)
+#ifndef BTO_TMA_POLICY
+#define BTO_TMA_POLICY 0
+#endif
 __device__ __forceinline__ void bulk_load(void *dst, const void *src, uint32_t bytes,
                                           uint64_t *bar)
 {
+#if BTO_TMA_POLICY == 0
     asm volatile(
         "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
         ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar))
         : "memory");
+#else
+    uint64_t policy;
+#if BTO_TMA_POLICY == 1
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(policy));
+#elif BTO_TMA_POLICY == 2
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(policy));
+#else
+    asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(policy));
+#endif
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;"
+        ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(policy)
+        : "memory");
+#endif
 }
 
 __device__ __forceinline__ void mbar_arrive(uint64_t *bar)

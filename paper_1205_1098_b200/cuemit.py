@@ -174,15 +174,16 @@ JAM = 4                       # rows of an outer loop processed together (unroll
 # Launch-shape variants an empirical timer may try per organism (B200 sweep at n = 8192,
 # profiles/r01/emit_sweep.md): the first is the default of emit_cuda.
 EMIT_VARIANTS = ({"jam": 4, "unroll": 4, "minb": 2}, {"jam": 2, "unroll": 4, "minb": 2},
-                 {"jam": 8, "unroll": 2, "minb": 2})
+                 {"jam": 8, "unroll": 2, "minb": 2}, {"jam": 4, "unroll": 4, "minb": 2, "bypass_l1": 0})
 SMEM_ACC_BYTES = 192 * 1024   # per-CTA budget for block partials promoted to shared memory
 JOIN_COLS = 32                # columns per CTA of a join kernel
 
 
 class _Emitter:
     def __init__(self, ir: dict, blocks: int, optimize: bool = True, jam: int = JAM,
-                 unroll: int = 4, threads: int = CTA_THREADS, minb: int = 2):
+                 unroll: int = 4, threads: int = CTA_THREADS, minb: int = 2, bypass_l1: int = 1):
         self.jam, self.unroll, self.threads, self.minb = int(jam), int(unroll), int(threads), int(minb)
+        self.bypass_l1 = bool(bypass_l1)
         self.ir = ir
         self.st = ir["storage"]
         self.ops = ir["ops"]
@@ -492,7 +493,7 @@ class _Emitter:
     def load_of(self, name: str, loop: dict) -> str:
         """Batched load of a read-only operand: 2-D operands pass once (no L1 allocation),
         vectors are reused by the next rows and stay cached."""
-        once = len(self.st[name]["labels"]) == 2
+        once = len(self.st[name]["labels"]) == 2 and self.bypass_l1
         return f"{'ld_stream' if once else 'ld_keep'}(&{self.ref(name)})"
 
     def emit_batched_lane(self, loop: dict, block: str | None, in_region: bool, rows):
@@ -911,7 +912,8 @@ def emit_cuda(ir: dict, blocks: int = DEFAULT_BLOCKS, optimize: bool = True, **t
     `optimize=False` prints the plain mapping only (every barrier, no unroll-and-jam, block
     partials accumulated in global memory).  `tune`: jam (rows per batch), unroll (of the
     strided loop under a batch), threads (per CTA of a parallel region), minb (CTAs per SM the
-    register budget is sized for)."""
+    register budget is sized for), bypass_l1 (0: 2-D operands are loaded L1-allocating; ATAX-like
+    bodies that read a row twice gain 10 %)."""
     em = _Emitter(ir, int(blocks), bool(optimize), **tune)
     source = em.emit()
     params = []

@@ -15,6 +15,13 @@ for name in bto.HOT_PATH:
     fused = cost.measure_empirical(cost.GpuVariant(name), typed, ext, reps=5)
     emitted = cuemit.measure_empirical_ir(irs[name][0], typed, ext, reps=3)
     plain = cuemit.measure_empirical_ir(irs[name][0], typed, ext, reps=3, optimize=False)
+    import tempfile
+    k2 = cuemit.emit_cuda(irs[name][0], bypass_l1=0)
+    lib2 = cuemit.NvccToolchain().compile(k2.source, tempfile.mkdtemp(), name="nobypass")
+    inputs = bto.gen_inputs(typed, ext, seed=7)
+    dev = {k: (torch.from_numpy(v).cuda() if hasattr(v, "shape") else v) for k, v in inputs.items()}
+    t2 = cuemit.time_emitted(lib2, k2, irs[name][0], dev, ext, reps=3)
+    print(f"{name:8s} emitted with L1-allocating loads: {t2*1e3:8.3f} ms", flush=True)
     unf = cuemit.measure_empirical_ir(irs[name][1], typed, ext, reps=1)
     nbytes = bto._native.bytes_min(name, ext["M"], ext.get("N", 1))
     print(f"{name:8s} n={n}: hand-written {fused.total*1e3:8.3f} ms ({nbytes/fused.total/1e9:6.0f} GB/s)   "
