@@ -8,6 +8,8 @@
 #include <map>
 #include <mutex>
 #include <thread>
+#include <deque>
+#include <atomic>
 #include <condition_variable>
 #if defined(__SSE2__)
 #include <emmintrin.h>

@@ -94,22 +94,91 @@ void stream_copy(char *dst, const char *src, size_t bytes)
     memcpy(dst, src, bytes);
 }
 
+// Persistent helpers for the bounce copies (a thread per piece and call cost ~0.5 ms of thread
+// creation per 64 MiB chunk, a third of the chunk's copy time).  Pieces of concurrent calls
+// (GEMVER fills inbound slots while its helper drains outbound ones) share one queue; a caller
+// works on the queue too until its own pieces are done.  The pool is created on first use and
+// never destroyed (its threads sleep on a condition variable and die with the process).
+class CopyPool {
+public:
+    static CopyPool &get()
+    {
+        static CopyPool *pool = new CopyPool();
+        return *pool;
+    }
+
+    void copy(char *dst, const char *src, size_t bytes, int nt)
+    {
+        const size_t piece = ((bytes / nt) + 4095) & ~size_t(4095);
+        std::atomic<int> left{0};
+        {
+            std::lock_guard<std::mutex> g(mu_);
+            for (size_t lo = 0; lo < bytes; lo += piece) {
+                const size_t len = lo + piece < bytes ? piece : bytes - lo;
+                queue_.push_back({dst + lo, src + lo, len, &left});
+                left.fetch_add(1, std::memory_order_relaxed);
+            }
+            while ((int)workers_ < nt - 1) {
+                std::thread([this] { serve(); }).detach();
+                ++workers_;
+            }
+        }
+        cv_.notify_all();
+        while (left.load(std::memory_order_acquire) > 0) {
+            Piece p;
+            if (take(&p)) {
+                run(p);
+            } else {
+                std::this_thread::yield();       // the last pieces are in other threads' hands
+            }
+        }
+    }
+
+private:
+    struct Piece { char *dst; const char *src; size_t len; std::atomic<int> *left; };
+
+    bool take(Piece *p)
+    {
+        std::lock_guard<std::mutex> g(mu_);
+        if (queue_.empty()) return false;
+        *p = queue_.front();
+        queue_.pop_front();
+        return true;
+    }
+
+    static void run(const Piece &p)
+    {
+        stream_copy(p.dst, p.src, p.len);
+        p.left->fetch_sub(1, std::memory_order_release);
+    }
+
+    void serve()
+    {
+        for (;;) {
+            Piece p;
+            {
+                std::unique_lock<std::mutex> g(mu_);
+                cv_.wait(g, [this] { return !queue_.empty(); });
+                p = queue_.front();
+                queue_.pop_front();
+            }
+            run(p);
+        }
+    }
+
+    std::mutex mu_;
+    std::condition_variable cv_;
+    std::deque<Piece> queue_;
+    size_t workers_ = 0;
+};
+
 void parallel_memcpy(char *dst, const char *src, size_t bytes, int nt)
 {
     if (nt <= 1 || bytes < (4u << 20)) {
         stream_copy(dst, src, bytes);
         return;
     }
-    std::vector<std::thread> pool;
-    const size_t piece = ((bytes / nt) + 4095) & ~size_t(4095);
-    for (int t = 1; t < nt; ++t) {
-        const size_t lo = piece * t;
-        if (lo >= bytes) break;
-        const size_t len = lo + piece < bytes ? piece : bytes - lo;
-        pool.emplace_back([=] { stream_copy(dst + lo, src + lo, len); });
-    }
-    stream_copy(dst, src, piece < bytes ? piece : bytes);
-    for (std::thread &th : pool) th.join();
+    CopyPool::get().copy(dst, src, bytes, nt);
 }
 
 // host (pageable) -> device, enqueued on `s`; returns once `src` has been read.
