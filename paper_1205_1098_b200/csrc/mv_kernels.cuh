@@ -92,7 +92,10 @@ __device__ __forceinline__ void mv_unit(const MvArgs &a, StripState<V> &st, long
     constexpr bool kN2 = (FLAGS & kFlagN2) != 0;
     constexpr bool kT = (FLAGS & kFlagT) != 0;
     constexpr bool kRank2 = (FLAGS & kFlagRank2) != 0;
-    constexpr bool kBypass = kN2;        // L1 bypass only for the two-matrix pass (common.cuh)
+#ifndef BTO_N2_BYPASS
+#define BTO_N2_BYPASS 1
+#endif
+    constexpr bool kBypass = kN2 && BTO_N2_BYPASS;   // L1 bypass only for the two-matrix pass (common.cuh)
     constexpr bool kInterior = MODE != 0;
     constexpr bool kRagged = MODE == 2;
     const long M = a.M, N = a.N;
