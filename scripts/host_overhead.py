@@ -14,6 +14,7 @@ x = [torch.rand(n, dtype=torch.float64, device="cuda") for _ in range(4)]
 A = torch.rand(256, 512, dtype=torch.float64, device="cuda")
 st = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
 P = lambda t: ctypes.c_void_p(t.data_ptr())
+B_ = torch.empty_like(A); xo = torch.empty(512, dtype=torch.float64, device="cuda"); wo = torch.empty(256, dtype=torch.float64, device="cuda")
 def bench(label, fn, reps=3000):
     for _ in range(50): fn()
     torch.cuda.synchronize(); t0 = time.perf_counter()
@@ -28,3 +29,9 @@ a, b, c, d = P(x[0]), P(x[1]), P(x[2]), P(x[3])
 bench("raw bto_vadd_async (args cached)", lambda: lib.bto_vadd_async(a, b, c, d, n, st))
 bench("ops.bicgk 256x512 (2 kernels)", lambda: ops.bicgk(A, x[0][:512], x[1][:256], x[2][:256], x[3][:512]))
 bench("ops.atax 256x512 (2 kernels)", lambda: ops.atax(A, x[0][:512], x[3][:512]))
+f = ops.bind("bicgk", A, x[0][:512], x[1][:256], x[2][:256], x[3][:512])
+bench("ops.bind('bicgk') 256x512 (2 kernels)", f)
+g = ops.bind("gemver", A, x[1][:256], x[0][:512], x[1][:256], x[0][:512], 0.5, 0.25, x[2][:256], x[3][:512],
+             torch.empty_like(A), torch.empty(512, dtype=torch.float64, device="cuda"), torch.empty(256, dtype=torch.float64, device="cuda"))
+bench("ops.bind('gemver') 256x512", g)
+bench("ops.gemver 256x512", lambda: ops.gemver(A, x[1][:256], x[0][:512], x[1][:256], x[0][:512], 0.5, 0.25, x[2][:256], x[3][:512], B_, xo, wo))
