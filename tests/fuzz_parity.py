@@ -1,0 +1,56 @@
+#!/usr/bin/env python
+"""Randomised differential test: every corpus kernel, random extents (biased to strip / tile
+edges), random launch tunables, device and host operands, against the CPU oracle.
+   fuzz_parity.py [seconds] [seed]"""
+import math, random, sys, time
+from pathlib import Path
+import numpy as np
+import torch
+REPO = Path(__file__).resolve().parent.parent
+sys.path.insert(0, str(REPO)); sys.path.insert(0, str(REPO / "tests"))   # test infrastructure: may use the oracle
+import paper_1205_1098_b200 as bto
+from paper_1205_1098_b200 import _native
+import oracle_lib
+budget = float(sys.argv[1]) if len(sys.argv) > 1 else 60.0
+rng = random.Random(int(sys.argv[2]) if len(sys.argv) > 2 else 0)
+oracle = oracle_lib.load_oracle() if hasattr(oracle_lib, "load_oracle") else oracle_lib
+ELEMENTWISE = {"axpydot": ("z",), "vadd": ("x",), "waxpby": ("w",), "gemver": ("B",)}
+def extent():
+    r = rng.random()
+    if r < 0.25: return rng.choice([1, 2, 3, 7, 8, 9, 15, 16, 17, 31, 32, 33, 63, 64, 65])
+    if r < 0.5: return max(1, rng.choice([256, 512, 1024, 1536, 2048]) + rng.randint(-3, 3))
+    if r < 0.9: return rng.randint(1, 3000)
+    return rng.randint(3000, 20000)
+t_end = time.time() + budget
+cases = fails = 0
+while time.time() < t_end:
+    name = rng.choice(sorted(bto.CORPUS))
+    g = bto.load_graph(name)
+    m, n = extent(), extent()
+    if m * n > 3e7: n = max(1, int(3e7 // m))
+    ext = {"M": m * n} if g.extent_names == ("M",) else {"M": m, "N": n}
+    tune = dict(mv_rows=rng.choice([0, 0, 8, 16, 32]), mv_vec=rng.choice([0, 0, 1, 2]),
+                grid_per_sm=rng.choice([0, 0, 1, 2, 4, 8]), mv_minb=rng.choice([0, 0, 1, 2, 4]),
+                skinny=rng.choice([1, 1, 0]), vec_unroll=rng.choice([1, 2, 4]), atax_fused=rng.choice([1, 1, 0]))
+    _native.set_tuning(**tune)
+    inputs = bto.random_inputs(g, ext, seed=cases)
+    want = oracle.oracle_run(name, inputs, ext, threads=rng.choice([1, 4, 8]))
+    host = rng.random() < 0.3
+    if host:
+        got = bto.run_kernel(bto.library_path(), bto.gpu_kernel(g), g, inputs, ext)
+    else:
+        dev = {k: (torch.from_numpy(np.ascontiguousarray(v)).cuda() if isinstance(v, np.ndarray) else v) for k, v in inputs.items()}
+        got = bto.run_kernel(bto.library_path(), bto.gpu_kernel(g), g, dev, ext)
+        got = {k: (v.cpu().numpy() if hasattr(v, "cpu") else v) for k, v in got.items()}
+    err = bto.max_rel_error(got, want)
+    tol = 1e-12 * max(1.0, math.log2(max(ext.values())))
+    bad = not (err <= tol) or any(np.any(np.isnan(np.asarray(got[o]))) for o in want)
+    for o in ELEMENTWISE.get(name, ()):
+        bad = bad or not np.array_equal(np.asarray(got[o]), np.asarray(want[o]))
+    cases += 1
+    if bad:
+        fails += 1
+        print("MISMATCH", name, ext, tune, "host" if host else "device", f"err={err:.3e}", flush=True)
+_native.set_tuning(mv_rows=0, mv_vec=0, grid_per_sm=0, mv_minb=0, skinny=1, vec_unroll=2, atax_fused=1)
+print(f"{cases} cases, {fails} mismatches")
+sys.exit(1 if fails else 0)

@@ -580,6 +580,17 @@ def test_cuda_graph_capture_and_replay(bto_lib, oracle):
     assert_matches("gemver", got, want, {"M": m, "N": n}, "graph replay")
 
 
+def test_randomised_differential_run(bto_lib, oracle):
+    """20 s of tests/fuzz_parity.py: random kernels, extents biased to tile / strip edges, random
+    launch tunables, host and device operands, all against the oracle."""
+    import subprocess, sys
+    from pathlib import Path
+    script = Path(__file__).with_name("fuzz_parity.py")
+    proc = subprocess.run([sys.executable, str(script), "20", "1205"], capture_output=True, text=True, timeout=300)
+    assert proc.returncode == 0, proc.stdout[-2000:] + proc.stderr[-2000:]
+    assert " 0 mismatches" in proc.stdout
+
+
 def test_bound_calls_replay(bto_lib, oracle):
     """GpuShardOps.bind pre-marshals a call; replaying it on new data in the same buffers gives
     the results of a fresh call."""
