@@ -282,7 +282,7 @@ SkinnyPlan plan_skinny(DeviceCtx &c, long M, long N, bool aligned)
     if (!p.pair && p.V == 2) p.V = 4;                             // (singles are built for V = 1, 4, 8)
     p.L = 1;
     while ((long)p.L * p.V < width) p.L *= 2;
-    const long unit = (long)(kSkinnyRows / p.V) * (kThreads / p.L);   // rows one CTA covers per step
+    const long unit = (long)skinny_rows(p.V) * (kThreads / p.L);      // rows one CTA covers per step
     const long per_sm = g_tuning.grid_per_sm > 0 ? g_tuning.grid_per_sm : 4;
     const long target = (long)c.sm_count * per_sm;
     long rows = (M + target - 1) / target;

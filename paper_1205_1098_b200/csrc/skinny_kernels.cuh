@@ -19,19 +19,22 @@ namespace bto {
 
 enum : int { kFlagAtax = 16 };
 constexpr long kSkinnyMaxN = 512;
-constexpr int kSkinnyRows = 8;            // rows per thread and unit
+// Rows per thread and unit for V column slots: 8 loads per matrix in flight, 16 for V = 2, 4
+// (measured: GEMVER 1M x 256 4.8 -> 5.8 TB/s, 2M x 100 4.3 -> 4.8; with V = 1 the wider unit
+// spills, with V = 8 it is slower)
+__host__ __device__ constexpr int skinny_rows(int V) { return ((V == 2 || V == 4) ? 16 : 8) / V; }
 
 struct SkinnyArgs {
     MvArgs mv;                // operands; colpart is [grid][N]
     FinArgs fin;              // row epilogue (rmode, ralpha, rbeta, rowy, rowout)
     int L;                    // threads per row (power of two, <= 32: a row never leaves its warp)
-    long rows_per_cta;        // multiple of (8 / V) * (kThreads / L)
+    long rows_per_cta;        // multiple of skinny_rows(V) * (kThreads / L)
 };
 
 // V slots per thread and row: slot v of thread cp holds column(s) (cp + L*v) * W, W = 2 (PAIR:
 // double2 loads, N even and 16-byte aligned operands) or 1.  V = 1 covers N <= 32*W, larger V
-// (then L = 32) up to N = 512; rows per thread and step shrink with V so that a thread always has
-// 8 loads per matrix in flight.
+// (then L = 32) up to N = 512; rows per thread and step shrink with V (skinny_rows) so that a
+// thread has 8 or 16 loads per matrix in flight.
 // (eight slots of a rank-2 pass spill ~100 bytes at 128 registers; one CTA per SM instead was
 // measured slower, 4.4 vs 4.8 TB/s at N = 500)
 template <int FLAGS, bool PAIR, int V>
@@ -46,7 +49,7 @@ mv_skinny_kernel(const SkinnyArgs s)
     static_assert(!kN2 || kN, "the second N-product rides on the first");
     static_assert(!kAtax || (kN && kT), "ATAX weights the column sums with the row dots");
     static_assert(V == 1 || V == 2 || V == 4 || V == 8, "slots per thread");
-    constexpr int R = kSkinnyRows / V;
+    constexpr int R = skinny_rows(V);
     constexpr int W = PAIR ? 2 : 1;
     // loads bypass L1 here (measured: 4M x 32 BiCGK 4.8 TB/s with the bypass, 4.4 without)
 
