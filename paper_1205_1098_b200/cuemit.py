@@ -205,6 +205,7 @@ class _Emitter:
         self.promoted: dict = {}
         self.preloaded: dict = {}      # operand -> register holding it (inside a load/compute batch)
         self.cur_threads = self.threads
+        self.strip_axis = None         # set while a region is emitted with a 2-D (block x column strip) grid
 
     # -- names and references (cemit.py:54-110) ----------------------------------
     def index(self, s: dict, block: str | None = None) -> str:
@@ -364,6 +365,50 @@ class _Emitter:
                         all(c == ("l", s["labels"][0], False) for c, _ in acc):
                     self.promoted[name] = s["extents"][0]
 
+    def _lane_loops(self, items: list):
+        for it in items:
+            if it["t"] == "loop":
+                if self.is_innermost(it):
+                    yield it
+                else:
+                    yield from self._lane_loops(it["body"])
+
+    def strip_width(self) -> int:
+        return self.threads * self.unroll
+
+    def strip_mappable(self, items: list):
+        """A region whose statements are all element-wise in ONE full-extent strided axis (no
+        uniform statements, no reductions that leave that axis) can be cut into column strips:
+        CTA (p, c) does block p of the partition and strip c of the strided axis.  Every CTA then
+        holds its column accumulators for one strip only (8 KiB of shared memory instead of 8 N),
+        so the SMs are full, and nothing new has to be joined.  Returns the axis or None."""
+        if not self.optimize or self.conservative:
+            return None
+        axes = set()
+
+        def walk(its) -> bool:
+            for it in its:
+                if it["t"] == "stmt":
+                    return False
+                if it["t"] != "loop":
+                    return False
+                if self.is_innermost(it):
+                    if it["sliced"]:
+                        return False
+                    axes.add(it["axis"])
+                    for st in it["body"]:       # every target moves with the strided axis
+                        name = st["target"] if st["role"] == "init" else \
+                            self.target_name(self.ops[str(st["op"])], True)
+                        if it["axis"] not in self.st[name]["labels"]:
+                            return False
+                elif not walk(it["body"]):
+                    return False
+            return True
+
+        if not walk(items) or len(axes) != 1:
+            return None
+        return next(iter(axes))
+
     def lane_private(self, name: str, key: tuple) -> bool:
         return all(c == key for c, _ in self.access.get(name, ()))
 
@@ -507,6 +552,8 @@ class _Emitter:
         w = self.w
         v, T = loop["axis"], self.cur_threads
         lo, hi = (f"{v}_lo", f"{v}_hi") if loop["sliced"] else ("0", loop["extent"])
+        if self.strip_axis == v and not loop["sliced"]:
+            lo, hi = f"{v}_s0_", f"{v}_s1_"               # this CTA's column strip
         accs = self.lane_accumulators(loop, block, in_region)
         R = self.jam if rows else 1
         U = 1 if self.is_global_rmw(loop, accs, in_region) else self.unroll
@@ -804,7 +851,22 @@ class _Emitter:
                 launches.append(f"long {nb} = {t};")
             ax, ext = root["axis"], root["extent"]
             smem_args = ""
-            if self.promoted:
+            strip = self.strip_mappable(root["body"])
+            strip_ext = None
+            if strip is not None:
+                # 2-D grid: blockIdx.x = block of the partition, blockIdx.y = column strip
+                strip_ext = next(l["extent"] for l in self._lane_loops(root["body"]))
+                sw = self.strip_width()
+                launches.append(f"const long strips{regions}_ = ({strip_ext} + {sw - 1}) / {sw};")
+                launches.append(f"{{ long want_ = ((long)sms_ * 8 + strips{regions}_ - 1) / strips{regions}_; "
+                                f"if (want_ < {org_t}) want_ = {org_t}; if ({nb} > want_) {nb} = want_; }}")
+                uses_smem = True                     # (sms_ is read from the device below)
+            if self.promoted and strip is not None:
+                total = len(self.promoted) * self.strip_width()
+                launches.append(f"const size_t smb{regions}_ = sizeof(double) * {total};")
+                launches.append(f"const int sm_ok{regions}_ = 1;")
+                smem_args = f", sm_ok{regions}_"
+            elif self.promoted:
                 # block partials indexed by the strided axis only: each thread owns its
                 # elements for the whole launch, so they accumulate in shared memory and
                 # reach the partial buffer once, at the end (when they fit; else in place)
@@ -827,26 +889,38 @@ class _Emitter:
             w.put(f"const long {ax}_lo = ({ext} * p_) / nblocks_;")
             w.put(f"const long {ax}_hi = ({ext} * (p_ + 1)) / nblocks_;")
             w.put(f"(void){ax}_lo; (void){ax}_hi;")
+            if strip is not None:
+                sw = self.strip_width()
+                w.put(f"const long {strip}_s0_ = (long)blockIdx.y * {sw};")
+                w.put(f"const long {strip}_s1_ = {strip}_s0_ + {sw} < {strip_ext} ? {strip}_s0_ + {sw} : {strip_ext};")
+                self.strip_axis = strip
             if self.promoted:
                 w.put("extern __shared__ double dyn_[];")
                 offset = "0"
                 for name, e in self.promoted.items():
                     size = self.st[name]["extents"][0]
-                    w.put(f"double *{name}_l = sm_ok_ ? dyn_ + ({offset}) : {name} + p_ * ({size});")
-                    offset += f" + {e}"
+                    if strip is not None:          # X_l[j] is valid for the strip's j
+                        w.put(f"double *{name}_l = dyn_ + ({offset}) - {strip}_s0_; (void)sm_ok_;")
+                        offset += f" + {self.strip_width()}"
+                    else:
+                        w.put(f"double *{name}_l = sm_ok_ ? dyn_ + ({offset}) : {name} + p_ * ({size});")
+                        offset += f" + {e}"
             self.emit_items(root["body"], "p_", True)
             if self.promoted:
                 w.open("if (sm_ok_)")
                 for name in self.promoted:
                     s = self.st[name]
                     lab, size = s["labels"][0], s["extents"][0]
-                    w.put(f"for (long {lab} = threadIdx.x; {lab} < {size}; {lab} += blockDim.x) "
+                    lo, hi = (f"{strip}_s0_", f"{strip}_s1_") if strip is not None else ("0", size)
+                    w.put(f"for (long {lab} = {lo} + threadIdx.x; {lab} < {hi}; {lab} += blockDim.x) "
                           f"{name}[p_ * ({size}) + {lab}] = {name}_l[{lab}];")
                 w.close()
+            self.strip_axis = None
             w.close()
             w.put()
             dyn = f"sm_ok{regions}_ ? smb{regions}_ : 0" if self.promoted else "0"
-            launches.append(f"{fname}<<<(unsigned){nb}, {self.threads}, {dyn}, 0>>>({call}, {nb}{smem_args});")
+            grid = f"dim3((unsigned){nb}, (unsigned)strips{regions}_)" if strip is not None else f"(unsigned){nb}"
+            launches.append(f"{fname}<<<{grid}, {self.threads}, {dyn}, 0>>>({call}, {nb}{smem_args});")
             self.promoted = {}
             for result in root["partials"]:
                 pname = self.partial_for(result)
@@ -1215,6 +1289,8 @@ def estimate_cost_ir(ir: dict, extents: dict, model: EmitModel | None = None,
     def has_loop(items):
         return any(it["t"] == "loop" for it in items)
 
+    strip = {"axis": None, "count": 1.0}          # 2-D (block x column strip) mapping of the launch
+
     def walk(items, trips, nb, threads, acc, in_region, batch):
         """acc: dict(bytes=, steps=) for one launch; `trips` executions per block, `batch`
         rows handled per execution (1 unless the enclosing loop is jammed)."""
@@ -1230,6 +1306,10 @@ def estimate_cost_ir(ir: dict, extents: dict, model: EmitModel | None = None,
                 walk(it["body"], trips * max(rng / jam, 1.0), nb, threads, acc, in_region, jam)
                 continue
             # strided (innermost) loop
+            ctas = nb
+            if strip["axis"] == it["axis"] and not it["sliced"]:
+                rng = min(rng, float(em.strip_width()))        # a CTA walks one strip of it
+                ctas = nb * strip["count"]
             per_thread = max(1.0, rng / threads)
             mats, vecs, rmw = set(), set(), False
             accs = em.lane_accumulators(it, "p_" if in_region else None, in_region)
@@ -1245,7 +1325,7 @@ def estimate_cost_ir(ir: dict, extents: dict, model: EmitModel | None = None,
                         continue
                     (mats if len(s_["labels"]) == 2 else vecs).add(n)
             rmw = em.is_global_rmw(it, accs, in_region)
-            acc["bytes"] += 8.0 * len(mats) * rng * trips * batch * nb + 8.0 * len(vecs) * rng * nb
+            acc["bytes"] += 8.0 * len(mats) * rng * trips * batch * ctas + 8.0 * len(vecs) * rng * ctas
             ends_in_sync = bool(accs) or em.loop_needs_barrier(it, in_region)
             trip = m.rmw_trip_us if rmw else (m.jam_trip_us if batch > 1 else m.trip_us)
             acc["steps"] += trips * ((m.step_us if ends_in_sync else m.free_step_us) + per_thread * batch * trip)
@@ -1277,7 +1357,13 @@ def estimate_cost_ir(ir: dict, extents: dict, model: EmitModel | None = None,
         em.begin_launch(root["body"], True)
         if em.has_sliced_lane_loop(root["body"]):
             nb = min(nb, max(org_t, float(int(ext[root["extent"]]) // em.threads)))
-        if em.promoted:
+        axis = em.strip_mappable(root["body"])
+        strip["axis"], strip["count"] = axis, 1.0
+        if axis is not None:
+            width = ext[next(l["extent"] for l in em._lane_loops(root["body"]))]
+            strip["count"] = float(-(-int(width) // em.strip_width()))
+            nb = min(nb, max(org_t, float(-(-m.sm_count * 8 // int(strip["count"])))))
+        elif em.promoted:
             smem = 8.0 * sum(ext[e] for e in em.promoted.values())
             if smem <= SMEM_ACC_BYTES:
                 nb = min(nb, max(org_t, m.sm_count * float(int(227 * 1024 // (smem + 2048)))))
@@ -1286,7 +1372,8 @@ def estimate_cost_ir(ir: dict, extents: dict, model: EmitModel | None = None,
         nb = max(1.0, min(nb, ext[root["extent"]]))
         acc = {"bytes": 0.0, "steps": 0.0}
         walk(root["body"], 1.0, nb, float(em.threads), acc, True, 1)
-        close(acc, nb)
+        close(acc, nb * strip["count"])
+        strip["axis"], strip["count"] = None, 1.0
         launches += 1
         for result in root["partials"]:          # join: read nb partial rows, write the result
             p = st[em.partial_for(result)]

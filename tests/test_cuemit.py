@@ -69,6 +69,14 @@ def test_structure_of_the_bicgk_max_fuse_kernel():
     # ATAX: the contracted row value is an array over the jammed rows
     atax = cuemit.emit_cuda(next(i for i in IRS["atax"] if i["organism"].startswith("{_{p(i)}{_i{_j 1}{_j 2}}}"))).source
     assert "double t0_s_a[4];" in atax and "double &t0_s = t0_s_a[r_];" in atax
+    # a region whose statements are all element-wise in the strided axis is cut into column strips:
+    # 2-D grid, the column partial of one strip in shared memory, nothing new to join
+    best = json.loads((Path(__file__).parent.parent / "profiles" / "r01" / "ga_best_irs.json").read_text())
+    gem2 = cuemit.emit_cuda(best["gemver"]["alternatives"][1]["ir"]).source
+    assert "const long j_s0_ = (long)blockIdx.y * 1024;" in gem2
+    assert "double *t3_part_l = dyn_ + (0) - j_s0_;" in gem2
+    assert "gemver_region0<<<dim3((unsigned)nb0_, (unsigned)strips1_), 256" in gem2
+    assert "blockIdx.y" not in opt                      # BiCGK's row dots leave the strided axis: 1-D
     # a value written by thread 0 and read by every thread keeps all barriers and is not jammed
     plain = cuemit.emit_cuda(next(i for i in IRS["gesummv"] if i["organism"].startswith("{_i{_j 1}}{_i 2}"))).source
     assert "cta_allreduce_n<" not in plain and "__syncthreads();" in plain
