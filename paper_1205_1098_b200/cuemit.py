@@ -143,6 +143,17 @@ __device__ __forceinline__ double cta_allreduce(double v, double *scratch)
     return total;
 }
 
+// warp-level only (strip mode: every warp writes its own partial of a row dot, no CTA barrier)
+template <int R>
+__device__ __forceinline__ void warp_reduce_n(double (&v)[R])
+{
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+#pragma unroll
+        for (int off = 16; off >= 1; off >>= 1) v[r] += __shfl_xor_sync(0xffffffffu, v[r], off);
+    }
+}
+
 // the same for R values at once (R rows of an unrolled-and-jammed loop): one pair of
 // barriers instead of R, every value summed in exactly the order cta_allreduce uses
 template <int R>
@@ -206,6 +217,7 @@ class _Emitter:
         self.preloaded: dict = {}      # operand -> register holding it (inside a load/compute batch)
         self.cur_threads = self.threads
         self.strip_axis = None         # set while a region is emitted with a 2-D (block x column strip) grid
+        self.row_accs: dict = {}       # row accumulator -> its per-strip partial buffer (strip mode)
 
     # -- names and references (cemit.py:54-110) ----------------------------------
     def index(self, s: dict, block: str | None = None) -> str:
@@ -260,6 +272,11 @@ class _Emitter:
         name = self.target_name(op, in_region)
         if self.st[name]["cls"] == "partial":
             return self.partial_ref(name, block), name
+        if self.strip_axis is not None and name in self.row_accs:
+            st = self.st[name]
+            warps = self.threads // 32
+            return (f"{self.row_accs[name]}[((long)blockIdx.y * {warps} + (threadIdx.x >> 5)) * ({st['extents'][0]}) "
+                    f"+ {st['labels'][0]}]"), name
         return self.ref(name), name
 
     def init_lvalue(self, name: str, block: str | None) -> str:
@@ -376,19 +393,35 @@ class _Emitter:
     def strip_width(self) -> int:
         return self.threads * self.unroll
 
-    def strip_mappable(self, items: list):
+    def strip_mappable(self, items: list, part_axis: str | None = None):
         """A region whose statements are all element-wise in ONE full-extent strided axis (no
         uniform statements, no reductions that leave that axis) can be cut into column strips:
         CTA (p, c) does block p of the partition and strip c of the strided axis.  Every CTA then
         holds its column accumulators for one strip only (8 KiB of shared memory instead of 8 N),
-        so the SMs are full, and nothing new has to be joined.  Returns the axis or None."""
+        so the SMs are full, and nothing new has to be joined.
+
+        One kind of reduction may leave the axis: a row dot `X[i] += ..` into an output / temporary
+        indexed by the partition axis only, which the region otherwise just zeroes (BiCGK's q).
+        Its strips write per-strip partials `X_sp_[c][i]`, added up in ascending strip order by a
+        small join kernel (`self.row_accs`).  Returns the strided axis or None."""
+        self.row_accs = {}
         if not self.optimize or self.conservative:
             return None
         axes = set()
+        row_accs = {}
+
+        def row_acc_ok(name: str) -> bool:
+            s = self.st[name]
+            return (part_axis is not None and s["cls"] in ("output", "temp") and s["order"] == "vec"
+                    and s["labels"] == [part_axis])
 
         def walk(its) -> bool:
             for it in its:
                 if it["t"] == "stmt":
+                    # the only uniform statement allowed: zeroing a row accumulator
+                    if it["role"] == "init" and row_acc_ok(it["target"]):
+                        row_accs.setdefault(it["target"], 0)
+                        continue
                     return False
                 if it["t"] != "loop":
                     return False
@@ -396,18 +429,37 @@ class _Emitter:
                     if it["sliced"]:
                         return False
                     axes.add(it["axis"])
-                    for st in it["body"]:       # every target moves with the strided axis
+                    for st in it["body"]:       # every target moves with the strided axis ...
                         name = st["target"] if st["role"] == "init" else \
                             self.target_name(self.ops[str(st["op"])], True)
-                        if it["axis"] not in self.st[name]["labels"]:
+                        if it["axis"] in self.st[name]["labels"]:
+                            continue
+                        op = self.ops[str(st["op"])] if st["role"] == "compute" else None
+                        if op is None or not op["reduction"] or not row_acc_ok(name):
                             return False
+                        row_accs[name] = row_accs.get(name, 0) + 1      # ... or is a row dot
                 elif not walk(it["body"]):
                     return False
             return True
 
         if not walk(items) or len(axes) != 1:
             return None
+        for name, count in row_accs.items():
+            # exactly one reduction feeds it and nothing in the region reads it
+            if count != 1 or any(m == "r" and c != "u0" for c, m in self.access.get(name, ())):
+                return None
+            if name in {n for it in self._all_stmts(items) if it["role"] == "compute"
+                        for n in self.ops[str(it["op"])]["operands"]}:
+                return None
+        self.row_accs = {name: f"{name}_sp_" for name in row_accs}
         return next(iter(axes))
+
+    def _all_stmts(self, items: list):
+        for it in items:
+            if it["t"] == "stmt":
+                yield it
+            else:
+                yield from self._all_stmts(it["body"])
 
     def lane_private(self, name: str, key: tuple) -> bool:
         return all(c == key for c, _ in self.access.get(name, ()))
@@ -441,6 +493,8 @@ class _Emitter:
         barrier = barrier and self.conservative
         if stmt["role"] == "init":
             name = stmt["target"]
+            if self.strip_axis is not None and name in self.row_accs:
+                return                                   # the strip partial is assigned, not accumulated
             if self.st[name]["cls"] == "contracted":
                 w.put(f"{self.scalar_names[name]} = 0.0;")
                 return
@@ -618,6 +672,18 @@ class _Emitter:
         w.close()
         w.close()
         for acc, lhs, sname in accs.values():
+            per_warp = self.strip_axis is not None and sname in self.row_accs
+            if per_warp:
+                # strip mode: a warp's lanes are summed, lane 0 stores the warp's partial of the
+                # row dot; strips x warps partials are added by the row join.  No CTA barrier.
+                if rows:
+                    w.put(f"warp_reduce_n<{R}>({acc}_a);")
+                    open_rows()
+                else:
+                    w.put(f"{{ double one_[1] = {{{acc}}}; warp_reduce_n<1>(one_); {acc} = one_[0]; }}")
+                w.put(f"if ((threadIdx.x & 31) == 0) {lhs} = {acc};")
+                close_rows()
+                continue
             if rows:
                 w.put(f"cta_allreduce_n<{R}>({acc}_a, scratch_);")
                 open_rows()
@@ -747,8 +813,21 @@ class _Emitter:
         for name, s in self.st.items():
             if s["cls"] in ("temp", "partial"):
                 out.append((f"double *__restrict__ {name}", name))
+        for sp in self.all_row_accs().values():           # per-strip partials of row dots (strip mode)
+            out.append((f"double *__restrict__ {sp}", sp))
         out += [(f"long {e}", e) for e in self.ir["extents"]]
         return out
+
+    def all_row_accs(self) -> dict:
+        """Row accumulators of every strip-mapped region of the kernel (name -> buffer)."""
+        found = {}
+        for root in self.ir["roots"]:
+            if root["t"] == "par":
+                self.begin_launch(root["body"], True)
+                if self.strip_mappable(root["body"], root["axis"]) is not None:
+                    found.update(self.row_accs)
+        self.row_accs = {}
+        return found
 
     def emit_join(self, jname: str, decl: str, pname: str, result: str):
         """Ascending join of the block partials (cemit.py:204-222) as its own kernel."""
@@ -797,6 +876,7 @@ class _Emitter:
     def emit(self) -> str:
         ir, w = self.ir, self.w
         kname = ir["name"].lower()
+        sp_buffers = list(self.all_row_accs().values())
         dparams = self.device_params()
         decl = ", ".join(d for d, _ in dparams)
         call = ", ".join(n for _, n in dparams)
@@ -851,7 +931,7 @@ class _Emitter:
                 launches.append(f"long {nb} = {t};")
             ax, ext = root["axis"], root["extent"]
             smem_args = ""
-            strip = self.strip_mappable(root["body"])
+            strip = self.strip_mappable(root["body"], root["axis"])
             strip_ext = None
             if strip is not None:
                 # 2-D grid: blockIdx.x = block of the partition, blockIdx.y = column strip
@@ -861,6 +941,9 @@ class _Emitter:
                 launches.append(f"{{ long want_ = ((long)sms_ * 8 + strips{regions}_ - 1) / strips{regions}_; "
                                 f"if (want_ < {org_t}) want_ = {org_t}; if ({nb} > want_) {nb} = want_; }}")
                 uses_smem = True                     # (sms_ is read from the device below)
+                for name, sp in self.row_accs.items():
+                    e0 = self.st[name]["extents"][0]
+                    launches.append(f"cudaMallocAsync(&{sp}, sizeof(double) * (size_t)strips{regions}_ * {self.threads // 32} * (size_t){e0}, 0);")
             if self.promoted and strip is not None:
                 total = len(self.promoted) * self.strip_width()
                 launches.append(f"const size_t smb{regions}_ = sizeof(double) * {total};")
@@ -921,6 +1004,22 @@ class _Emitter:
             dyn = f"sm_ok{regions}_ ? smb{regions}_ : 0" if self.promoted else "0"
             grid = f"dim3((unsigned){nb}, (unsigned)strips{regions}_)" if strip is not None else f"(unsigned){nb}"
             launches.append(f"{fname}<<<{grid}, {self.threads}, {dyn}, 0>>>({call}, {nb}{smem_args});")
+            for name, sp in (self.row_accs.items() if strip is not None else ()):
+                # ascending (strip, warp) partials, a thread per row
+                e0, lab = self.st[name]["extents"][0], self.st[name]["labels"][0]
+                jname = f"{kname}_rows{regions}_{name}"
+                w.open(f"__global__ void __launch_bounds__(256) {jname}({decl}, long strips_)")
+                w.put(f"const long {lab} = (long)blockIdx.x * 256 + threadIdx.x;")
+                w.open(f"if ({lab} < {e0})")
+                w.put(f"double acc = {sp}[{lab}];")
+                w.put(f"for (long c = 1; c < strips_; ++c) acc += {sp}[c * ({e0}) + {lab}];")
+                w.put(f"{self.ref(name)} = acc;")
+                w.close()
+                w.close()
+                w.put()
+                launches.append(f"{jname}<<<(unsigned)(({e0} + 255) / 256), 256, 0, 0>>>({call}, strips{regions}_ * {self.threads // 32});")
+                launches.append(f"cudaFreeAsync({sp}, 0);")
+            self.row_accs = {}
             self.promoted = {}
             for result in root["partials"]:
                 pname = self.partial_for(result)
@@ -967,6 +1066,8 @@ class _Emitter:
         for name, size in temps:
             w.put(f"double *{name} = nullptr;")
             w.put(f"cudaMallocAsync(&{name}, sizeof(double) * ({size}), 0);")
+        for sp in sp_buffers:
+            w.put(f"double *{sp} = nullptr;")
         for stmt in launches:
             w.put(stmt)
         for name, _ in temps:      # stream-ordered pool: no device-wide sync per temporary
@@ -1357,7 +1458,8 @@ def estimate_cost_ir(ir: dict, extents: dict, model: EmitModel | None = None,
         em.begin_launch(root["body"], True)
         if em.has_sliced_lane_loop(root["body"]):
             nb = min(nb, max(org_t, float(int(ext[root["extent"]]) // em.threads)))
-        axis = em.strip_mappable(root["body"])
+        axis = em.strip_mappable(root["body"], root["axis"])
+        row_joins = len(em.row_accs)
         strip["axis"], strip["count"] = axis, 1.0
         if axis is not None:
             width = ext[next(l["extent"] for l in em._lane_loops(root["body"]))]
@@ -1373,7 +1475,12 @@ def estimate_cost_ir(ir: dict, extents: dict, model: EmitModel | None = None,
         acc = {"bytes": 0.0, "steps": 0.0}
         walk(root["body"], 1.0, nb, float(em.threads), acc, True, 1)
         close(acc, nb * strip["count"])
+        for _ in range(row_joins if axis is not None else 0):    # join of a row dot's strip partials
+            per_launch.append((m.launch_us + 8.0 * ext[root["extent"]] * (strip["count"] + 1)
+                               / (m.peak_gbs * 1e9) * 1e6) * 1e-6)
+            launches += 1
         strip["axis"], strip["count"] = None, 1.0
+        em.row_accs = {}
         launches += 1
         for result in root["partials"]:          # join: read nb partial rows, write the result
             p = st[em.partial_for(result)]

@@ -52,31 +52,36 @@ def test_structure_of_the_bicgk_max_fuse_kernel():
     assert "cta_allreduce(lacc1, scratch_)" in src
     assert "long nb0_ = 64;" in src and "bicgk_region0<<<(unsigned)nb0_, 256, 0, 0>>>" in src
     assert "bicgk_join1_s" in src
-    # optimised: rows four at a time, column partial in shared memory, one batched reduction,
+    # optimised: rows four at a time, one batched reduction, explicit load / compute batches with
+    # a literal stride, and -- q being a pure row dot -- a 2-D grid of column strips: the column
+    # partial of a strip in shared memory, the row dot's strip partials joined by a small kernel;
     # no barrier besides the reduction's own (q is only ever touched by thread 0)
     opt = cuemit.emit_cuda(ir, blocks=64).source
     assert "for (; i_b_ + 4 <= i_hi; i_b_ += 4)" in opt and "for (long i = i_b_; i < i_hi; ++i)" in opt
-    assert "double *s_part_l = sm_ok_ ? dyn_ + (0) : s_part + p_ * (N);" in opt
-    # explicit load / compute batches with a literal stride: all loads first, then the statements
-    assert "for (; j_b_ + 768 < N; j_b_ += 1024)" in opt and "double A_v[4][4];" in opt
+    assert "const long j_s0_ = (long)blockIdx.y * 1024;" in opt
+    assert "double *s_part_l = dyn_ + (0) - j_s0_;" in opt
+    assert "for (; j_b_ + 768 < j_s1_; j_b_ += 1024)" in opt and "double A_v[4][4];" in opt
     assert "A_v[r_][u_] = ld_stream(&A[i * N + j]);" in opt and "p_v[u_] = ld_keep(&p[j]);" in opt
     assert "__launch_bounds__(256, 2) bicgk_region0" in opt
     assert "s_part_l[j] += __dmul_rn(A_v[r_][u_], r[i]);" in opt
-    assert "cta_allreduce_n<4>(lacc1_a, scratch_);" in opt
-    assert "s_part[p_ * (N) + j] = s_part_l[j];" in opt
-    body = opt[opt.index("bicgk_region0("):opt.index("bicgk_join1_s")]
+    assert "warp_reduce_n<4>(lacc1_a);" in opt
+    assert "if ((threadIdx.x & 31) == 0) q_sp_[((long)blockIdx.y * 8 + (threadIdx.x >> 5)) * (M) + i] = lacc1;" in opt
+    assert "bicgk_rows1_q<<<" in opt and "acc += q_sp_[c * (M) + i];" in opt
+    assert "bicgk_region0<<<dim3((unsigned)nb0_, (unsigned)strips1_), 256" in opt
+    body = opt[opt.index("bicgk_region0("):opt.index("bicgk_rows1_q")]
     assert "__syncthreads" not in body
-    # ATAX: the contracted row value is an array over the jammed rows
+    # ATAX: the row dot is consumed by the second strided loop, so a CTA keeps whole rows (1-D
+    # grid); the contracted row value is an array over the jammed rows, the column partial lives
+    # in shared memory when it fits
     atax = cuemit.emit_cuda(next(i for i in IRS["atax"] if i["organism"].startswith("{_{p(i)}{_i{_j 1}{_j 2}}}"))).source
     assert "double t0_s_a[4];" in atax and "double &t0_s = t0_s_a[r_];" in atax
-    # a region whose statements are all element-wise in the strided axis is cut into column strips:
-    # 2-D grid, the column partial of one strip in shared memory, nothing new to join
+    assert "double *y_part_l = sm_ok_ ? dyn_ + (0) : y_part + p_ * (N);" in atax
+    assert "y_part[p_ * (N) + j] = y_part_l[j];" in atax and "blockIdx.y" not in atax
+    # a region whose statements are all element-wise in the strided axis needs no row join at all
     best = json.loads((Path(__file__).parent.parent / "profiles" / "r01" / "ga_best_irs.json").read_text())
     gem2 = cuemit.emit_cuda(best["gemver"]["alternatives"][1]["ir"]).source
-    assert "const long j_s0_ = (long)blockIdx.y * 1024;" in gem2
-    assert "double *t3_part_l = dyn_ + (0) - j_s0_;" in gem2
+    assert "double *t3_part_l = dyn_ + (0) - j_s0_;" in gem2 and "_sp_" not in gem2
     assert "gemver_region0<<<dim3((unsigned)nb0_, (unsigned)strips1_), 256" in gem2
-    assert "blockIdx.y" not in opt                      # BiCGK's row dots leave the strided axis: 1-D
     # a value written by thread 0 and read by every thread keeps all barriers and is not jammed
     plain = cuemit.emit_cuda(next(i for i in IRS["gesummv"] if i["organism"].startswith("{_i{_j 1}}{_i 2}"))).source
     assert "cta_allreduce_n<" not in plain and "__syncthreads();" in plain
