@@ -31,7 +31,8 @@ Mapping (the reference's emission rules, cemit.py:112-222, re-targeted):
 * top-level items outside any region (serial code on the CPU) run in a single CTA.
 
 The emitted translation unit exports `extern "C" void <kernel>(...)` with the
-reference's argument order (cemit.py:225-241) taking DEVICE pointers.
+reference's argument order (cemit.py:225-241) taking DEVICE pointers; the call is
+stream-ordered on the default stream (the caller synchronises, `run_emitted` does).
 """
 from __future__ import annotations
 
@@ -192,9 +193,11 @@ JOIN_COLS = 32                # columns per CTA of a join kernel
 
 class _Emitter:
     def __init__(self, ir: dict, blocks: int, optimize: bool = True, jam: int = JAM,
-                 unroll: int = 4, threads: int = CTA_THREADS, minb: int = 2, bypass_l1: int = 1):
+                 unroll: int = 4, threads: int = CTA_THREADS, minb: int = 2, bypass_l1: int = 1,
+                 sync: int = 0):
         self.jam, self.unroll, self.threads, self.minb = int(jam), int(unroll), int(threads), int(minb)
         self.bypass_l1 = bool(bypass_l1)
+        self.sync = bool(sync)
         self.ir = ir
         self.st = ir["storage"]
         self.ops = ir["ops"]
@@ -1072,7 +1075,10 @@ class _Emitter:
             w.put(stmt)
         for name, _ in temps:      # stream-ordered pool: no device-wide sync per temporary
             w.put(f"cudaFreeAsync({name}, 0);")
-        w.put("cudaStreamSynchronize(0);")
+        if self.sync or not self.optimize:
+            w.put("cudaStreamSynchronize(0);")       # the reference's protocol: results ready on return
+        # (default: stream-ordered like the library's own device-pointer entry points -- operands
+        #  are device buffers, temporaries are freed in stream order; the caller synchronises)
         w.close()
         w.put()
         w.open(f'extern "C" int {kname}_last_cuda_error(void)')
@@ -1087,7 +1093,7 @@ def emit_cuda(ir: dict, blocks: int = DEFAULT_BLOCKS, optimize: bool = True, **t
     `optimize=False` prints the plain mapping only (every barrier, no unroll-and-jam, block
     partials accumulated in global memory).  `tune`: jam (rows per batch), unroll (of the
     strided loop under a batch), threads (per CTA of a parallel region), minb (CTAs per SM the
-    register budget is sized for), bypass_l1 (0: 2-D operands are loaded L1-allocating; ATAX-like
+    register budget is sized for), sync (1: cudaStreamSynchronize before returning), bypass_l1 (0: 2-D operands are loaded L1-allocating; ATAX-like
     bodies that read a row twice gain 10 %)."""
     em = _Emitter(ir, int(blocks), bool(optimize), **tune)
     source = em.emit()
@@ -1345,16 +1351,16 @@ class EmitModel:
     profiles/r01/organism_times.json (120 organisms x n = 1024, 2048, 4096) by
     scripts/fit_emit_model.py."""
     peak_gbs: float = 6500.0        # HBM ceiling of a full grid
-    cta_gbs: float = 96.0          # what one CTA streams on its own
-    launch_us: float = 11.0         # per kernel launch (incl. its share of the final sync)
-    step_us: float = 0.13           # one strided-loop execution that ends in a barrier / CTA reduction
+    cta_gbs: float = 98.0          # what one CTA streams on its own
+    launch_us: float = 6.4         # per kernel launch (incl. its share of the final sync)
+    step_us: float = 0.53           # one strided-loop execution that ends in a barrier / CTA reduction
     free_step_us: float = 0.0       # ... that ends in neither (barrier analysis removed them)
     trip_us: float = 0.17           # one trip of a thread through a strided loop
     jam_trip_us: float = 0.30       # the same per row when rows are batched (unroll-and-jam; a trip then
                                     # carries `unroll` elements per row, hence the larger figure)
-    rmw_trip_us: float = 0.15       # a trip that read-modify-writes global memory
-    stmt_us: float = 1.27           # a uniform statement that writes memory and needs its barrier
-    free_stmt_us: float = 0.15      # ... and does not
+    rmw_trip_us: float = 0.13       # a trip that read-modify-writes global memory
+    stmt_us: float = 0.80           # a uniform statement that writes memory and needs its barrier
+    free_stmt_us: float = 0.06      # ... and does not
     alloc_us: float = 0.0           # stream-ordered malloc + free of one temporary / partial per call
                                     # (the reference pays malloc/free per call too, cemit.py:183-202)
     sm_count: int = 148

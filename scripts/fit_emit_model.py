@@ -26,7 +26,7 @@ def loss(x):
     model = replace(base, **{n: float(np.exp(v)) for n, v in zip(names, x)})
     return float(np.mean(np.log(predict(model) / meas) ** 2))
 
-x0 = np.log([getattr(base, n) for n in names])
+x0 = np.log([max(getattr(base, n), 1e-3) for n in names])     # (zero coefficients: start small, not at -inf)
 res = minimize(loss, x0, method="Nelder-Mead", options={"maxiter": 1500, "xatol": 1e-3, "fatol": 1e-5})
 model = replace(base, **{n: float(np.exp(v)) for n, v in zip(names, res.x)})
 pred = predict(model)
