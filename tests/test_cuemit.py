@@ -82,6 +82,10 @@ def test_structure_of_the_bicgk_max_fuse_kernel():
     gem2 = cuemit.emit_cuda(best["gemver"]["alternatives"][1]["ir"]).source
     assert "double *t3_part_l = dyn_ + (0) - j_s0_;" in gem2 and "_sp_" not in gem2
     assert "gemver_region0<<<dim3((unsigned)nb0_, (unsigned)strips1_), 256" in gem2
+    # a pure vector region deals its own axis out in interleaved tiles (all CTAs sweep together)
+    axp = cuemit.emit_cuda(IRS["axpydot"][0]).source
+    assert "for (long t_ = p_; t_ * 1024 < M; t_ += nblocks_)" in axp and "const long k_t0_ = t_ * 1024;" in axp
+    assert "long nb0_ = (M + 1023) / 1024;" in axp
     # a value written by thread 0 and read by every thread keeps all barriers and is not jammed
     plain = cuemit.emit_cuda(next(i for i in IRS["gesummv"] if i["organism"].startswith("{_i{_j 1}}{_i 2}"))).source
     assert "cta_allreduce_n<" not in plain and "__syncthreads();" in plain
