@@ -20,7 +20,8 @@ bad = 0
 t0 = time.time()
 cases = []
 for name in ("bicgk", "gesummv", "gemver", "atax", "batax", "dgemvt", "axpydot"):
-    for (m, n) in [(4096, 4096), (1000, 8192), (8192, 1026), (333, 32768)]:
+    for (m, n) in [(4096, 4096), (1000, 8192), (8192, 1026), (333, 32768),
+                   (100000, 32), (40000, 100), (20000, 256), (9000, 500), (9, 300000), (5000, 1000)]:
         cases.append((name, m, n, {}))
 for c in (1, 2, 4, 8, 16):
     for (m, n) in [(2048, 4096), (777, 16384), (5000, 2050)]:
