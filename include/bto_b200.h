@@ -223,6 +223,11 @@ int   bto_device_info(int *sm_count, int *max_threads_per_sm,
  * arena (both cached between calls); bto_release_workspace frees them.      */
 long  bto_workspace_bytes(void);
 int   bto_release_workspace(void);
+/* Host <-> device copies with the staging the section-1 entry points use (pageable
+ * buffers of 16 MiB and more go through the pinned bounce slots at 45-50 GB/s instead of
+ * ~11 GB/s); synchronous: the data has arrived when the call returns.          */
+int   bto_copy_to_device(void *device_dst, const void *host_src, long bytes);
+int   bto_copy_to_host(void *host_dst, const void *device_src, long bytes);
 
 #ifdef __cplusplus
 }

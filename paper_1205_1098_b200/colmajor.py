@@ -83,10 +83,15 @@ def run_colmajor(name: str, graph, inputs: dict, extents: dict, stream=None) -> 
             vals.append(float(v))
             continue
         want = tuple(int(extents[d]) for d in graph.dims[iname])
-        t = v if hasattr(v, "is_cuda") else torch.from_numpy(np.asarray(v, dtype=np.float64))
-        if tuple(t.shape) != want:
-            raise ValueError(f"{iname}: expected shape {want}, got {tuple(t.shape)}")
-        t = t.to("cuda", torch.float64)
+        if tuple(np.shape(v)) != want:
+            raise ValueError(f"{iname}: expected shape {want}, got {tuple(np.shape(v))}")
+        if hasattr(v, "is_cuda"):
+            t = v.to("cuda", torch.float64)
+        elif decl.kind == "matrix":
+            # F-ordered host array = row-major transpose: copy that buffer, view it back
+            t = _native.to_device(np.asarray(v, dtype=np.float64).T).t()
+        else:
+            t = _native.to_device(v)
         # the buffer the reference would pass: F-ordered logical matrix = row-major transpose
         vals.append(t.t().contiguous() if decl.kind == "matrix" else t.contiguous())
     M, N = int(extents[graph.extent_names[0]]), int(extents[graph.extent_names[1]])
@@ -140,4 +145,8 @@ def run_colmajor(name: str, graph, inputs: dict, extents: dict, stream=None) -> 
     stream.synchronize()
     if on_gpu:
         return outs
-    return {k: v.cpu().numpy() for k, v in outs.items()}
+    host = {}
+    for k, v in outs.items():
+        # a column-major matrix comes back F-ordered, like the reference's reshape(order="F")
+        host[k] = _native.to_host(v.t()).T if (v.dim() == 2 and not v.is_contiguous()) else _native.to_host(v)
+    return host

@@ -632,4 +632,26 @@ int bto_release_workspace(void)
     return BTO_OK;
 }
 
+int bto_copy_to_device(void *device_dst, const void *host_src, long bytes)
+{
+    AsyncCall ac;
+    if (ac.rc != BTO_OK) return ac.rc;
+    if (bytes < 0 || (bytes > 0 && (!device_dst || !host_src))) return fail(BTO_ERR_INVALID, "copy_to_device: bad argument");
+    if (bytes == 0) return BTO_OK;
+    BTO_TRY(copy_in(*ac.ctx, device_dst, host_src, (size_t)bytes, ac.ctx->stream));
+    CUDA_TRY(cudaStreamSynchronize(ac.ctx->stream));
+    return BTO_OK;
+}
+
+int bto_copy_to_host(void *host_dst, const void *device_src, long bytes)
+{
+    AsyncCall ac;
+    if (ac.rc != BTO_OK) return ac.rc;
+    if (bytes < 0 || (bytes > 0 && (!host_dst || !device_src))) return fail(BTO_ERR_INVALID, "copy_to_host: bad argument");
+    if (bytes == 0) return BTO_OK;
+    BTO_TRY(copy_out(*ac.ctx, host_dst, device_src, (size_t)bytes, ac.ctx->stream));
+    CUDA_TRY(cudaStreamSynchronize(ac.ctx->stream));
+    return BTO_OK;
+}
+
 }  // extern "C"

@@ -177,11 +177,9 @@ def run_generic(graph: TypedSpec, inputs: dict, extents: dict, stream=None) -> d
             env[name] = GenericValue("scalar", coef=float(value))
             continue
         want = tuple(int(extents[d]) for d in graph.dims[name])
-        t = value if hasattr(value, "is_cuda") else torch.from_numpy(
-            np.ascontiguousarray(np.asarray(value, dtype=np.float64)))
-        if tuple(t.shape) != want:
-            raise ValueError(f"{name}: expected shape {want}, got {tuple(t.shape)}")
-        t = t.to("cuda", torch.float64)
+        if tuple(np.shape(value)) != want:
+            raise ValueError(f"{name}: expected shape {want}, got {tuple(np.shape(value))}")
+        t = value.to("cuda", torch.float64) if hasattr(value, "is_cuda") else _native.to_device(value)
         if decl.kind == "vector":
             env[name] = GenericValue("col" if decl.orientation == "column" else "row", t.contiguous())
         elif decl.orientation == "column":       # column-major operand: store the transpose
@@ -205,6 +203,6 @@ def run_generic(graph: TypedSpec, inputs: dict, extents: dict, stream=None) -> d
         if tuple(data.shape) != want:
             raise ValueError(f"{name}: computed shape {tuple(data.shape)}, declared {want}")
         data = data.contiguous()
-        outputs[name] = data if on_gpu else data.cpu().numpy()
+        outputs[name] = data if on_gpu else _native.to_host(data)
     ex.stream.synchronize()
     return outputs

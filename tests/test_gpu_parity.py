@@ -591,6 +591,21 @@ def test_randomised_differential_run(bto_lib, oracle):
     assert " 0 mismatches" in proc.stdout
 
 
+def test_staged_host_copies_round_trip(bto_lib):
+    """bto_copy_to_device / bto_copy_to_host: below and above the bounce threshold, more chunks
+    than slots, non-contiguous input, pinned memory."""
+    rng = np.random.default_rng(5)
+    for shape in ((1,), (1000, 3), (2 * 1024 * 1024 + 1,), (3001, 3001), (6000, 5000)):
+        a = rng.uniform(-1, 1, size=shape)
+        t = _native.to_device(a)
+        assert tuple(t.shape) == shape and torch.equal(t.cpu(), torch.from_numpy(a))
+        assert np.array_equal(_native.to_host(t), a)
+    a = rng.uniform(-1, 1, size=(2500, 2600))
+    assert np.array_equal(_native.to_host(_native.to_device(a.T)), a.T)          # strided view in
+    p = torch.from_numpy(a).pin_memory().numpy()
+    assert np.array_equal(_native.to_host(_native.to_device(p)), a)
+
+
 def test_bound_calls_replay(bto_lib, oracle):
     """GpuShardOps.bind pre-marshals a call; replaying it on new data in the same buffers gives
     the results of a fresh call."""
