@@ -228,6 +228,9 @@ int   bto_release_workspace(void);
  * ~11 GB/s); synchronous: the data has arrived when the call returns.          */
 int   bto_copy_to_device(void *device_dst, const void *host_src, long bytes);
 int   bto_copy_to_host(void *host_dst, const void *device_src, long bytes);
+/* host_dst[0 .. count) = value with the copy threads (first touch of fresh pages in
+ * parallel: the NaN prefill of a large output, runtime.py:99-150, at 30+ GB/s).   */
+int   bto_fill_host(double *host_dst, long count, double value);
 
 #ifdef __cplusplus
 }

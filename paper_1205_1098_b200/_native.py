@@ -59,7 +59,7 @@ EXPORTED = tuple(SIGNATURES) + tuple(f"bto_{k}_async" for k in SIGNATURES) + (
     "bto_last_error", "bto_last_error_string", "bto_clear_error",
     "bto_abi_version", "bto_set_stream", "bto_set_tuning", "bto_get_tuning",
     "bto_kernel_launches", "bto_bytes_min", "bto_device_info",
-    "bto_workspace_bytes", "bto_release_workspace", "bto_copy_to_device", "bto_copy_to_host",
+    "bto_workspace_bytes", "bto_release_workspace", "bto_copy_to_device", "bto_copy_to_host", "bto_fill_host",
 )
 
 _lib = None
@@ -138,6 +138,8 @@ def load() -> ctypes.CDLL:
     lib.bto_copy_to_device.argtypes = [_P, _P, _L]
     lib.bto_copy_to_host.restype = c_int
     lib.bto_copy_to_host.argtypes = [_P, _P, _L]
+    lib.bto_fill_host.restype = c_int
+    lib.bto_fill_host.argtypes = [_P, _L, _D]
     _lib = lib
     return lib
 
@@ -206,4 +208,14 @@ def to_host(tensor):
     out = np.empty(tuple(t.shape), dtype=np.float64)
     torch.cuda.current_stream().synchronize()
     check(load().bto_copy_to_host(ctypes.c_void_p(out.ctypes.data), ctypes.c_void_p(t.data_ptr()), out.nbytes))
+    return out
+
+
+def filled(size: int, value: float):
+    """np.full(size, value) with the first touch of the pages done by the copy threads."""
+    import ctypes
+
+    import numpy as np
+    out = np.empty(int(size), dtype=np.float64)
+    check(load().bto_fill_host(ctypes.c_void_p(out.ctypes.data), out.size, float(value)))
     return out

@@ -632,6 +632,20 @@ int bto_release_workspace(void)
     return BTO_OK;
 }
 
+int bto_fill_host(double *host_dst, long count, double value)
+{
+    if (count < 0 || (count > 0 && !host_dst)) return fail(BTO_ERR_INVALID, "fill_host: bad argument");
+    unsigned long long bits;
+    memcpy(&bits, &value, sizeof(bits));
+    const size_t bytes = (size_t)count * sizeof(double);
+    if (bytes < (8u << 20)) {
+        stream_fill(reinterpret_cast<char *>(host_dst), bits, bytes);
+    } else {
+        CopyPool::get().copy(reinterpret_cast<char *>(host_dst), nullptr, bytes, host_copy_threads(), bits);
+    }
+    return BTO_OK;
+}
+
 int bto_copy_to_device(void *device_dst, const void *host_src, long bytes)
 {
     AsyncCall ac;

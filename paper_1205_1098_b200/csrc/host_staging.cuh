@@ -94,6 +94,25 @@ void stream_copy(char *dst, const char *src, size_t bytes)
     memcpy(dst, src, bytes);
 }
 
+// dst[0 .. bytes) = the 8-byte pattern `bits`, non-temporal (bytes is a multiple of 8)
+void stream_fill(char *dst, unsigned long long bits, size_t bytes)
+{
+    unsigned long long *p = reinterpret_cast<unsigned long long *>(dst);
+    size_t n = bytes / 8;
+#if defined(__SSE2__)
+    while (n && (reinterpret_cast<uintptr_t>(p) & 15)) { *p++ = bits; --n; }
+    const __m128i v = _mm_set1_epi64x((long long)bits);
+    for (; n >= 8; n -= 8, p += 8) {
+        _mm_stream_si128(reinterpret_cast<__m128i *>(p), v);
+        _mm_stream_si128(reinterpret_cast<__m128i *>(p + 2), v);
+        _mm_stream_si128(reinterpret_cast<__m128i *>(p + 4), v);
+        _mm_stream_si128(reinterpret_cast<__m128i *>(p + 6), v);
+    }
+    _mm_sfence();
+#endif
+    while (n) { *p++ = bits; --n; }
+}
+
 // Persistent helpers for the bounce copies (a thread per piece and call cost ~0.5 ms of thread
 // creation per 64 MiB chunk, a third of the chunk's copy time).  Pieces of concurrent calls
 // (GEMVER fills inbound slots while its helper drains outbound ones) share one queue; a caller
@@ -107,7 +126,8 @@ public:
         return *pool;
     }
 
-    void copy(char *dst, const char *src, size_t bytes, int nt)
+    // src == nullptr: fill dst with the 8-byte pattern `bits` instead of copying
+    void copy(char *dst, const char *src, size_t bytes, int nt, unsigned long long bits = 0)
     {
         const size_t piece = ((bytes / nt) + 4095) & ~size_t(4095);
         std::atomic<int> left{0};
@@ -115,7 +135,7 @@ public:
             std::lock_guard<std::mutex> g(mu_);
             for (size_t lo = 0; lo < bytes; lo += piece) {
                 const size_t len = lo + piece < bytes ? piece : bytes - lo;
-                queue_.push_back({dst + lo, src + lo, len, &left});
+                queue_.push_back({dst + lo, src ? src + lo : nullptr, len, &left, bits});
                 left.fetch_add(1, std::memory_order_relaxed);
             }
             while ((int)workers_ < nt - 1) {
@@ -135,7 +155,7 @@ public:
     }
 
 private:
-    struct Piece { char *dst; const char *src; size_t len; std::atomic<int> *left; };
+    struct Piece { char *dst; const char *src; size_t len; std::atomic<int> *left; unsigned long long bits; };
 
     bool take(Piece *p)
     {
@@ -148,7 +168,11 @@ private:
 
     static void run(const Piece &p)
     {
-        stream_copy(p.dst, p.src, p.len);
+        if (p.src) {
+            stream_copy(p.dst, p.src, p.len);
+        } else {
+            stream_fill(p.dst, p.bits, p.len);
+        }
         p.left->fetch_sub(1, std::memory_order_release);
     }
 

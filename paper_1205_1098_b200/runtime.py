@@ -234,7 +234,7 @@ def _marshal(binary, kernel: GeneratedKernel, graph, inputs: dict, extents: dict
                              device=keep[0].device if keep else "cuda")
             args.append(ctypes.c_void_p(buf.data_ptr()))
         else:
-            buf = np.full(size, np.nan, dtype=np.float64)
+            buf = _native.filled(size, np.nan) if size >= (1 << 20) else np.full(size, np.nan, dtype=np.float64)
             args.append(ctypes.c_void_p(buf.ctypes.data))
         out_bufs[name] = buf
         keep.append(buf)

@@ -89,3 +89,14 @@ def test_product_code_never_touches_the_oracle():
             text = path.read_text()
             assert "oracle_lib" not in text and "libbto_oracle" not in text, path
             assert "/root/reference" not in text, path
+
+
+def test_host_fill_needs_no_gpu():
+    """bto_fill_host (the parallel NaN prefill of large outputs) is pure host code."""
+    import numpy as np
+    from paper_1205_1098_b200 import _native
+    for size, value in ((1, 2.5), (1000, -0.0), ((3 << 20) + 3, float("nan")), (5 << 20, 1e300)):
+        out = _native.filled(size, value)
+        assert out.shape == (size,) and out.dtype == np.float64
+        want = np.full(size, value)
+        assert np.array_equal(out.view(np.uint64), want.view(np.uint64))
