@@ -276,6 +276,19 @@ class Suite:
             self.az = torch.empty(self.an, dtype=torch.float64, device=dev)
             self.abeta = torch.empty(1, dtype=torch.float64, device=dev)
 
+    def operands(self, name: str):
+        """(inputs, outputs) of this rank's shard of sequence `name`, as device tensors."""
+        if name == "axpydot":
+            return [self.aw, self.av, self.au], [self.az, self.abeta]
+        if name == "bicgk":
+            return [self.A, self.vecN[0], self.vecM[0]], [self.q, self.s]
+        if name == "atax":
+            return [self.A, self.vecN[0]], [self.s]
+        if name == "gesummv":
+            return [self.GA, self.GB, self.vecN[0][: self.g]], [self.gy]
+        return ([self.A, self.vecM[1], self.vecN[1], self.vecM[2], self.vecN[2], self.vecM[0], self.vecN[3]],
+                [self.Bm, self.x, self.w])
+
     def launch(self, name: str):
         r = self.runner
         if name == "axpydot":
@@ -370,6 +383,57 @@ def e2e_host(torch, kernels, steps: int, warmup: int) -> dict:
             "api": f"C symbols of include/bto_b200.h section 1 with {host_kind[0]} host pointers"}
 
 
+def e2e_sharded(torch, dist, suite, kernels, steps: int, warmup: int) -> dict:
+    """N > 1: every rank pushes ITS shard of each sequence's inputs from pinned host memory, runs
+    the sharded sequence (exchange included) and pulls its outputs back, blocking per sequence
+    like a host-pointer call; whole-job bytes over the slowest rank's wall time."""
+    mirrors = {}
+
+    def host(t):
+        key = (t.data_ptr(), t.numel())
+        if key not in mirrors:
+            mirrors[key] = torch.empty(t.numel(), dtype=torch.float64, pin_memory=True)
+            mirrors[key].copy_(t.reshape(-1))
+        return mirrors[key]
+
+    plan = []
+    h2d = d2h = 0.0
+    for k in kernels:
+        ins, outs = suite.operands(k)
+        plan.append((k, [(t, host(t)) for t in ins], [(t, host(t)) for t in outs]))
+        h2d += sum(8.0 * t.numel() for t in ins)
+        d2h += sum(8.0 * t.numel() for t in outs)
+
+    def step():
+        for k, ins, outs in plan:
+            for t, h in ins:
+                t.view(-1).copy_(h, non_blocking=True) if t.is_contiguous() else t.copy_(h.view(t.shape), non_blocking=True)
+            suite.launch(k)
+            for t, h in outs:
+                h.copy_(t.reshape(-1), non_blocking=True)
+            torch.cuda.synchronize()
+
+    for _ in range(warmup):
+        step()
+    if suite.world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        step()
+    torch.cuda.synchronize()
+    sec = (time.perf_counter() - t0) / steps
+    if suite.world > 1:
+        t = torch.tensor([sec, h2d, d2h], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t[:1], op=dist.ReduceOp.MAX)
+        dist.all_reduce(t[1:], op=dist.ReduceOp.SUM)
+        sec, h2d, d2h = t.tolist()
+    total = sum(bytes_min(k, *BENCH[k]) for k in kernels)
+    return {"value": total / sec / 1e9, "unit": "GB/s", "ms_per_step": sec * 1e3,
+            "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+            "api": f"ShardedRunner on {suite.world} ranks, every rank's shard from / to pinned host memory"}
+
+
 def run_gpu_arm(args) -> int:
     import torch
     import torch.distributed as dist
@@ -427,6 +491,12 @@ def run_gpu_arm(args) -> int:
         vals = t.tolist()
         total_ms = vals[0]
         per_ms = dict(zip(kernels, vals[1:]))
+    sharded_e2e = None
+    if (world > 1 or os.environ.get("BTO_BENCH_SHARDED_E2E")) and not args.no_e2e:
+        try:
+            sharded_e2e = e2e_sharded(torch, dist, suite, kernels, steps=max(1, min(args.steps, 3)), warmup=1)
+        except Exception as exc:  # e.g. not enough pinned host memory
+            sharded_e2e = {"value": None, "error": f"{type(exc).__name__}: {exc}"}
     if rank != 0:
         if world > 1:
             dist.destroy_process_group()
@@ -476,7 +546,9 @@ def run_gpu_arm(args) -> int:
         "gpu_launches": launches,
     }
     line["suite_frac_of_peak"] = round(value / (peak * world), 4)
-    if world == 1 and not args.no_e2e:
+    if sharded_e2e is not None:
+        line["e2e"] = sharded_e2e
+    elif world == 1 and not args.no_e2e:
         try:
             line["e2e"] = e2e_host(torch, kernels, steps=max(1, min(args.steps, 3)), warmup=1)
         except Exception as exc:  # e.g. not enough pinned host memory
