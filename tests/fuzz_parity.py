@@ -36,6 +36,11 @@ while time.time() < t_end:
     inputs = bto.random_inputs(g, ext, seed=cases)
     want = oracle.oracle_run(name, inputs, ext, threads=rng.choice([1, 4, 8]))
     host = rng.random() < 0.3
+    from paper_1205_1098_b200.colmajor import COLMAJOR_SEQUENCES
+    colmajor = name in COLMAJOR_SEQUENCES and rng.random() < 0.25
+    if colmajor:        # same logical kernel on F-ordered operands: fused, roles swapped (colmajor.py)
+        from paper_1205_1098_b200 import spec as bspec
+        g = bspec.infer_shapes(bspec.parse_kernel(bspec.CORPUS[name].replace("matrix(row)", "matrix(column)")))
     if host:
         got = bto.run_kernel(bto.library_path(), bto.gpu_kernel(g), g, inputs, ext)
     else:
@@ -50,7 +55,8 @@ while time.time() < t_end:
     cases += 1
     if bad:
         fails += 1
-        print("MISMATCH", name, ext, tune, "host" if host else "device", f"err={err:.3e}", flush=True)
+        print("MISMATCH", name, ext, tune, "host" if host else "device", "colmajor" if colmajor else "",
+              f"err={err:.3e}", flush=True)
 _native.set_tuning(mv_rows=0, mv_vec=0, grid_per_sm=0, mv_minb=0, skinny=1, vec_unroll=2, atax_fused=1)
 print(f"{cases} cases, {fails} mismatches")
 sys.exit(1 if fails else 0)
