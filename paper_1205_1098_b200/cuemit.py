@@ -194,10 +194,11 @@ JOIN_COLS = 32                # columns per CTA of a join kernel
 class _Emitter:
     def __init__(self, ir: dict, blocks: int, optimize: bool = True, jam: int = JAM,
                  unroll: int = 4, threads: int = CTA_THREADS, minb: int = 2, bypass_l1: int = 1,
-                 sync: int = 0):
+                 sync: int = 0, auto: int = 1):
         self.jam, self.unroll, self.threads, self.minb = int(jam), int(unroll), int(threads), int(minb)
         self.bypass_l1 = bool(bypass_l1)
         self.sync = bool(sync)
+        self.auto = bool(auto)         # per-region launch shapes (region_shape) may override the above
         self.ir = ir
         self.st = ir["storage"]
         self.ops = ir["ops"]
@@ -403,6 +404,37 @@ class _Emitter:
                 return False
             lanes += 1
         return lanes > 0
+
+    # Launch shape of a region that reads a 2-D operand in TWO strided loops of the same outer
+    # iteration (ATAX: the row dot, then the row again for the column sums): the second read
+    # should come from L2, so the rows in flight (CTAs x jam x row bytes) must fit it -- few,
+    # large CTAs and two rows per batch: 296 CTAs x 2 x 64 KiB = 38 MB at N = 8192.
+    # B200 sweep (scripts/emit_atax_sweep.py): 0.182 -> 0.120 ms for the max-fuse ATAX at n = 8192.
+    REREAD_SHAPE = {"jam": 2, "unroll": 4, "threads": 512, "minb": 2, "bypass_l1": False, "per_sm": 2}
+
+    def rereads(self, items: list) -> bool:
+        for it in items:
+            if it["t"] != "loop" or self.is_innermost(it):
+                continue
+            seen = set()
+            for inner in it["body"]:
+                if inner["t"] == "loop" and self.is_innermost(inner):
+                    mats = {n for st in inner["body"] if st["role"] == "compute"
+                            for n in self.ops[str(st["op"])]["operands"]
+                            if len(self.st[n]["labels"]) == 2 and self.st[n]["cls"] != "contracted"}
+                    if mats & seen:
+                        return True
+                    seen |= mats
+            if self.rereads(it["body"]):
+                return True
+        return False
+
+    def region_shape(self, root: dict):
+        """Per-region override of (jam, unroll, threads, minb, bypass_l1) and the CTAs per SM cap;
+        None: the emitter's own settings."""
+        if self.optimize and self.auto and self.rereads(root["body"]):
+            return dict(self.REREAD_SHAPE)
+        return None
 
     def _lane_loops(self, items: list):
         for it in items:
@@ -950,6 +982,11 @@ class _Emitter:
             fname = f"{kname}_region{regions}"
             nb = f"nb{regions}_"
             regions += 1
+            saved = (self.jam, self.unroll, self.threads, self.minb, self.bypass_l1)
+            shape = self.region_shape(root)
+            if shape:
+                self.jam, self.unroll, self.threads = shape["jam"], shape["unroll"], shape["threads"]
+                self.minb, self.bypass_l1 = shape["minb"], shape["bypass_l1"]
             self.begin_launch(root["body"], True)
             # When the strided (innermost) loops run over the block's own slice, a
             # slice narrower than the CTA leaves threads idle: cap the block count
@@ -966,6 +1003,10 @@ class _Emitter:
                                 f"if ({nb} < {org_t}) {nb} = {org_t}; if ({nb} > {t}) {nb} = {t};")
             else:
                 launches.append(f"long {nb} = {t};")
+            if shape:
+                uses_smem = True                     # (sms_ is read from the device below)
+                launches.append(f"{{ long cap_ = (long)sms_ * {shape['per_sm']}; if (cap_ < {org_t}) cap_ = {org_t}; "
+                                f"if ({nb} > cap_) {nb} = cap_; }}")
             ax, ext = root["axis"], root["extent"]
             smem_args = ""
             strip = self.strip_mappable(root["body"], root["axis"])
@@ -1389,15 +1430,15 @@ class EmitModel:
     peak_gbs: float = 6500.0        # HBM ceiling of a full grid
     cta_gbs: float = 97.5          # what one CTA streams on its own
     launch_us: float = 6.0         # per kernel launch (incl. its share of the final sync)
-    step_us: float = 0.53           # one strided-loop execution that ends in a barrier / CTA reduction
+    step_us: float = 0.50           # one strided-loop execution that ends in a barrier / CTA reduction
     free_step_us: float = 0.0       # ... that ends in neither (barrier analysis removed them)
     trip_us: float = 0.17           # one trip of a thread through a strided loop
-    jam_trip_us: float = 0.31       # the same per row when rows are batched (unroll-and-jam; a trip then
+    jam_trip_us: float = 0.30       # the same per row when rows are batched (unroll-and-jam; a trip then
                                     # carries `unroll` elements per row, hence the larger figure)
     rmw_trip_us: float = 0.14       # a trip that read-modify-writes global memory
-    stmt_us: float = 0.81           # a uniform statement that writes memory and needs its barrier
-    free_stmt_us: float = 0.06      # ... and does not
-    alloc_us: float = 0.04           # stream-ordered malloc + free of one temporary / partial per call
+    stmt_us: float = 0.84           # a uniform statement that writes memory and needs its barrier
+    free_stmt_us: float = 0.07      # ... and does not
+    alloc_us: float = 0.01           # stream-ordered malloc + free of one temporary / partial per call
                                     # (the reference pays malloc/free per call too, cemit.py:183-202)
     sm_count: int = 148
 
@@ -1497,6 +1538,11 @@ def estimate_cost_ir(ir: dict, extents: dict, model: EmitModel | None = None,
         flush_serial()
         org_t = float(ir["threads"][root["slot"]])
         nb = max(org_t, float(blocks))
+        saved = (em.jam, em.unroll, em.threads, em.minb, em.bypass_l1)
+        shape = em.region_shape(root)
+        if shape:                                     # the emitter's per-region launch shape
+            em.jam, em.unroll, em.threads = shape["jam"], shape["unroll"], shape["threads"]
+            nb = min(nb, max(org_t, float(m.sm_count * shape["per_sm"])))
         em.begin_launch(root["body"], True)
         if em.has_sliced_lane_loop(root["body"]):
             nb = min(nb, max(org_t, float(int(ext[root["extent"]]) // em.threads)))
@@ -1523,6 +1569,7 @@ def estimate_cost_ir(ir: dict, extents: dict, model: EmitModel | None = None,
             launches += 1
         strip["axis"], strip["count"] = None, 1.0
         em.row_accs = {}
+        em.jam, em.unroll, em.threads, em.minb, em.bypass_l1 = saved
         launches += 1
         for result in root["partials"]:          # join: read nb partial rows, write the result
             p = st[em.partial_for(result)]

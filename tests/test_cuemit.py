@@ -74,7 +74,11 @@ def test_structure_of_the_bicgk_max_fuse_kernel():
     # grid); the contracted row value is an array over the jammed rows, the column partial lives
     # in shared memory when it fits
     atax = cuemit.emit_cuda(next(i for i in IRS["atax"] if i["organism"].startswith("{_{p(i)}{_i{_j 1}{_j 2}}}"))).source
-    assert "double t0_s_a[4];" in atax and "double &t0_s = t0_s_a[r_];" in atax
+    # ... and, because A is read by both loops, the L2-friendly launch shape: two rows per batch,
+    # 512-thread CTAs, two CTAs per SM
+    assert "double t0_s_a[2];" in atax and "double &t0_s = t0_s_a[r_];" in atax
+    assert "__launch_bounds__(512, 2) atax_region0" in atax and "long cap_ = (long)sms_ * 2;" in atax
+    assert "double t0_s_a[4];" in cuemit.emit_cuda(IRS["atax"][0], auto=0).source
     assert "double *y_part_l = sm_ok_ ? dyn_ + (0) : y_part + p_ * (N);" in atax
     assert "y_part[p_ * (N) + j] = y_part_l[j];" in atax and "blockIdx.y" not in atax
     # a region whose statements are all element-wise in the strided axis needs no row join at all
