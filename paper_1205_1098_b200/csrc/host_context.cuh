@@ -72,6 +72,7 @@ struct Tuning {
     long pdl = 1;            // joins launched as programmatic dependents of their producer
     long debug = 0;          // print launch plans to stderr
     long exchange_phases = 3;    // bit 0 publish, bit 1 wait+reduce (tests emulate ranks with 1, 2)
+    long rowstream = 1;          // GESUMMV on wide matrices streams whole rows (rowstream_kernels.cuh)
     long skinny = 1;             // N <= 256: rows shared by L threads (skinny_kernels.cuh)
     long host_bounce = 1;        // pageable operands >= 16 MiB go through pinned bounce slots
     long host_nt = 1;            // non-temporal stores in the host-side bounce copies

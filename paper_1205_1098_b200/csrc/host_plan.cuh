@@ -4,6 +4,7 @@
 #include "host_context.cuh"
 #include "mv_kernels.cuh"
 #include "skinny_kernels.cuh"
+#include "rowstream_kernels.cuh"
 #include "vec_kernels.cuh"
 
 namespace bto_host {
@@ -335,10 +336,16 @@ struct Pass {
     size_t off_row = 0, off_row2 = 0, off_col = 0;
     long M = 0, N = 0;
 
+    bool rowstream = false;        // whole-row streaming (rowstream_kernels.cuh), N-products only
+
     int prepare(DeviceCtx &c, long m, long n, bool aligned, WsLayout *lay)
     {
         M = m;
         N = n;
+        // two-matrix row dots of a wide matrix: stream whole rows (7.3 vs 6.9-7.07 TB/s at n = 24576)
+        rowstream = FLAGS == (kFlagN | kFlagN2) && aligned && g_tuning.rowstream != 0 &&
+                    n >= 4096 && m >= 4L * c.sm_count;
+        if (rowstream) return BTO_OK;
         // (a full 512-column strip of a rank-2 pass is mv_tile_kernel's best case: 5.9 vs 4.9 TB/s)
         if (skinny_applies(N, aligned) && !((FLAGS & kFlagRank2) && N == kSkinnyMaxN)) {
             skinny = plan_skinny(c, M, N, aligned);
@@ -356,6 +363,30 @@ struct Pass {
     // through f.cmode.
     int run(DeviceCtx &c, MvArgs a, FinArgs f, cudaStream_t stream) const
     {
+        if constexpr (FLAGS == (kFlagN | kFlagN2)) {
+            if (rowstream) {
+                RowStreamArgs r{};
+                r.A = a.A; r.A2 = a.A2; r.colw = a.colw; r.fin = f; r.M = M; r.N = N;
+                const long per_sm = g_tuning.grid_per_sm > 0 ? g_tuning.grid_per_sm : 4;
+                const long target = (long)c.sm_count * per_sm;
+                long rows = (M + target - 1) / target;
+                rows = ((rows + kRsRows - 1) / kRsRows) * kRsRows;
+                r.rows_per_cta = rows;
+                const long grid = (M + rows - 1) / rows;
+                cudaLaunchConfig_t cfg;
+                memset(&cfg, 0, sizeof(cfg));
+                cfg.gridDim = dim3((unsigned)grid, 1, 1);
+                cfg.blockDim = dim3(kRsThreads, 1, 1);
+                cfg.stream = stream;
+                cudaLaunchAttribute attr[1];
+                attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+                attr[0].val.programmaticStreamSerializationAllowed = g_tuning.pdl ? 1 : 0;
+                cfg.attrs = attr;
+                cfg.numAttrs = 1;
+                CUDA_TRY(cudaLaunchKernelEx(&cfg, rowstream_kernel<true>, r));
+                return check_launch("rowstream_kernel");
+            }
+        }
         if (skinny.grid > 0) {
             a.M = M;
             a.N = N;

@@ -405,6 +405,26 @@ def test_extreme_aspect_ratios(bto_lib, oracle, shape):
         _native.set_tuning(skinny=1)
 
 
+@pytest.mark.parametrize("shape", [(600, 4096), (1001, 4098), (593, 6002), (2500, 9000), (4097, 4100)])
+def test_gesummv_row_streaming(bto_lib, oracle, shape):
+    """Wide GESUMMV streams whole rows (rowstream_kernels.cuh) instead of column strips: one
+    launch, no partials; checked against the oracle with that path on and off."""
+    m, n = shape
+    g = bto.load_graph("gesummv")
+    ext = {"M": m, "N": n}
+    inputs = bto.random_inputs(g, ext, seed=n)
+    want = oracle.oracle_run("gesummv", inputs, ext, threads=8)
+    try:
+        for on in (1, 0):
+            _native.set_tuning(rowstream=on)
+            before = _native.kernel_launches()
+            got = run_device("gesummv", inputs, ext)
+            assert _native.kernel_launches() - before == (1 if on else 2)
+            assert_matches("gesummv", got, want, ext, f"rowstream={on}")
+    finally:
+        _native.set_tuning(rowstream=1)
+
+
 def test_column_major_corpus_kernels_stay_fused(bto_lib, oracle):
     """`matrix(column)` operands: the same logical kernel, the
     buffers are F-ordered.  The library maps every corpus sequence onto its row-major fused
