@@ -57,7 +57,9 @@ def main(rep, launches, out):
     lines += ["", "## launch list (`--metrics gpu__time_duration.sum`, last step)", "",
               "| # | kernel | grid | ms | share of step |", "|---|---|---|---|---|"]
     lrows = [r for r in csv.DictReader(l for l in open(launches) if l.startswith('"'))]
-    last = lrows[-11:]
+    # the last step: everything from the last vec_kernel (AXPYDOT opens a step) on
+    start = max(i for i, r in enumerate(lrows) if 'vec_kernel' in r['Kernel Name'])
+    last = lrows[start:]
     total = sum(float(r["Metric Value"].replace(",", "")) for r in last)
     for r in last:
         ns = float(r["Metric Value"].replace(",", ""))
