@@ -372,13 +372,15 @@ def e2e_host(torch, kernels, steps: int, warmup: int) -> dict:
     for _ in range(warmup):
         step()
     torch.cuda.synchronize()
-    t0 = time.perf_counter()
+    times = []
     for _ in range(steps):
-        step()
-    torch.cuda.synchronize()
-    sec = (time.perf_counter() - t0) / steps
+        t0 = time.perf_counter()
+        step()                                   # every call returns with its outputs on the host
+        times.append(time.perf_counter() - t0)
+    sec = statistics.median(times)               # (host-side hiccups: one step in ten runs 10 % long)
     total = sum(bytes_min(k, *BENCH[k]) for k in kernels)
     return {"value": total / sec / 1e9, "unit": "GB/s", "ms_per_step": sec * 1e3,
+            "step_ms": [round(t * 1e3, 2) for t in times], "timing": "median step, wall clock",
             "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
             "api": f"C symbols of include/bto_b200.h section 1 with {host_kind[0]} host pointers"}
 
