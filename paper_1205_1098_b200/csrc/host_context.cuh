@@ -78,7 +78,7 @@ struct Tuning {
     long host_nt = 1;            // non-temporal stores in the host-side bounce copies
     long host_threads = 0;       // host threads copying into / out of the bounce slots (0 = auto)
     long host_pipeline = 1;  // overlap H2D / compute / D2H in row panels for host operands
-    long host_panel_mib = 256;   // panel size of that pipeline
+    long host_panel_mib = 64;    // panel size of that pipeline
 };
 
 struct DeviceCtx {

@@ -255,7 +255,7 @@ def test_host_operand_pipeline(bto_lib, oracle):
         assert_matches("gemver", run_host("gemver", inputs, ext),
                        oracle.oracle_run("gemver", inputs, ext, threads=8), ext, "unpipelined")
     finally:
-        _native.set_tuning(host_pipeline=1, host_panel_mib=256)
+        _native.set_tuning(host_pipeline=1, host_panel_mib=64)
 
 
 def test_pageable_host_operands_bounce(bto_lib, oracle):
@@ -280,7 +280,7 @@ def test_pageable_host_operands_bounce(bto_lib, oracle):
         assert_matches("gemver", run_host("gemver", inputs, ext),
                        oracle.oracle_run("gemver", inputs, ext, threads=8), ext, "no bounce")
     finally:
-        _native.set_tuning(host_bounce=1, host_threads=0, host_panel_mib=256)
+        _native.set_tuning(host_bounce=1, host_threads=0, host_panel_mib=64)
 
 
 def test_reference_style_ctypes_binding(bto_lib, oracle):
