@@ -55,7 +55,7 @@ rowstream_kernel(const RowStreamArgs a)
 #pragma unroll
             for (int u = 0; u < U; ++u) {
                 const long jj = j + 2L * u * kRsThreads;
-                x[u] = *reinterpret_cast<const double2 *>(a.colw + jj);
+                x[u] = make_double2(__ldg(a.colw + jj), __ldg(a.colw + jj + 1));   // (x may sit at any 8-byte offset)
 #pragma unroll
                 for (int i = 0; i < R; ++i) {
                     e[i][u] = ld_stream2<true>(a.A + row[i] * N + jj);
@@ -76,7 +76,7 @@ rowstream_kernel(const RowStreamArgs a)
             }
         }
         for (; j + 1 < N; j += 2L * kRsThreads) {           // what is left of the row (pairs)
-            const double2 x = *reinterpret_cast<const double2 *>(a.colw + j);
+            const double2 x = make_double2(__ldg(a.colw + j), __ldg(a.colw + j + 1));
 #pragma unroll
             for (int i = 0; i < R; ++i) {
                 const double2 e = ld_stream2<true>(a.A + row[i] * N + j);

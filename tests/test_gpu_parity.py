@@ -421,6 +421,14 @@ def test_gesummv_row_streaming(bto_lib, oracle, shape):
             got = run_device("gesummv", inputs, ext)
             assert _native.kernel_launches() - before == (1 if on else 2)
             assert_matches("gesummv", got, want, ext, f"rowstream={on}")
+        # x at an odd 8-byte offset next to 16-byte-aligned matrices
+        dev = {k: (torch.from_numpy(v).cuda() if isinstance(v, np.ndarray) else v) for k, v in inputs.items()}
+        shifted = torch.empty(n + 1, dtype=torch.float64, device="cuda")[1:]
+        shifted.copy_(dev["x"])
+        assert shifted.data_ptr() % 16 == 8
+        dev["x"] = shifted
+        out = bto.run_kernel(bto.library_path(), bto.gpu_kernel(g), g, dev, ext)
+        assert_matches("gesummv", {k: v.cpu().numpy() for k, v in out.items()}, want, ext, "misaligned x")
     finally:
         _native.set_tuning(rowstream=1)
 
