@@ -161,6 +161,11 @@ def hbm_traffic(kernel: str, M: int, N: int, variant: GpuVariant | None = None,
         fused = variant.get("atax_fused", 1) and N % 2 == 0 and N <= 16 * 8192
         seq = "atax" if fused else "atax2"
     passes, partials, rereads = [], 0.0, 0.0
+    joins = 0
+    if kernel in ("atax", "batax") and N <= 512 and variant.get("skinny", 1):
+        # shared-row kernel (csrc/skinny_kernels.cuh): single pass, one partial row per CTA
+        grid = machine.sm_count * (variant.get("grid_per_sm") or 4)
+        return Traffic(algo, 0.0, 2 * 8.0 * grid * N, 2, (("N", 8.0 * M * N, 0.0, 128 * 1024),))
     for idx, (kind, reads, writes) in enumerate(_SEQUENCE[seq]):
         if kind == "ATAX":
             c = variant.get("atax_cluster") or next(c for c in (1, 2, 4, 8, 16)
@@ -170,14 +175,24 @@ def hbm_traffic(kernel: str, M: int, N: int, variant: GpuVariant | None = None,
             passes.append((kind, 8.0 * M * N, 0.0, 64 * 1024))
             continue
         nstrips, slots, inflight = _pass_geometry(kind, variant, machine, M, N)
-        if "N" in kind:
-            partials += 2 * 8.0 * nstrips * M * (2 if kind == "NN" else 1)
-        if "T" in kind:
-            partials += 2 * 8.0 * slots * N
+        if N <= 512 and variant.get("skinny", 1):
+            # shared-row kernels: row results written in-kernel, one partial row per CTA for T
+            if "T" in kind:
+                partials += 2 * 8.0 * machine.sm_count * (variant.get("grid_per_sm") or 4) * N
+                joins += 1
+        elif kind == "NN" and N >= 4096 and M >= 4 * machine.sm_count and variant.get("rowstream", 1):
+            pass                        # whole-row streaming (csrc/rowstream_kernels.cuh): no partials, no join
+        else:
+            if "N" in kind:
+                partials += 2 * 8.0 * nstrips * M * (2 if kind == "NN" else 1)
+            if "T" in kind:
+                partials += 2 * 8.0 * slots * N
+            joins += 1
         passes.append((kind, 8.0 * M * N * reads, 8.0 * M * N * writes, inflight))
         if seq == "atax2" and idx == 1:
             rereads += 8.0 * M * N
-    return Traffic(algo, rereads, partials, 2 * len(passes), tuple(passes))
+    joins += sum(1 for k, *_ in passes if k == "ATAX")
+    return Traffic(algo, rereads, partials, len(passes) + joins, tuple(passes))
 
 
 def estimate_cost(variant: GpuVariant, graph, machine: GpuMachineModel) -> CostReport:
