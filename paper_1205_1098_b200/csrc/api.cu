@@ -557,8 +557,9 @@ int bto_set_tuning(const char *key, long value)
     if (slot == &g_tuning.mv_minb) ok = value == 0 || value == 1 || value == 2 || value == 3 || value == 4 || value == 6;
     if (slot == &g_tuning.mv_vec) ok = value == 0 || value == 1 || value == 2;
     if (slot == &g_tuning.vec_unroll) ok = value == 1 || value == 2 || value == 4;
-    if (slot == &g_tuning.atax_fused || slot == &g_tuning.host_pipeline || slot == &g_tuning.host_bounce || slot == &g_tuning.host_nt || slot == &g_tuning.skinny || slot == &g_tuning.rowstream) ok = value == 0 || value == 1;
+    if (slot == &g_tuning.atax_fused || slot == &g_tuning.host_pipeline || slot == &g_tuning.host_bounce || slot == &g_tuning.host_nt || slot == &g_tuning.skinny) ok = value == 0 || value == 1;
     if (slot == &g_tuning.host_threads) ok = value >= 0 && value <= 64;
+    if (slot == &g_tuning.rowstream) ok = value >= 0 && value <= 2;
     if (slot == &g_tuning.host_panel_mib) ok = value >= 1 && value <= 4096;
     if (slot == &g_tuning.exchange_phases) ok = value >= 1 && value <= 3;
     if (slot == &g_tuning.atax_cluster) ok = value == 0 || value == 1 || value == 2 || value == 4 || value == 8 || value == 16;

@@ -343,8 +343,8 @@ struct Pass {
         M = m;
         N = n;
         // two-matrix row dots of a wide matrix: stream whole rows (7.3 vs 6.9-7.07 TB/s at n = 24576)
-        rowstream = FLAGS == (kFlagN | kFlagN2) && aligned && g_tuning.rowstream != 0 &&
-                    n >= 4096 && m >= 4L * c.sm_count;
+        rowstream = (FLAGS == (kFlagN | kFlagN2) || (FLAGS == kFlagN && g_tuning.rowstream == 2)) &&
+                    aligned && g_tuning.rowstream != 0 && n >= 4096 && m >= 4L * c.sm_count;
         if (rowstream) return BTO_OK;
         // (a full 512-column strip of a rank-2 pass is mv_tile_kernel's best case: 5.9 vs 4.9 TB/s)
         if (skinny_applies(N, aligned) && !((FLAGS & kFlagRank2) && N == kSkinnyMaxN)) {
@@ -363,7 +363,7 @@ struct Pass {
     // through f.cmode.
     int run(DeviceCtx &c, MvArgs a, FinArgs f, cudaStream_t stream) const
     {
-        if constexpr (FLAGS == (kFlagN | kFlagN2)) {
+        if constexpr (FLAGS == (kFlagN | kFlagN2) || FLAGS == kFlagN) {
             if (rowstream) {
                 RowStreamArgs r{};
                 r.A = a.A; r.A2 = a.A2; r.colw = a.colw; r.fin = f; r.M = M; r.N = N;
@@ -383,7 +383,7 @@ struct Pass {
                 attr[0].val.programmaticStreamSerializationAllowed = g_tuning.pdl ? 1 : 0;
                 cfg.attrs = attr;
                 cfg.numAttrs = 1;
-                CUDA_TRY(cudaLaunchKernelEx(&cfg, rowstream_kernel<true>, r));
+                CUDA_TRY(cudaLaunchKernelEx(&cfg, rowstream_kernel<(FLAGS & kFlagN2) != 0>, r));
                 return check_launch("rowstream_kernel");
             }
         }
