@@ -1192,14 +1192,20 @@ DEFAULT_TEMPLATE = "{cc} -O3 -std=c++17 -gencode arch=compute_100a,code=sm_100a 
 
 @dataclass
 class NvccToolchain:
+    """`cache_dir` (or $BTO_NVCC_CACHE): compiled translation units are kept there under the hash of
+    (source, command), so a search that meets the same organism and launch shape again -- or a
+    second process -- skips nvcc (3-5 s per kernel)."""
     cc: str | None = None
     template: str = ""
+    cache_dir: str | None = None
 
     def __post_init__(self):
         if not self.cc:
             self.cc = os.environ.get("BTO_NVCC") or shutil.which("nvcc") or "/usr/local/cuda/bin/nvcc"
         if not self.template:
             self.template = os.environ.get("BTO_NVCC_TEMPLATE", DEFAULT_TEMPLATE)
+        if self.cache_dir is None:
+            self.cache_dir = os.environ.get("BTO_NVCC_CACHE") or None
 
     @property
     def available(self) -> bool:
@@ -1215,9 +1221,24 @@ class NvccToolchain:
         cmd = shlex.split(self.template.format(cc=self.cc, src=src, bin=binary))
         if shared:       # nvcc does not take -fPIC directly
             cmd += ["-shared", "-Xcompiler", "-fPIC"]
+        cached = None
+        if self.cache_dir:
+            import hashlib
+            key = hashlib.sha256((source + "\0" + self.template + "\0" + str(shared)).encode()).hexdigest()[:32]
+            cached = Path(self.cache_dir) / (key + (".so" if shared else ".bin"))
+            if cached.exists():
+                shutil.copyfile(cached, binary)
+                if not shared:
+                    binary.chmod(0o755)
+                return binary
         proc = subprocess.run(cmd, capture_output=True, text=True)
         if proc.returncode != 0:
             raise ToolchainError(f"compile failed ({' '.join(cmd)}):\n{proc.stderr.strip()}")
+        if cached is not None:
+            cached.parent.mkdir(parents=True, exist_ok=True)
+            tmp = cached.with_suffix(cached.suffix + f".{os.getpid()}.tmp")
+            shutil.copyfile(binary, tmp)
+            os.replace(tmp, cached)                  # atomic: concurrent searches may share the cache
         return binary
 
 

@@ -119,6 +119,21 @@ def test_emitted_cuda_compiles_for_sm_100a(tmp_path):
     assert all(path.exists() for _, _, path in built)
 
 
+def test_compile_cache_skips_nvcc(tmp_path):
+    """A second compile of the same source comes from the cache (no nvcc run)."""
+    import time
+    k = cuemit.emit_cuda(IRS["vadd"][0])
+    tc = cuemit.NvccToolchain(cache_dir=str(tmp_path / "cache"))
+    if not tc.available:
+        pytest.skip("no nvcc")
+    t0 = time.perf_counter(); first = tc.compile(k.source, tmp_path, name="a"); t1 = time.perf_counter()
+    second = tc.compile(k.source, tmp_path, name="b"); t2 = time.perf_counter()
+    assert first.read_bytes() == second.read_bytes() and len(list((tmp_path / "cache").iterdir())) == 1
+    assert (t2 - t1) < 0.5 * (t1 - t0)
+    other = tc.compile(k.source.replace("vadd_region0", "vadd_region0x"), tmp_path, name="c")
+    assert other.exists() and len(list((tmp_path / "cache").iterdir())) == 2
+
+
 def test_compile_failure_is_reported(tmp_path):
     if not cuemit.NvccToolchain().available:
         pytest.skip("nvcc not available")
