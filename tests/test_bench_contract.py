@@ -1,0 +1,65 @@
+"""bench.py's JSON line against the driver's contract, checked on the committed line of the
+round's final run (profiles/r01/bench_v11_final.json) and on the reference arm's code path
+(which runs on CPU: the oracle / oracle/_ref, a bounded sample)."""
+from __future__ import annotations
+
+import json
+import subprocess
+import sys
+from pathlib import Path
+
+import pytest
+
+REPO = Path(__file__).resolve().parent.parent
+FINAL = REPO / "profiles" / "r01" / "bench_v11_final.json"
+
+
+def _line(text: str) -> dict:
+    return json.loads(text.strip().splitlines()[-1])
+
+
+def test_committed_bench_line_has_every_contract_key():
+    d = _line(FINAL.read_text())
+    for key in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better",
+                "scaling", "vs_baseline", "dtype", "data", "config", "roofline", "cpu_baseline", "e2e",
+                "clocks", "gpu_launches"):
+        assert key in d, key
+    assert d["unit"] == "GB/s" and d["higher_is_better"] is True and d["vs_baseline"] is None
+    assert d["dtype"] == "f64" and d["data"] == "synthetic" and d["n_gpus"] == 1
+    assert "workload" in d["config"] and "model" not in d["config"]
+    r = d["roofline"]
+    assert r["bound"] == "hbm" and r["unit"] == "GB/s" and abs(r["frac"] - r["achieved"] / r["peak"]) < 1e-3
+    assert r["traffic"] is None or 0.9 < r["traffic"] / r["algorithmic_bytes"] < 1.1     # no wasted re-reads
+    c = d["cpu_baseline"]
+    assert c["kind"] in ("reference", "port") and c["cores"] >= 1 and c["value"] > 0 and c["sample"]
+    e = d["e2e"]
+    assert e["value"] > 0 and e["h2d_bytes_per_step"] > 0 and e["d2h_bytes_per_step"] > 0
+    assert e["value"] < d["value"]                      # PCIe-bound: never the device-resident figure
+    assert d["gpu_launches"] > 0 and d["steps"] >= 1 and d["warmup"] >= 3
+    assert set(d["clocks"]) >= {"sm_mhz", "sm_max_mhz", "reasons"}
+    bad = {"hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown"}
+    assert not bad & set(d["clocks"]["reasons"])
+    # the time-based value is consistent with the per-step time and the suite's algorithmic bytes
+    total = sum(v["bytes_min"] for v in d["per_kernel"].values())
+    assert abs(d["value"] - total / (d["ms_per_step"] * 1e-3) / 1e9) < 0.01 * d["value"]
+
+
+def test_reference_arm_runs_on_cpu_and_prints_the_contract_line():
+    """`bench.py --impl reference` times the reference's generated C (oracle/_ref) or the oracle
+    port on the host cores; one AXPYDOT step of the bounded sample keeps this test short."""
+    proc = subprocess.run([sys.executable, str(REPO / "bench.py"), "--impl", "reference", "--kernel", "axpydot",
+                           "--steps", "1", "--warmup", "1"], capture_output=True, text=True, timeout=600)
+    assert proc.returncode == 0, proc.stderr[-2000:]
+    d = _line(proc.stdout)
+    assert d["impl"] == "reference" and d["unit"] == "GB/s" and d["value"] > 0
+    assert d["cpu_baseline"]["kind"] in ("reference", "port") and d["cpu_baseline"]["value"] == d["value"]
+    assert d["e2e"] == {"value": d["value"], "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}
+    assert d["gpu_launches"] == 0
+
+
+def test_other_ranks_of_the_reference_arm_exit_without_work():
+    import os
+    env = dict(os.environ, RANK="1", WORLD_SIZE="2")
+    proc = subprocess.run([sys.executable, str(REPO / "bench.py"), "--impl", "reference", "--gpus", "2"],
+                          capture_output=True, text=True, timeout=120, env=env)
+    assert proc.returncode == 0 and proc.stdout.strip() == ""
