@@ -63,3 +63,21 @@ def test_other_ranks_of_the_reference_arm_exit_without_work():
     proc = subprocess.run([sys.executable, str(REPO / "bench.py"), "--impl", "reference", "--gpus", "2"],
                           capture_output=True, text=True, timeout=120, env=env)
     assert proc.returncode == 0 and proc.stdout.strip() == ""
+
+
+@pytest.mark.gpu
+def test_gpu_arm_single_kernel_mode_and_tuning_flag():
+    """`bench.py --kernel gesummv --tune rowstream=0` on the device: one JSON line, the tunable
+    takes effect (two launches per step instead of one)."""
+    lines = {}
+    for flag in ("rowstream=1", "rowstream=0"):
+        proc = subprocess.run([sys.executable, str(REPO / "bench.py"), "--kernel", "gesummv", "--steps", "2",
+                               "--warmup", "3", "--no-e2e", "--no-cpu", "--tune", flag],
+                              capture_output=True, text=True, timeout=600)
+        assert proc.returncode == 0, proc.stderr[-2000:]
+        lines[flag] = _line(proc.stdout)
+    on, off = lines["rowstream=1"], lines["rowstream=0"]
+    assert on["gpu_launches"] == 2 and off["gpu_launches"] == 4
+    for d in (on, off):
+        assert d["n_gpus"] == 1 and d["roofline"]["kernel"] == "gesummv" and 3000 < d["value"] < 9000
+        assert list(d["per_kernel"]) == ["gesummv"]
