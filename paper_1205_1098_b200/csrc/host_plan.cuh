@@ -89,7 +89,7 @@ bool mv_shape_ok(int R, int V)
     if (FLAGS & kFlagN2) return false;
     if (R == 16 && V == 1) return true;
     if (R == 32 && V == 1) return (FLAGS & kFlagN) == 0;
-    if (R == 8 && V == 2) return FLAGS == kFlagN || FLAGS == (kFlagT | kFlagRank2);
+    if (R == 8 && V == 2) return FLAGS == kFlagN || FLAGS == (kFlagT | kFlagRank2) || FLAGS == (kFlagN | kFlagT);
     return false;
 }
 
@@ -102,7 +102,7 @@ MvKernel mv_kernel_ptr(int R, int V, bool aligned, int minb)
         if constexpr ((FLAGS & kFlagN) == 0) {
             if (R == 32 && V == 1) return mv_kernel_minb<FLAGS, 32, 1>(minb);
         }
-        if constexpr (FLAGS == kFlagN || FLAGS == (kFlagT | kFlagRank2)) {
+        if constexpr (FLAGS == kFlagN || FLAGS == (kFlagT | kFlagRank2) || FLAGS == (kFlagN | kFlagT)) {
             if (R == 8 && V == 2) return mv_kernel_minb<FLAGS, 8, 2>(minb);
         }
     }
@@ -117,7 +117,7 @@ struct MvDefault { int rows, vec, grid_per_sm, minb; };
 template <int FLAGS>
 constexpr MvDefault mv_default()
 {
-    if (FLAGS == (kFlagN | kFlagT)) return {8, 1, 8, 4};        // BiCGK         7.10 TB/s
+    if (FLAGS == (kFlagN | kFlagT)) return {8, 2, 8, 2};        // BiCGK         7.07 TB/s (1024-column strips: half the barriers per byte)
     if (FLAGS == (kFlagN | kFlagN2)) return {8, 1, 4, 4};       // GESUMMV       7.04 TB/s
     if (FLAGS == (kFlagT | kFlagRank2)) return {16, 1, 2, 1};   // GEMVER pass 1 6.29 TB/s (r+w)
     if (FLAGS == (kFlagN | kFlagRank2)) return {8, 1, 4, 2};    // column-major GEMVER pass 1 6.38 TB/s (r+w)
