@@ -1,5 +1,5 @@
 """bench.py's JSON line against the driver's contract, checked on the committed line of the
-round's final run (profiles/r01/bench_v11_final.json) and on the reference arm's code path
+round's final run (profiles/r01/bench_v14_final.json) and on the reference arm's code path
 (which runs on CPU: the oracle / oracle/_ref, a bounded sample)."""
 from __future__ import annotations
 
@@ -11,7 +11,7 @@ from pathlib import Path
 import pytest
 
 REPO = Path(__file__).resolve().parent.parent
-FINAL = REPO / "profiles" / "r01" / "bench_v11_final.json"
+FINAL = REPO / "profiles" / "r01" / "bench_v14_final.json"
 
 
 def _line(text: str) -> dict:
