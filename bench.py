@@ -544,12 +544,15 @@ def run_gpu_arm(args) -> int:
                      "frac": round(dom["gbs"] / (peak * world), 4),
                      "traffic": traffic, "traffic_source": traffic_src, "peak_source": peak_src,
                      "algorithmic_bytes": dom["bytes_min"],
+                     "nominal_peak": 8000.0 * world,         # BASELINE.json north_star: ~8 TB/s per GPU
+                     "frac_nominal": round(dom["gbs"] / (8000.0 * world), 4),
                      "peak_note": "the measured peak is a read+write copy; read-dominated kernels "
                                   "reach 7.1-7.5 TB/s on this part, hence fractions above 1"},
         "clocks": clocks.summary(),
         "gpu_launches": launches,
     }
     line["suite_frac_of_peak"] = round(value / (peak * world), 4)
+    line["suite_frac_of_nominal_8tbs"] = round(value / (8000.0 * world), 4)
     if sharded_e2e is not None:
         line["e2e"] = sharded_e2e
     elif world == 1 and not args.no_e2e:
