@@ -1,5 +1,6 @@
 #!/usr/bin/env python
-"""Fused ATAX: correctness across cluster sizes + timing at the bench size (run on a B200)."""
+"""Fused ATAX: correctness across cluster sizes (against the oracle: test infrastructure, hence under tests/)
++ timing at the bench size (run on a B200)."""
 from __future__ import annotations
 
 import statistics
