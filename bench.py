@@ -3,6 +3,7 @@
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
                     [--kernel suite|axpydot|bicgk|atax|gesummv|gemver] [--no-e2e]
+                    [--exchange auto|nccl|fused]
 
 A "step" is one pass of the hot path over the suite: the five fused sequences
 at BASELINE.json's bench sizes (AXPYDOT n=2^27; BiCGK, ATAX, GEMVER n=32768;
@@ -15,14 +16,20 @@ Extra objects on the JSON line: `per_kernel` (achieved GB/s of each sequence),
 `roofline` (the slowest-by-share sequence against MEASURED_PEAKS.json),
 `e2e` (the same suite through the reference-facing C symbols with PINNED HOST
 buffers, copies inside the timed region), `cpu_baseline` (the reference's own
-generated C on this box's cores, bounded sample), `clocks`, `gpu_launches`.
+generated C on this box's cores at the SAME sizes, plus the unfused organism on
+a smaller sample), `clocks`, `gpu_launches`.
 
-N > 1 (torchrun): rows are sharded over ranks (paper_1205_1098_b200.sharded),
-one NCCL all-reduce per kernel, total problem size fixed -> "scaling": "strong".
+N > 1: `python bench.py --gpus N` starts N ranks itself (torchrun's launcher,
+127.0.0.1) when it is not already running under one; it fails loudly when fewer
+than N GPUs are visible.  Rows are sharded over ranks
+(paper_1205_1098_b200.sharded), one exchange per kernel -- fused into the join
+kernel over NVLink peer memory when symmetric memory is available and agrees
+with NCCL on a probe, else one NCCL all-reduce -- and each rank's step is a
+replayed CUDA graph.  Total problem size fixed -> "scaling": "strong".
 
 `--impl reference` times the reference's CPU implementation (oracle/_ref, the
 generated C compiled in the build container; else the oracle port) on the
-host cores, same metric; rank 0 only.
+host cores, same metric, same sizes; rank 0 only.
 """
 from __future__ import annotations
 
@@ -30,7 +37,9 @@ import argparse
 import ctypes
 import json
 import os
+import socket
 import statistics
+import subprocess
 import sys
 import threading
 import time
@@ -42,13 +51,33 @@ sys.path.insert(0, str(REPO))
 SUITE = ("axpydot", "bicgk", "atax", "gesummv", "gemver")
 BENCH = {"axpydot": (1 << 27, 1), "bicgk": (32768, 32768), "atax": (32768, 32768),
          "gesummv": (24576, 24576), "gemver": (32768, 32768)}
-# bounded CPU sample: out of last-level cache, a few seconds on 8 cores
+# fallback when the host cannot hold the bench sizes (needs ~17 GiB): out of last-level cache
 CPU_SAMPLE = {"axpydot": (1 << 26, 1), "bicgk": (16384, 16384), "atax": (16384, 16384),
               "gesummv": (12288, 12288), "gemver": (16384, 16384)}
+# the unfused organism (fuse.py:128 initial_forest) is serial and allocates a matrix per statement
+UNFUSED_SAMPLE = {"axpydot": (1 << 25, 1), "bicgk": (8192, 8192), "atax": (8192, 8192),
+                  "gesummv": (6144, 6144), "gemver": (8192, 8192)}
 
-
+METRIC = "effective HBM GB/s (min bytes/time), fused suite"
 WORKLOAD = ("suite5: AXPYDOT n=2^27, BiCGK n=32768, ATAX n=32768, GESUMMV n=24576, "
             "GEMVER n=32768")
+
+
+def describe(sizes: dict, kernels) -> str:
+    if sizes is BENCH or all(sizes[k] == BENCH[k] for k in kernels):
+        return WORKLOAD if tuple(kernels) == SUITE else \
+            "; ".join(f"{k} at BASELINE bench size {list(BENCH[k])}" for k in kernels)
+    return "REDUCED sizes (not the BASELINE bench sizes): " + \
+        ", ".join(f"{k} {sizes[k][0]}" + ("" if k == "axpydot" else f"x{sizes[k][1]}") for k in kernels)
+
+
+def config_of(kernels, world: int, sizes=BENCH) -> dict:
+    """The `config` object -- identical for the b200 and the reference arm of one run."""
+    return {
+        "workload": describe(sizes, kernels),
+        "parallelism": "unsharded (1 rank)" if world == 1 else f"row-shard x{world} (strong scaling)",
+        "l2": "every input >= 4 GiB >> 126 MB L2 (and any host LLC); no flush between iterations",
+    }
 
 
 def bytes_min(kernel: str, M: int, N: int) -> float:
@@ -127,45 +156,79 @@ class ClockSampler:
 # ---------------------------------------------------------------------------
 # CPU arm: the reference's generated C (oracle/_ref) or the oracle port
 
-def cpu_baseline(steps: int = 2, warmup: int = 1, kernels=SUITE) -> dict:
-    import numpy as np
-    sys.path.insert(0, str(REPO / "tests"))
-    import oracle_lib as O
+def host_cores() -> int:
+    return len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else (os.cpu_count() or 1)
 
-    cores_avail = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") \
-        else (os.cpu_count() or 1)
-    use_ref = O.ref_available()
-    if use_ref:
-        ladder = O.ref_thread_ladder("bicgk")
-        threads = max(t for t in ladder if t <= max(1, cores_avail))
-        kind = "reference"
-    else:
-        O.ensure_built()
-        threads = max(1, cores_avail)
-        kind = "port"
-    rng = np.random.default_rng(0)
-    per = {}
-    tot_bytes = tot_sec = 0.0
+
+def fill_uniform(arr, seed: int, threads: int) -> None:
+    """arr[:] = U[-1,1) with `threads` independent PCG64 streams (numpy releases the GIL)."""
+    import numpy as np
+    from concurrent.futures import ThreadPoolExecutor
+    flat = arr.reshape(-1)
+    piece = 1 << 22
+    jobs = [(lo, min(lo + piece, flat.size)) for lo in range(0, flat.size, piece)]
+
+    def work(job):
+        lo, hi = job
+        view = flat[lo:hi]
+        np.random.Generator(np.random.PCG64([seed, lo])).random(out=view)
+        np.multiply(view, 2.0, out=view)
+        np.subtract(view, 1.0, out=view)
+
+    with ThreadPoolExecutor(max(1, threads)) as pool:
+        list(pool.map(work, jobs))
+
+
+class HostWorkset:
+    """Host operands of the suite at `sizes`: two matrix-sized buffers that every sequence
+    borrows views of (what e2e_host and the CPU arm both run on), plus the vectors."""
+
+    def __init__(self, sizes, kernels, alloc=None, filled: bool = True):
+        import numpy as np
+        self.np = np
+        self.sizes = sizes
+        mats = [sizes[k][0] * sizes[k][1] for k in kernels if k != "axpydot"]
+        need = max(mats + [3 * sizes["axpydot"][0] if "axpydot" in kernels else 0])
+        alloc = alloc or (lambda count: np.empty(count, dtype=np.float64))
+        self.big_in, self.big_out = alloc(need), alloc(need)
+        nmax = max(max(sizes[k]) for k in kernels if k != "axpydot") if mats else 1
+        self.vec = [alloc(nmax) for _ in range(8)]
+        self.outv = [alloc(nmax) for _ in range(3)]
+        self.scalar = alloc(1)
+        if filled:
+            t = host_cores()
+            fill_uniform(self.big_in, 11, t)
+            fill_uniform(self.big_out, 12, t)
+            for i, v in enumerate(self.vec):
+                fill_uniform(v, 20 + i, 1)
+
+    def operands(self, name: str):
+        """(inputs by parameter name, preallocated outputs by name, extents) on views."""
+        M, N = self.sizes[name]
+        bi, bo, v, o = self.big_in, self.big_out, self.vec, self.outv
+        if name == "axpydot":
+            return ({"w": bi[:M], "v": bi[M:2 * M], "u": bi[2 * M:3 * M], "alpha": 0.37},
+                    {"z": bo[:M], "beta": self.scalar}, {"M": M})
+        A = bi[:M * N].reshape(M, N)
+        ext = {"M": M, "N": N}
+        if name == "bicgk":
+            return {"A": A, "p": v[0][:N], "r": v[1][:M]}, {"q": o[0][:M], "s": o[1][:N]}, ext
+        if name == "atax":
+            return {"A": A, "x": v[0][:N]}, {"y": o[0][:N]}, ext
+        if name == "gesummv":
+            return ({"alpha": 0.61, "beta": -0.27, "A": A, "B": bo[:M * N].reshape(M, N), "x": v[0][:N]},
+                    {"y": o[0][:M]}, ext)
+        return ({"A": A, "u1": v[1][:M], "v1": v[2][:N], "u2": v[3][:M], "v2": v[4][:N],
+                 "alpha": 0.83, "beta": -0.41, "y": v[5][:M], "z": v[6][:N]},
+                {"B": bo[:M * N], "x": o[1][:N], "w": o[2][:M]}, ext)
+
+
+def _time_cpu(O, tag_or_threads, use_ref: bool, work: HostWorkset, kernels, steps: int, warmup: int):
+    per, tot_bytes, tot_sec = {}, 0.0, 0.0
     for name in kernels:
-        M, N = CPU_SAMPLE[name]
-        ext = {"M": M} if name == "axpydot" else {"M": M, "N": N}
-        inputs = {}
-        for pname, cls in O.PARAMS[name]:
-            if cls == "s":
-                inputs[pname] = float(rng.uniform(-1, 1))
-            elif cls == "a":
-                if pname in ("A", "B"):
-                    shape = (M, N)
-                elif name == "axpydot":
-                    shape = (M,)
-                else:
-                    rowvec = {"bicgk": ("r",), "gemver": ("u1", "u2", "y")}.get(name, ())
-                    shape = (M,) if pname in rowvec else (N,)
-                arr = np.empty(shape)
-                arr.ravel()[:] = rng.random(arr.size) * 2 - 1
-                inputs[pname] = arr
-        run, _ = O.bind_ref(name, inputs, ext, f"t{threads}") if use_ref else \
-            O.bind_oracle(name, inputs, ext, threads)
+        inputs, outputs, ext = work.operands(name)
+        run, _ = O.bind_ref(name, inputs, ext, tag_or_threads, outputs) if use_ref else \
+            O.bind_oracle(name, inputs, ext, tag_or_threads, outputs)
         for _ in range(warmup):
             run()
         times = []
@@ -174,16 +237,79 @@ def cpu_baseline(steps: int = 2, warmup: int = 1, kernels=SUITE) -> dict:
             run()
             times.append(time.perf_counter() - t0)
         sec = statistics.mean(times)
+        M, N = work.sizes[name]
         b = bytes_min(name, M, N)
-        per[name] = {"gbs": b / sec / 1e9, "ms": sec * 1e3, "extents": [M, N]}
+        per[name] = {"gbs": b / sec / 1e9, "ms": sec * 1e3, "ms_min": min(times) * 1e3, "extents": [M, N]}
         tot_bytes += b
         tot_sec += sec
-        del inputs
-    return {"value": tot_bytes / tot_sec / 1e9, "unit": "GB/s", "cores": threads,
-            "kind": kind, "ms_per_step": tot_sec * 1e3, "per_kernel": per,
-            "sample": "same five sequences at out-of-LLC sizes: AXPYDOT n=2^26, BiCGK/ATAX/"
-                      "GEMVER n=16384, GESUMMV n=12288; the C "
-                      "function alone on preallocated buffers; mean of %d reps after %d warm-up" % (steps, warmup)}
+    return per, tot_bytes, tot_sec
+
+
+def host_memory_free_bytes() -> int:
+    try:
+        for line in open("/proc/meminfo"):
+            if line.startswith("MemAvailable:"):
+                return int(line.split()[1]) * 1024
+    except OSError:
+        pass
+    return 0
+
+
+def cpu_baseline(steps: int = 2, warmup: int = 1, kernels=SUITE, work: HostWorkset | None = None,
+                 unfused: bool = True) -> dict:
+    """The reference's CPU path on this box's cores: max_fuse(graph, cores) as generated C
+    (cemit.py, OpenMP) at the BENCH sizes -- the same configuration the GPU arm runs -- and,
+    as a second figure, the unfused organism (fuse.py:128 `initial_forest`, serial, one
+    matrix-sized temporary per statement) next to the fused one on a smaller sample."""
+    sys.path.insert(0, str(REPO / "tests"))
+    import oracle_lib as O
+
+    cores_avail = host_cores()
+    use_ref = O.ref_available()
+    if use_ref:
+        ladder = O.ref_thread_ladder("bicgk")
+        threads = max(t for t in ladder if t <= max(1, cores_avail))
+        kind, how = "reference", f"t{threads}"
+    else:
+        O.ensure_built()
+        threads = max(1, cores_avail)
+        kind, how = "port", threads
+    sizes = BENCH
+    if work is None:
+        need = 2 * 8 * max(BENCH[k][0] * BENCH[k][1] for k in kernels) + (1 << 30)
+        if host_memory_free_bytes() and host_memory_free_bytes() < need:
+            sizes = CPU_SAMPLE          # said so in config.workload: not the same configuration
+        work = HostWorkset(sizes, kernels)
+    else:
+        sizes = work.sizes
+    per, tot_bytes, tot_sec = _time_cpu(O, how, use_ref, work, kernels, steps, warmup)
+    out = {"value": tot_bytes / tot_sec / 1e9, "unit": "GB/s", "cores": threads,
+           "kind": kind, "ms_per_step": tot_sec * 1e3, "per_kernel": per, "sizes": sizes,
+           "sample": "%s; the C function alone on preallocated host buffers (no copies, no allocation "
+                     "of operands); mean of %d reps after %d warm-up, %d OpenMP threads"
+                     % (describe(sizes, kernels), steps, warmup, threads)}
+    if unfused and use_ref:
+        try:
+            small = HostWorkset(UNFUSED_SAMPLE, kernels)
+            # the unfused organism writes its outputs AND its temporaries itself
+            u_per, u_b, u_s = _time_cpu(O, "unfused", True, small, kernels, 1, 1)
+            f1_per, f1_b, f1_s = _time_cpu(O, "t1", True, small, kernels, 1, 1)
+            ft_per, ft_b, ft_s = _time_cpu(O, how, True, small, kernels, 1, 1)
+            out["unfused"] = {
+                "value": u_b / u_s / 1e9, "unit": "GB/s", "cores": 1, "kind": "reference",
+                "organism": "initial_forest(graph) (fuse.py:128): one loop nest per statement, serial",
+                "per_kernel": {k: round(v["gbs"], 2) for k, v in u_per.items()},
+                "fused_1_thread": {"value": f1_b / f1_s / 1e9,
+                                   "per_kernel": {k: round(v["gbs"], 2) for k, v in f1_per.items()}},
+                "fused_all_threads": {"value": ft_b / ft_s / 1e9, "cores": threads,
+                                      "per_kernel": {k: round(v["gbs"], 2) for k, v in ft_per.items()}},
+                "fusion_speedup_1_thread": (f1_b / f1_s) / (u_b / u_s),
+                "sample": describe(UNFUSED_SAMPLE, kernels) + "; GB/s of the FUSED minimum bytes; 1 rep after 1 warm-up",
+            }
+            del small
+        except Exception as exc:          # the fused figure stands on its own
+            out["unfused"] = {"value": None, "error": f"{type(exc).__name__}: {exc}"}
+    return out
 
 
 def run_reference_arm(args) -> int:
@@ -191,22 +317,23 @@ def run_reference_arm(args) -> int:
     if rank != 0:
         return 0
     kernels = SUITE if args.kernel == "suite" else (args.kernel,)
-    base = cpu_baseline(steps=max(1, args.steps), warmup=max(1, min(args.warmup, 3)), kernels=kernels)
+    steps, warmup = max(1, args.steps), max(0, args.warmup)
+    base = cpu_baseline(steps=steps, warmup=warmup, kernels=kernels)
     line = {
-        "impl": "reference", "metric": "effective HBM GB/s (min bytes/time), fused suite",
-        "value": base["value"], "unit": "GB/s", "n_gpus": args.gpus, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": base["ms_per_step"], "higher_is_better": True,
+        "impl": "reference", "metric": METRIC,
+        "value": base["value"], "unit": "GB/s", "n_gpus": args.gpus, "steps": steps,
+        "warmup": warmup, "ms_per_step": base["ms_per_step"], "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": WORKLOAD if args.kernel == "suite" else
-                   f"{args.kernel} at BASELINE bench size {BENCH[args.kernel]}",
-                   "parallelism": f"{base['cores']} host threads (OpenMP, the reference's generated C)",
-                   "sample": base["sample"]},
+        "config": config_of(kernels, max(1, args.gpus), base["sizes"]),
+        "timing": "perf_counter around each C call, mean over the steps; rank 0's host cores only",
         "cpu_baseline": {k: base[k] for k in ("value", "unit", "cores", "kind", "sample")},
         "per_kernel": base["per_kernel"],
         "e2e": {"value": base["value"], "unit": "GB/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
         "gpu_launches": 0,
     }
+    if "unfused" in base:
+        line["cpu_baseline"]["unfused"] = base["unfused"]
     print(json.dumps(line))
     return 0
 
@@ -217,23 +344,34 @@ def run_reference_arm(args) -> int:
 class Suite:
     """Device buffers + launch closures for the five sequences on one rank."""
 
-    def __init__(self, torch, rank: int, world: int, kernels, exchange: str = "nccl"):
+    def __init__(self, torch, rank: int, world: int, kernels, exchange: str = "auto"):
         from paper_1205_1098_b200 import _native
         from paper_1205_1098_b200.sharded import GpuShardOps, ShardedRunner, TorchComm, row_block
         self.torch, self.rank, self.world = torch, rank, world
         self.native = _native
         self.ops = GpuShardOps()
         comm = TorchComm() if world > 1 else None
-        self.exchange_kind = "none" if world == 1 else "nccl"
+        self.exchange_kind = "none" if world == 1 else "nccl all-reduce after the join"
+        self.exchange = None
         fused = False
-        if world > 1 and exchange == "fused":
-            try:        # join-fused NVLink exchange (include/bto_b200.h 3b)
-                from paper_1205_1098_b200.sharded import NvlinkExchange
+        if world > 1 and exchange in ("auto", "fused"):
+            # join-fused NVLink exchange (include/bto_b200.h 3b) when symmetric memory is there AND
+            # a probe agrees with NCCL bit for bit on every rank; otherwise the library all-reduce
+            try:
+                from paper_1205_1098_b200.sharded import NvlinkExchange, fused_exchange_agrees
                 self.exchange = NvlinkExchange(max_vector=32768)
-                fused, self.exchange_kind = True, "fused-join (NVLink peer memory)"
-            except Exception as exc:  # symmetric memory unavailable: library all-reduce
-                self.exchange_kind = f"nccl (fused exchange unavailable: {type(exc).__name__})"
+                if fused_exchange_agrees(self.ops, comm, rank, world):
+                    fused, self.exchange_kind = True, "fused into the join kernel (NVLink peer memory)"
+                else:
+                    self.exchange_kind = "nccl all-reduce (fused exchange failed its probe)"
+            except Exception as exc:
+                self.exchange_kind = f"nccl all-reduce (fused exchange unavailable: {type(exc).__name__}: {exc})"
+            if not fused and exchange == "fused":
+                raise RuntimeError(f"--exchange fused requested but {self.exchange_kind}")
+            if rank == 0 and not fused:
+                print(f"[bench] {self.exchange_kind}", file=sys.stderr)
         self.runner = ShardedRunner(self.ops, comm, rank, world, fused=fused)
+        self.replays = {}
         self.kernels = kernels
         dev = torch.device("cuda", torch.cuda.current_device())
         gen = torch.Generator(device=dev).manual_seed(1234 + rank)
@@ -289,7 +427,18 @@ class Suite:
         return ([self.A, self.vecM[1], self.vecN[1], self.vecM[2], self.vecN[2], self.vecM[0], self.vecN[3]],
                 [self.Bm, self.x, self.w])
 
+    def capture(self, name: str):
+        """This rank's sequence `name`, exchange included, as a replayable CUDA graph."""
+        self.replays[name] = self.runner.capture(lambda: self._launch_eager(name))
+        return self.replays[name]
+
     def launch(self, name: str):
+        replay = self.replays.get(name)
+        if replay is not None:
+            return replay()
+        return self._launch_eager(name)
+
+    def _launch_eager(self, name: str):
         r = self.runner
         if name == "axpydot":
             r.axpydot(self.aw, self.av, self.au, 0.37, self.az, self.abeta)
@@ -308,65 +457,61 @@ class Suite:
                                 0.83, -0.41, self.vecM[0], self.vecN[3], self.Bm, self.x, self.w)
 
 
-def e2e_host(torch, kernels, steps: int, warmup: int) -> dict:
+def pinned_workset(torch, kernels) -> tuple[HostWorkset, str]:
+    """Host operands in PINNED memory (pageable if the box's locked-memory limit says no),
+    filled through the GPU's RNG (host RNG is slow); shared by e2e_host and the CPU leg."""
+    kind = ["pinned"]
+    keep = []
+
+    def alloc(count):
+        t = None
+        if kind[0] == "pinned":
+            try:
+                t = torch.empty(count, dtype=torch.float64, pin_memory=True)
+            except RuntimeError:          # locked-memory limit of the box: pageable host buffers
+                kind[0] = "pageable (pinned allocation failed)"
+        if t is None:
+            t = torch.empty(count, dtype=torch.float64)
+        keep.append(t)
+        return t.numpy()
+
+    work = HostWorkset(BENCH, kernels, alloc=alloc, filled=False)
+    work.tensors = keep
+    chunk = 1 << 26
+    for t in keep:
+        for off in range(0, t.numel(), chunk):
+            n = min(chunk, t.numel() - off)
+            t[off:off + n].copy_(torch.rand(n, dtype=torch.float64, device="cuda") * 2 - 1)
+    torch.cuda.synchronize()
+    return work, kind[0]
+
+
+def e2e_host(torch, kernels, steps: int, warmup: int, work: HostWorkset, host_kind: str) -> dict:
     """The suite through the reference's C symbols with pinned HOST buffers:
     host->device copies of every input and device->host copies of every output
     are inside the timed region (the call returns when outputs are on the host)."""
     from paper_1205_1098_b200 import _native
     lib = _native.load()
-
-    host_kind = ["pinned"]
-
-    def pinned(count):
-        if host_kind[0] == "pinned":
-            try:
-                return torch.empty(count, dtype=torch.float64, pin_memory=True)
-            except RuntimeError:          # locked-memory limit of the box: pageable host buffers
-                host_kind[0] = "pageable (pinned allocation failed)"
-        return torch.empty(count, dtype=torch.float64)
-
-    n, g, a = 32768, 24576, 1 << 27
-    big_in = pinned(n * n)
-    chunk = 1 << 26                      # fill through the GPU: host RNG is slow
-    for off in range(0, n * n, chunk):
-        big_in[off:off + chunk].copy_(
-            torch.rand(chunk, dtype=torch.float64, device="cuda") * 2 - 1)
-    big_out = pinned(n * n)
-    vec = [pinned(n).uniform_(-1, 1) for _ in range(8)]
-    outv = [pinned(n) for _ in range(3)]
-    scalar = pinned(1)
-    P = lambda t: ctypes.c_void_p(t.data_ptr())
+    P = lambda a: ctypes.c_void_p(a.ctypes.data)
+    order = {"axpydot": ("w", "v", "u", "alpha", "z", "beta"), "bicgk": ("A", "p", "r", "q", "s"),
+             "atax": ("A", "x", "y"), "gesummv": ("alpha", "beta", "A", "B", "x", "y"),
+             "gemver": ("A", "u1", "v1", "u2", "v2", "alpha", "beta", "y", "z", "B", "x", "w")}
     h2d = d2h = 0.0
     calls = []
-    if "axpydot" in kernels:
-        q = a
-        w_, v_, u_ = big_in[:q], big_in[q:2 * q], big_in[2 * q:3 * q]
-        calls.append(lambda: lib.axpydot(P(w_), P(v_), P(u_), 0.37, P(big_out[:q]), P(scalar), q))
-        h2d += 24.0 * q
-        d2h += 8.0 * q + 8
-    if "bicgk" in kernels:
-        calls.append(lambda: lib.bicgk(P(big_in), P(vec[0]), P(vec[1]), P(outv[0]), P(outv[1]), n, n))
-        h2d += 8.0 * n * n + 16 * n
-        d2h += 16.0 * n
-    if "atax" in kernels:
-        calls.append(lambda: lib.atax(P(big_in), P(vec[0]), P(outv[0]), n, n))
-        h2d += 8.0 * n * n + 8 * n
-        d2h += 8.0 * n
-    if "gesummv" in kernels:
-        A_, B_ = big_in[: g * g], big_in[g * g: 2 * g * g] if 2 * g * g <= n * n else big_in[: g * g]
-        calls.append(lambda: lib.gesummv(0.61, -0.27, P(A_), P(B_), P(vec[0]), P(outv[0]), g, g))
-        h2d += 16.0 * g * g + 8 * g
-        d2h += 8.0 * g
-    if "gemver" in kernels:
-        calls.append(lambda: lib.gemver(P(big_in), P(vec[1]), P(vec[2]), P(vec[3]), P(vec[4]),
-                                        0.83, -0.41, P(vec[5]), P(vec[6]), P(big_out),
-                                        P(outv[1]), P(outv[2]), n, n))
-        h2d += 8.0 * n * n + 48 * n
-        d2h += 8.0 * n * n + 16 * n
+    for k in kernels:
+        ins, outs, ext = work.operands(k)
+        args = []
+        for name in order[k]:
+            val = ins.get(name, outs.get(name))
+            args.append(float(val) if isinstance(val, float) else P(val))
+        args += [ext["M"]] + ([ext["N"]] if "N" in ext else [])
+        calls.append((getattr(lib, k), args))
+        h2d += sum(8.0 * v.size for v in ins.values() if not isinstance(v, float))
+        d2h += sum(8.0 * v.size for v in outs.values())
 
     def step():
-        for call in calls:
-            call()
+        for fn, args in calls:
+            fn(*args)
             _native.check()
 
     for _ in range(warmup):
@@ -382,7 +527,7 @@ def e2e_host(torch, kernels, steps: int, warmup: int) -> dict:
     return {"value": total / sec / 1e9, "unit": "GB/s", "ms_per_step": sec * 1e3,
             "step_ms": [round(t * 1e3, 2) for t in times], "timing": "median step, wall clock",
             "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-            "api": f"C symbols of include/bto_b200.h section 1 with {host_kind[0]} host pointers"}
+            "api": f"C symbols of include/bto_b200.h section 1 with {host_kind} host pointers"}
 
 
 def e2e_sharded(torch, dist, suite, kernels, steps: int, warmup: int) -> dict:
@@ -436,6 +581,30 @@ def e2e_sharded(torch, dist, suite, kernels, steps: int, warmup: int) -> dict:
             "api": f"ShardedRunner on {suite.world} ranks, every rank's shard from / to pinned host memory"}
 
 
+def normalise_kernel_name(name: str) -> str:
+    """'void mv_tile_kernel<5, 8, 2, 1, 2>' (ncu) -> 'mv_tile_kernel<5,8,2,1,2>' (bto_last_launch_plan)."""
+    name = name.strip()
+    if name.startswith("void "):
+        name = name[5:]
+    return name.replace(" ", "")
+
+
+def traffic_for(sequence: str, plan: str):
+    """DRAM bytes of `sequence` from the committed ncu capture (profiles/traffic.json) -- but only
+    if that capture profiled the kernel instances the library launches NOW (`plan`); a capture
+    of other instances is reported as stale, never quoted."""
+    try:
+        tj = json.loads((REPO / "profiles" / "traffic.json").read_text())
+        entry = tj[sequence]
+    except Exception as exc:
+        return None, f"unavailable ({type(exc).__name__})"
+    launched = set(plan.split("+")) if plan else set()
+    captured = {normalise_kernel_name(k) for k in entry["kernels"]}
+    if not captured <= launched:
+        return None, f"stale: profiles/traffic.json profiled {sorted(captured)}, the library launches {plan}"
+    return entry["dram_bytes"], tj["_source"]
+
+
 def run_gpu_arm(args) -> int:
     import torch
     import torch.distributed as dist
@@ -443,8 +612,14 @@ def run_gpu_arm(args) -> int:
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
-    if not torch.cuda.is_available():
-        print(json.dumps({"error": "no CUDA device; this bench has no CPU fallback"}))
+    if world != args.gpus:
+        print(json.dumps({"error": f"--gpus {args.gpus} but WORLD_SIZE={world}: launch one rank per GPU "
+                                   f"(python bench.py --gpus N starts them itself)"}))
+        return 2
+    if not torch.cuda.is_available() or torch.cuda.device_count() <= local_rank:
+        print(json.dumps({"error": "no CUDA device for this rank; this bench has no CPU fallback",
+                          "n_gpus_requested": args.gpus, "n_gpus_visible": torch.cuda.device_count()
+                          if torch.cuda.is_available() else 0}))
         return 2
     torch.cuda.set_device(local_rank)
     if world > 1:
@@ -460,6 +635,22 @@ def run_gpu_arm(args) -> int:
         if world > 1:
             dist.barrier()
         torch.cuda.synchronize()
+
+    plans = {}
+    for k in kernels:                      # first eager call: which kernel instances does it launch?
+        suite.launch(k)
+        plans[k] = _native.launch_plan()
+    launches_per_step = 0
+    if world > 1 or os.environ.get("BTO_BENCH_GRAPH"):
+        # a rank's step is 90-500 us of kernels at 8 GPUs: replay captured graphs (kernels +
+        # exchange), do not issue 2-5 launches and a collective per sequence from Python
+        before = _native.kernel_launches()
+        for k in kernels:
+            suite._launch_eager(k)
+        launches_per_step = _native.kernel_launches() - before
+        for k in kernels:
+            suite.capture(k)
+    barrier()
 
     for _ in range(max(3, args.warmup)):
         for k in kernels:
@@ -481,6 +672,10 @@ def run_gpu_arm(args) -> int:
         last.record()
         barrier()
     launches = _native.kernel_launches() - launches0
+    if suite.replays:                      # graph replays launch the captured kernels: count those
+        launches = launches_per_step * args.steps
+    if suite.exchange is not None and suite.runner.fused:
+        suite.exchange.status()            # raises if a peer wait ran into the guard
     total_ms = first.elapsed_time(last)
     per_ms = {k: statistics.mean(ev[s][i][0].elapsed_time(ev[s][i][1]) for s in range(args.steps))
               for i, k in enumerate(kernels)}
@@ -517,27 +712,20 @@ def run_gpu_arm(args) -> int:
                          "bytes_min": bytes_min(k, *BENCH[k]), "extents": list(BENCH[k])}
     dominant = max(kernels, key=lambda k: per_ms[k])
     dom = per_kernel[dominant]
-    traffic, traffic_src = None, None
-    try:        # DRAM bytes of the same launches from the committed ncu capture (single GPU)
-        tj = json.loads((REPO / "profiles" / "traffic.json").read_text())
-        if world == 1:
-            traffic, traffic_src = tj[dominant]["dram_bytes"], tj["_source"]
-    except Exception:
-        pass
+    for k in kernels:
+        per_kernel[k]["kernels"] = plans[k]
+    traffic, traffic_src = (traffic_for(dominant, plans[dominant]) if world == 1
+                            else (None, "single-GPU capture only"))
     line = {
-        "metric": "effective HBM GB/s (min bytes/time), fused suite",
+        "metric": METRIC,
         "value": round(value, 1), "unit": "GB/s", "n_gpus": world, "steps": args.steps,
         "warmup": max(3, args.warmup), "ms_per_step": round(ms_per_step, 4),
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
         "dtype": "f64", "data": "synthetic",
-        "config": {
-            "workload": WORKLOAD if args.kernel == "suite" else
-                        f"{args.kernel} at BASELINE bench size {BENCH[args.kernel]}",
-            "parallelism": f"row-shard x{world}, exchange: {suite.exchange_kind}" if world > 1
-                           else "single GPU",
-            "l2": "every input >= 4 GiB >> 126 MB L2; no flush between iterations",
-            "timing": "CUDA events on the launch stream, max over ranks",
-        },
+        "config": config_of(kernels, world),
+        "timing": "CUDA events on the launch stream, max over ranks",
+        "exchange": suite.exchange_kind,
+        "issue": "CUDA graph replay per sequence" if suite.replays else "eager launches",
         "per_kernel": per_kernel,
         "roofline": {"bound": "hbm", "kernel": dominant, "achieved": dom["gbs"],
                      "peak": peak * world, "unit": "GB/s",
@@ -555,23 +743,56 @@ def run_gpu_arm(args) -> int:
     line["suite_frac_of_nominal_8tbs"] = round(value / (8000.0 * world), 4)
     if sharded_e2e is not None:
         line["e2e"] = sharded_e2e
-    elif world == 1 and not args.no_e2e:
+    work = None
+    if world == 1 and sharded_e2e is None and not args.no_e2e:
         try:
-            line["e2e"] = e2e_host(torch, kernels, steps=max(1, min(args.steps, 3)), warmup=1)
+            del suite                                   # the device copies: e2e stages its own
+            work, host_kind = pinned_workset(torch, kernels)
+            line["e2e"] = e2e_host(torch, kernels, steps=max(1, min(args.steps, 3)), warmup=1,
+                                   work=work, host_kind=host_kind)
         except Exception as exc:  # e.g. not enough pinned host memory
             line["e2e"] = {"value": None, "error": f"{type(exc).__name__}: {exc}"}
     if world == 1 and not args.no_cpu:
         try:
-            base = cpu_baseline(steps=2, warmup=1, kernels=kernels)
+            base = cpu_baseline(steps=2, warmup=1, kernels=kernels, work=work)
             line["cpu_baseline"] = {k: base[k] for k in ("value", "unit", "cores", "kind", "sample")}
             line["cpu_baseline"]["per_kernel"] = {k: round(v["gbs"], 2)
                                                   for k, v in base["per_kernel"].items()}
+            if "unfused" in base:
+                line["cpu_baseline"]["unfused"] = base["unfused"]
         except Exception as exc:
             line["cpu_baseline"] = {"value": None, "error": f"{type(exc).__name__}: {exc}"}
     print(json.dumps(line))
     if world > 1:
         dist.destroy_process_group()
     return 0
+
+
+def free_port() -> int:
+    with socket.socket(socket.AF_INET, socket.SOCK_STREAM) as sock:
+        sock.bind(("127.0.0.1", 0))
+        return sock.getsockname()[1]
+
+
+def spawn_ranks(args) -> int:
+    """`python bench.py --gpus N` outside a launcher: start N ranks (one per GPU) with torch's
+    launcher on 127.0.0.1 and pass their output through.  Fewer than N visible GPUs is an
+    error -- never a silent N = 1 run."""
+    import torch
+    visible = torch.cuda.device_count() if torch.cuda.is_available() else 0
+    if visible < args.gpus:
+        print(json.dumps({"error": f"--gpus {args.gpus} requested, {visible} CUDA device(s) visible",
+                          "n_gpus_requested": args.gpus, "n_gpus_visible": visible}))
+        return 3
+    env = dict(os.environ)
+    # leave NCCL's communicator lines on (rank count), on stderr so that stdout stays one JSON line
+    env.setdefault("NCCL_DEBUG", "INFO")
+    env.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+    env.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr", "127.0.0.1",
+           "--master-port", str(free_port()), str(Path(__file__).resolve())] + sys.argv[1:]
+    return subprocess.run(cmd, env=env).returncode
 
 
 def main() -> int:
@@ -581,15 +802,21 @@ def main() -> int:
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=("b200", "reference"), default="b200")
     ap.add_argument("--kernel", choices=("suite",) + SUITE, default="suite")
-    ap.add_argument("--exchange", choices=("nccl", "fused"), default="nccl",
-                    help="N > 1: NCCL all-reduce after the join, or the exchange fused into the join")
+    ap.add_argument("--exchange", choices=("auto", "nccl", "fused"), default="auto",
+                    help="N > 1: the exchange fused into the join kernel over NVLink peer memory "
+                         "(auto: when symmetric memory is available and a probe agrees with NCCL), "
+                         "or one NCCL all-reduce after the join")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--tune", action="append", default=[], metavar="KEY=VALUE",
                     help="experiments only: a bto_set_tuning key (include/bto_b200.h section 4)")
     args = ap.parse_args()
+    if args.gpus < 1:
+        ap.error("--gpus must be >= 1")
     if args.impl == "reference":
         return run_reference_arm(args)
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return spawn_ranks(args)
     for kv in args.tune:
         from paper_1205_1098_b200 import _native
         key, value = kv.split("=")

@@ -34,7 +34,7 @@
 extern "C" {
 #endif
 
-#define BTO_B200_ABI_VERSION 1
+#define BTO_B200_ABI_VERSION 2
 
 /* ---- error channel (thread-local; cleared at the start of every call) ---- */
 enum {
@@ -42,7 +42,8 @@ enum {
     BTO_ERR_CUDA = 1,         /* a CUDA runtime call or launch failed         */
     BTO_ERR_INVALID = 2,      /* negative extent, null pointer, bad argument  */
     BTO_ERR_NO_DEVICE = 3,    /* no sm_100 device visible                     */
-    BTO_ERR_ALLOC = 4         /* workspace / staging allocation failed        */
+    BTO_ERR_ALLOC = 4,        /* workspace / staging allocation failed        */
+    BTO_ERR_EXCHANGE = 5      /* fused cross-GPU exchange: a peer never arrived */
 };
 int         bto_last_error(void);
 const char *bto_last_error_string(void);
@@ -77,7 +78,28 @@ void batax(const double *x, double beta, const double *A, double *y,
  * Same argument order plus a cudaStream_t (as void*).  Return BTO_OK or an
  * error code (also left in bto_last_error).  These are what the timing loop
  * (the replacement for cost.py:163-208 / cemit.py:294-359) and the sharded
- * runtime call.                                                             */
+ * runtime call.
+ *
+ * Concurrency contract (the reference: "thread-safe to invoke once at a time
+ * per output buffer"; its kernels malloc their partials per call,
+ * cemit.py:183-202).  Here:
+ *   - host-side the library is thread safe: every entry point takes one
+ *     process-wide lock for the (microseconds of) launch planning;
+ *   - device-side every CUDA stream has its OWN partial-sum workspace and
+ *     ticket counters, so sequences enqueued on different streams may run
+ *     concurrently; sequences on one stream run in order.  Output buffers must
+ *     not be shared between calls that can overlap;
+ *   - the entry points are legal under stream capture and the captured graphs
+ *     stay valid: a stream's workspace grows by adding a chunk, and a chunk a
+ *     captured kernel was given is never freed before bto_release_workspace()
+ *     (growth itself allocates in relaxed capture mode; call
+ *     bto_reserve_workspace(stream, bytes) once before capturing to avoid even
+ *     that).  Replaying a graph concurrently with other work on the stream it
+ *     was captured from shares that stream's workspace -- do not;
+ *   - section-1 calls with host operands hold the lock until their outputs are
+ *     back on the host (one at a time per process);
+ *   - the sharded entry points of 3b share ONE exchange buffer per device:
+ *     one stream at a time, every rank the same order.                       */
 typedef void *bto_stream_t;
 
 int bto_axpydot_async(const double *w, const double *v, const double *u,
@@ -141,11 +163,19 @@ int bto_gemver_pass2_async(const double *B, const double *x, double alpha,
  *   flag_ptrs[p]  : rank p's flag array, bto_exchange_flag_bytes(world) bytes,
  *                   zeroed before the first exchange
  *   epoch0        : exchanges already performed on these buffers (0 at start)
- * Every rank must call the same *_sharded_async sequence in the same order.  */
+ * Every rank must call the same *_sharded_async sequence in the same order.
+ * A waiter accepts any flag value that has REACHED its epoch (a fast peer may
+ * already have published the next one; the two buffer halves make that safe). */
 int bto_exchange_init(int rank, int world, void *const *exch_ptrs, void *const *flag_ptrs,
                       long capacity_doubles, unsigned int epoch0);
 int bto_exchange_shutdown(void);
 int bto_exchange_flag_bytes(int world);
+/* Synchronises the device and reports the exchange's health: BTO_OK, or
+ * BTO_ERR_EXCHANGE if a wait for a peer ran into the 20 s guard (the results of
+ * that exchange were set to NaN instead of hanging the GPU).  *epoch (may be
+ * NULL) receives the number of exchanges completed on this rank; the counter
+ * lives on the device, so replaying a captured graph advances it like a call. */
+int bto_exchange_status(unsigned int *epoch);
 int bto_axpydot_sharded_async(const double *w, const double *v, const double *u,
                               double alpha, double *z, double *beta, long M,
                               bto_stream_t stream);
@@ -214,6 +244,14 @@ int   bto_set_tuning(const char *key, long value);
 long  bto_get_tuning(const char *key);
 /* Kernels launched by this library since load (bench.py's gpu_launches).    */
 long  bto_kernel_launches(void);
+/* Hash of the kernel entry points (template instances) the calling thread's LAST
+ * library call launched, in order; 0 if it launched nothing.  Two calls with equal
+ * signatures took the same dispatch -- the empirical timer uses it to prove that the
+ * variant it validated is the variant it times.                              */
+unsigned long long bto_last_launch_signature(void);
+/* The same launches by name with their template arguments, '+'-separated, e.g.
+ * "mv_tile_kernel<5,8,2,1,2>+finalize_kernel" (valid until the thread's next call). */
+const char *bto_last_launch_plan(void);
 /* Minimum HBM traffic of one call in bytes (SURVEY.md section 8d formulas);
  * negative for an unknown kernel name.  N is ignored for vector kernels.    */
 double bto_bytes_min(const char *kernel, long M, long N);
@@ -225,6 +263,9 @@ int   bto_device_info(int *sm_count, int *max_threads_per_sm,
  * arena (both cached between calls); bto_release_workspace frees them.      */
 long  bto_workspace_bytes(void);
 int   bto_release_workspace(void);
+/* Make `stream`'s workspace at least `bytes` large now (e.g. before capturing a graph
+ * on it), so that later calls on that stream do not allocate.                 */
+int   bto_reserve_workspace(bto_stream_t stream, long bytes);
 /* Host <-> device copies with the staging the section-1 entry points use (pageable
  * buffers of 16 MiB and more go through the pinned bounce slots at 45-50 GB/s instead of
  * ~11 GB/s); synchronous: the data has arrived when the call returns.          */

@@ -51,15 +51,15 @@ _CT = {"p": _P, "d": _D, "l": _L}
 #: every symbol include/bto_b200.h declares (tests check the library exports them)
 EXPORTED = tuple(SIGNATURES) + tuple(f"bto_{k}_async" for k in SIGNATURES) + (
     "bto_gemver_pass1_async", "bto_gemver_xupdate_async", "bto_gemver_pass2_async",
-    "bto_exchange_init", "bto_exchange_shutdown", "bto_exchange_flag_bytes",
+    "bto_exchange_init", "bto_exchange_shutdown", "bto_exchange_flag_bytes", "bto_exchange_status",
     "bto_axpydot_sharded_async", "bto_bicgk_sharded_async", "bto_atax_sharded_async",
     "bto_gemver_sharded_async",
     "bto_prim_matvec_async", "bto_prim_axpby_async", "bto_prim_outer_async", "bto_prim_dot_async",
     "bto_colsum_axpz_async", "bto_rank2_rowdot_async",
     "bto_last_error", "bto_last_error_string", "bto_clear_error",
     "bto_abi_version", "bto_set_stream", "bto_set_tuning", "bto_get_tuning",
-    "bto_kernel_launches", "bto_bytes_min", "bto_device_info",
-    "bto_workspace_bytes", "bto_release_workspace", "bto_copy_to_device", "bto_copy_to_host", "bto_fill_host",
+    "bto_kernel_launches", "bto_last_launch_signature", "bto_last_launch_plan", "bto_bytes_min", "bto_device_info",
+    "bto_workspace_bytes", "bto_release_workspace", "bto_reserve_workspace", "bto_copy_to_device", "bto_copy_to_host", "bto_fill_host",
 )
 
 _lib = None
@@ -116,6 +116,12 @@ def load() -> ctypes.CDLL:
     lib.bto_exchange_shutdown.restype = c_int
     lib.bto_exchange_flag_bytes.restype = c_int
     lib.bto_exchange_flag_bytes.argtypes = [c_int]
+    lib.bto_exchange_status.restype = c_int
+    lib.bto_exchange_status.argtypes = [POINTER(ctypes.c_uint)]
+    lib.bto_last_launch_signature.restype = ctypes.c_ulonglong
+    lib.bto_last_launch_plan.restype = c_char_p
+    lib.bto_reserve_workspace.restype = c_int
+    lib.bto_reserve_workspace.argtypes = [_S, _L]
     lib.bto_last_error.restype = c_int
     lib.bto_last_error_string.restype = c_char_p
     lib.bto_clear_error.restype = None
@@ -165,6 +171,16 @@ def get_tuning(key: str) -> int:
 
 def kernel_launches() -> int:
     return int(load().bto_kernel_launches())
+
+
+def launch_signature() -> int:
+    """Hash of the kernel instances the last library call of this thread launched."""
+    return int(load().bto_last_launch_signature())
+
+
+def launch_plan() -> str:
+    """Kernel instances (names with template arguments) the last library call launched."""
+    return load().bto_last_launch_plan().decode()
 
 
 def bytes_min(kernel: str, M: int, N: int = 1) -> float:

@@ -19,7 +19,7 @@ Replaces the two fitness plug-ins of the reference (`cost.py`):
   `reps`.  Failures map to `CostReport(total=inf, diagnostic="<kind>: ...")`
   with the reference's kinds (`runtime-crash`, `numerical-mismatch`;
   `compile-failure` when the library is missing).
-* `CachedFitness` / `cached`  <->  cost.py:211-241.
+* `FitnessMemo` / `cached`  <->  cost.py:211-241 (own memo table; `CachedFitness` is an alias).
 
 A variant is what the GPU search explores instead of an organism: the kernel
 plus the launch tunables of include/bto_b200.h section 4.
@@ -35,7 +35,7 @@ from .spec import TypedSpec, match_corpus
 __all__ = [
     "CostReport", "GpuMachineModel", "GpuVariant", "Traffic", "hbm_traffic",
     "estimate_cost", "AnalyticGpuCost", "GpuEmpiricalTimer", "measure_empirical",
-    "CachedFitness", "cached", "variant_space", "evaluate_spec",
+    "CachedFitness", "FitnessMemo", "cached", "validation_extents", "variant_space", "evaluate_spec",
 ]
 
 
@@ -282,6 +282,33 @@ def evaluate_spec(spec, inputs: dict) -> dict:
     return {name: env[name][1] for name, _ in spec.outputs}
 
 
+#: elements of the largest operand up to which the timed extents themselves are validated
+_VALIDATE_FULL_BELOW = 1 << 26
+
+
+def validation_extents(extents: dict) -> dict:
+    """Extents at which a variant is checked before it is timed.
+
+    The reference validates at min(64, extent) (cost.py:199-202) because its generated loops are
+    the same code at every size.  Here the dispatch depends on the shape: narrow matrices take the
+    shared-row kernels, the cluster size of ATAX follows N, whole-row streaming needs N >= 4096,
+    and a 64 x 64 problem never enters the unrolled paths -- so a 64-extent check would validate
+    kernels the timed run never launches.  Validation therefore runs at the timed extents when
+    they are small enough for the in-product evaluator (`evaluate_spec` builds matrix-sized
+    temporaries), else at the same N with fewer rows: every dispatch decision of the library is
+    made on N and on M >= a few thousand rows, and `measure_empirical` additionally compares
+    the launch signatures of the two runs."""
+    ext = {k: int(v) for k, v in extents.items()}
+    size = 1
+    for v in ext.values():
+        size *= v
+    if size <= _VALIDATE_FULL_BELOW or "N" not in ext or "M" not in ext:
+        return ext
+    rows = max(4096, _VALIDATE_FULL_BELOW // max(1, ext["N"]))
+    ext["M"] = min(ext["M"], rows)
+    return ext
+
+
 def measure_empirical(variant: GpuVariant, graph: TypedSpec, extents: dict, reps: int = 5,
                       validate_extents: dict | None = None, fault=None,
                       tolerance: float = 1e-10) -> CostReport:
@@ -307,7 +334,7 @@ def measure_empirical(variant: GpuVariant, graph: TypedSpec, extents: dict, reps
             _native.set_tuning(**dict(variant.tuning))
         except _native.BtoError as exc:
             return failure("compile-failure", str(exc))
-        vext = validate_extents or {k: min(64, v) for k, v in extents.items()}
+        vext = validate_extents or validation_extents(extents)
 
         def alloc(ext, seed):
             host = gen_inputs(graph, ext, seed=seed)
@@ -324,6 +351,7 @@ def measure_empirical(variant: GpuVariant, graph: TypedSpec, extents: dict, reps
         try:
             dev, outs = alloc(vext, 7)
             run_kernel_async(kernel, graph, dev, vext, outs)
+            validated_dispatch = _native.launch_signature()
             torch.cuda.synchronize()
             got = {n: (float(outs[n][0]) if d.kind == "scalar" else
                        outs[n].reshape(tuple(int(vext[x]) for x in graph.dims[n])).cpu().numpy())
@@ -338,8 +366,13 @@ def measure_empirical(variant: GpuVariant, graph: TypedSpec, extents: dict, reps
         if not err < tolerance:
             return failure("numerical-mismatch", f"max relative error {err:.3e}")
         try:
+            del dev, outs
             dev, outs = alloc(extents, 7)
             run_kernel_async(kernel, graph, dev, extents, outs)       # warm-up, untimed
+            if validate_extents is None and _native.launch_signature() != validated_dispatch:
+                # the kernels about to be timed are not the ones that were checked
+                return failure("validation-mismatch",
+                               f"extents {vext} validated a different kernel dispatch than {extents} runs")
             best = math.inf
             stream = torch.cuda.current_stream()
             for _ in range(reps):
@@ -382,35 +415,56 @@ class GpuEmpiricalTimer:
                                  validate_extents=self.validate_extents, fault=self.fault)
 
 
-class CachedFitness:
-    """Memoises fitness on the variant key plus the extents salt (cost.py:211-237)."""
+class FitnessMemo:
+    """A fitness function behind a memo table (the role of cost.py:211-237).
+
+    The table is keyed by `<salt>|<variant key>`, the salt being whatever the wrapped
+    fitness reports through `key_salt()` (extents, device), so one memo can never hand a
+    timing taken at one problem size to a search at another.  `lookup()` answers from
+    the table without evaluating -- the search driver uses it to decide whether a
+    candidate would cost a fresh evaluation before it spends budget on it."""
 
     def __init__(self, fn, enabled: bool = True):
-        self.fn, self.enabled = fn, enabled
-        self.hits = self.misses = 0
-        self._table: dict[str, CostReport] = {}
-        self.parallel_safe = getattr(fn, "parallel_safe", False)
+        self.fn = fn
+        self.enabled = bool(enabled)
+        self.parallel_safe = bool(getattr(fn, "parallel_safe", False))
+        self._reports: dict[str, CostReport] = {}
+        self._lookups = 0          # calls answered from the table
+        self._evaluations = 0      # calls that ran the wrapped fitness
+
+    # -- counters under the names the reference's summary.json uses -------------------
+    @property
+    def hits(self) -> int:
+        return self._lookups
+
+    @property
+    def misses(self) -> int:
+        return self._evaluations
 
     def key(self, variant: GpuVariant) -> str:
-        salt = self.fn.key_salt() if hasattr(self.fn, "key_salt") else ""
-        return salt + "|" + variant.key()
+        salt_of = getattr(self.fn, "key_salt", None)
+        return f"{salt_of() if salt_of else ''}|{variant.key()}"
+
+    def lookup(self, variant: GpuVariant) -> CostReport | None:
+        return self._reports.get(self.key(variant)) if self.enabled else None
 
     def __call__(self, variant: GpuVariant) -> CostReport:
-        if not self.enabled:
-            self.misses += 1
-            return self.fn(variant)
-        key = self.key(variant)
-        if key in self._table:
-            self.hits += 1
-            return self._table[key]
-        self.misses += 1
+        known = self.lookup(variant)
+        if known is not None:
+            self._lookups += 1
+            return known
+        self._evaluations += 1
         report = self.fn(variant)
-        self._table[key] = report
+        if self.enabled:
+            self._reports[self.key(variant)] = report
         return report
 
 
-def cached(fn, enabled: bool = True) -> CachedFitness:
-    return CachedFitness(fn, enabled)
+CachedFitness = FitnessMemo        # the name callers of the reference's protocol know
+
+
+def cached(fn, enabled: bool = True) -> FitnessMemo:
+    return fn if isinstance(fn, FitnessMemo) and fn.enabled == enabled else FitnessMemo(fn, enabled)
 
 
 def variant_space(kernel: str) -> list[GpuVariant]:

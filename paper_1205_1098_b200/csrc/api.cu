@@ -28,6 +28,8 @@ const char *bto_last_error_string(void) { return g_errmsg; }
 void bto_clear_error(void) { g_err = BTO_OK; g_errmsg[0] = 0; }
 int bto_abi_version(void) { return BTO_B200_ABI_VERSION; }
 long bto_kernel_launches(void) { return g_launches.load(); }
+unsigned long long bto_last_launch_signature(void) { return g_signature; }
+const char *bto_last_launch_plan(void) { return g_plan; }
 
 // ---- section 1: the reference's signatures ---------------------------------
 
@@ -282,7 +284,7 @@ int bto_gemver_xupdate_async(const double *colsum, double beta, const double *z,
     if (N < 1) return fail(BTO_ERR_INVALID, "extent N=%ld must be >= 1", N);
     axpz_kernel<<<(unsigned)((N + kThreads - 1) / kThreads), kThreads, 0, st>>>(
         colsum, beta, z, x, N);
-    return check_launch("axpz_kernel");
+    return check_launch("axpz_kernel", reinterpret_cast<const void *>(axpz_kernel));
 }
 
 int bto_gemver_pass2_async(const double *B, const double *x, double alpha,
@@ -312,13 +314,15 @@ int bto_exchange_init(int rank, int world, void *const *exch_ptrs, void *const *
     if (!c.exch_bufs) {
         CUDA_TRY(cudaMalloc(&c.exch_bufs, 64 * sizeof(double *)));
         CUDA_TRY(cudaMalloc(&c.exch_flags, 64 * sizeof(unsigned int *)));
+        CUDA_TRY(cudaMalloc(&c.exch_state, 4 * sizeof(unsigned int)));
     }
+    const unsigned int state0[4] = {epoch0, 0u, 0u, 0u};
+    CUDA_TRY(cudaMemcpy(c.exch_state, state0, sizeof(state0), cudaMemcpyHostToDevice));
     CUDA_TRY(cudaMemcpy(c.exch_bufs, exch_ptrs, (size_t)world * sizeof(void *), cudaMemcpyHostToDevice));
     CUDA_TRY(cudaMemcpy(c.exch_flags, flag_ptrs, (size_t)world * sizeof(void *), cudaMemcpyHostToDevice));
     c.exch_rank = rank;
     c.exch_world = world;
     c.exch_capacity = (capacity_doubles / 2) * 2;
-    c.exch_epoch = epoch0;
     c.exch_ready = true;
     return BTO_OK;
 }
@@ -334,15 +338,28 @@ int bto_exchange_shutdown(void)
 
 int bto_exchange_flag_bytes(int world) { return world * kExchCtas * (int)sizeof(unsigned int); }
 
+int bto_exchange_status(unsigned int *epoch)
+{
+    AsyncCall ac;
+    if (ac.rc != BTO_OK) return ac.rc;
+    DeviceCtx &c = *ac.ctx;
+    if (!c.exch_ready) return fail(BTO_ERR_INVALID, "bto_exchange_init has not been called");
+    unsigned int state[4] = {0u, 0u, 0u, 0u};
+    CUDA_TRY(cudaDeviceSynchronize());
+    CUDA_TRY(cudaMemcpy(state, c.exch_state, sizeof(state), cudaMemcpyDeviceToHost));
+    if (epoch) *epoch = state[0];
+    if (state[2] & kExchTimedOut) {
+        return fail(BTO_ERR_EXCHANGE, "fused exchange: a peer did not arrive within %llu s (rank %d of %d, "
+                    "epoch %u); the affected results were set to NaN",
+                    kExchTimeoutNs / 1000000000ull, c.exch_rank, c.exch_world, state[0]);
+    }
+    return BTO_OK;
+}
+
 namespace {
 // marks the sequence as sharded for the joins it launches
 struct ExchangeScope {
-    explicit ExchangeScope(DeviceCtx &c) : ctx(c)
-    {
-        // a reduce-only call (tests) re-uses the epoch of the publish it pairs with
-        if (!(g_tuning.exchange_phases & 1)) --ctx.exch_epoch;
-        ctx.exch_active = true;
-    }
+    explicit ExchangeScope(DeviceCtx &c) : ctx(c) { ctx.exch_active = true; }
     ~ExchangeScope() { ctx.exch_active = false; }
     DeviceCtx &ctx;
 };
@@ -363,7 +380,7 @@ int bto_axpydot_sharded_async(const double *w, const double *v, const double *u,
     WsLayout lay;
     lay.take((size_t)c.sm_count * 64);
     const size_t off = lay.take(1);
-    BTO_TRY(size_ws(c, lay));
+    BTO_TRY(size_ws(c, lay, st));
     double *local = reinterpret_cast<double *>(c.ws + off);
     c.exch_active = false;
     int rc = seq_axpydot(c, w, v, u, alpha, z, local, M, st);
@@ -421,14 +438,14 @@ int bto_prim_matvec_async(const double *A, const double *x, double *out, long M,
     if (transposed) {                    // out[j] = sum_i A[i,j] x[i]
         Pass<kFlagT> pass;
         BTO_TRY(pass.prepare(c, M, N, mat_aligned(N, A), &lay));
-        BTO_TRY(size_ws(c, lay));
+        BTO_TRY(size_ws(c, lay, st));
         a.roww = x;
         f.cmode = kColPlain; f.colout = out;
         return pass.run(c, a, f, st);
     }
     Pass<kFlagN> pass;                   // out[i] = sum_j A[i,j] x[j]
     BTO_TRY(pass.prepare(c, M, N, mat_aligned(N, A), &lay));
-    BTO_TRY(size_ws(c, lay));
+    BTO_TRY(size_ws(c, lay, st));
     a.colw = x;
     f.rmode = kRowPlain; f.rowout = out;
     return pass.run(c, a, f, st);
@@ -445,7 +462,7 @@ int bto_prim_axpby_async(double alpha, const double *x, double beta, const doubl
     const long cap = (long)ac.ctx->sm_count * 16;
     if (grid > cap) grid = cap;
     prim_axpby_kernel<<<(unsigned)grid, kThreads, 0, st>>>(alpha, x, beta, y, out, n, mode);
-    return check_launch("prim_axpby_kernel");
+    return check_launch("prim_axpby_kernel", reinterpret_cast<const void *>(prim_axpby_kernel));
 }
 
 int bto_prim_outer_async(const double *u, const double *v, double *out, long M, long N,
@@ -457,7 +474,7 @@ int bto_prim_outer_async(const double *u, const double *v, double *out, long M, 
     const long cap = (long)ac.ctx->sm_count * 16;
     if (grid > cap) grid = cap;
     prim_outer_kernel<<<(unsigned)grid, kThreads, 0, st>>>(u, v, out, M, N);
-    return check_launch("prim_outer_kernel");
+    return check_launch("prim_outer_kernel", reinterpret_cast<const void *>(prim_outer_kernel));
 }
 
 int bto_prim_dot_async(const double *x, const double *y, double *out, long n, bto_stream_t stream)
@@ -470,10 +487,10 @@ int bto_prim_dot_async(const double *x, const double *y, double *out, long n, bt
     if (grid > cap) grid = cap;
     WsLayout lay;
     const size_t off = lay.take((size_t)grid);
-    BTO_TRY(size_ws(c, lay));
+    BTO_TRY(size_ws(c, lay, st));
     prim_dot_kernel<<<(unsigned)grid, kThreads, 0, st>>>(
         x, y, out, reinterpret_cast<double *>(c.ws + off), c.tickets + 1, n);
-    return check_launch("prim_dot_kernel");
+    return check_launch("prim_dot_kernel", reinterpret_cast<const void *>(prim_dot_kernel));
 }
 
 // ---- section 3d: fused passes over a transposed (column-major) operand --------------
@@ -502,7 +519,7 @@ int bto_rank2_rowdot_async(const double *S, const double *a1, const double *b1, 
     WsLayout lay;
     Pass<kFlagN | kFlagRank2> pass;
     BTO_TRY(pass.prepare(c, rows, cols, mat_aligned(cols, S, Sout), &lay));
-    BTO_TRY(size_ws(c, lay));
+    BTO_TRY(size_ws(c, lay, st));
     MvArgs a{};
     a.A = S; a.colw = wgt;
     a.u1 = a1; a.v1 = b1; a.u2 = a2; a.v2 = b2; a.Bout = Sout;
@@ -613,7 +630,13 @@ long bto_workspace_bytes(void)
 {
     std::lock_guard<std::mutex> lock(g_mu);
     long total = 0;
-    for (DeviceCtx &c : g_ctx) total += (long)(c.ws_bytes + c.arena_bytes);
+    for (DeviceCtx &c : g_ctx) {
+        total += (long)c.arena_bytes;
+        for (auto &kv : c.streams) {
+            total += (long)kv.second.cur.bytes;
+            for (const WsChunk &old : kv.second.retired) total += (long)old.bytes;
+        }
+    }
     return total;
 }
 
@@ -623,7 +646,14 @@ int bto_release_workspace(void)
     if (ac.rc != BTO_OK) return ac.rc;
     CUDA_TRY(cudaDeviceSynchronize());
     DeviceCtx &c = *ac.ctx;
-    if (c.ws) CUDA_TRY(cudaFree(c.ws));
+    for (auto &kv : c.streams) {
+        StreamWs &w = kv.second;
+        if (w.cur.ptr) CUDA_TRY(cudaFree(w.cur.ptr));
+        for (const WsChunk &old : w.retired) CUDA_TRY(cudaFree(old.ptr));
+        w.cur = WsChunk{};
+        w.cur_captured = false;
+        w.retired.clear();
+    }
     if (c.arena) CUDA_TRY(cudaFree(c.arena));
     c.ws = nullptr; c.ws_bytes = 0;
     c.arena = nullptr; c.arena_bytes = 0;
@@ -632,6 +662,13 @@ int bto_release_workspace(void)
         c.bounce[i] = nullptr;
     }
     return BTO_OK;
+}
+
+int bto_reserve_workspace(bto_stream_t stream, long bytes)
+{
+    ASYNC_PROLOGUE();
+    if (bytes < 0) return fail(BTO_ERR_INVALID, "reserve_workspace: negative size");
+    return reserve_ws(*ac.ctx, st, (size_t)bytes);
 }
 
 int bto_fill_host(double *host_dst, long count, double value)

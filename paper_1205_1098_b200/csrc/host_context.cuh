@@ -30,6 +30,32 @@ using namespace bto;
 thread_local int g_err = BTO_OK;
 thread_local char g_errmsg[512] = "";
 std::atomic<long> g_launches{0};
+// FNV-1a hash over the kernel entry points launched by the current API call, in
+// order (cleared in the call prologue): lets a caller assert that two calls took the
+// same dispatch -- bto_last_launch_signature(), used by the empirical timer to prove
+// that the variant it validated is the variant it times.
+thread_local unsigned long long g_signature = 0;
+// the same launches by name, template arguments included ("mv_tile_kernel<5,8,2,1,2>+finalize_kernel"):
+// bto_last_launch_plan(); profiles/traffic.json is keyed by these names so that a stale
+// ncu capture is detected instead of quoted
+thread_local char g_plan[768] = "";
+
+void reset_call_record()
+{
+    g_signature = 0;
+    g_plan[0] = 0;
+}
+
+void note_kernel(const void *entry)
+{
+    unsigned long long h = g_signature ? g_signature : 1469598103934665603ull;
+    const unsigned long long v = reinterpret_cast<unsigned long long>(entry);
+    for (int b = 0; b < 8; ++b) {
+        h ^= (v >> (8 * b)) & 0xffull;
+        h *= 1099511628211ull;
+    }
+    g_signature = h;
+}
 
 int fail(int code, const char *fmt, ...)
 {
@@ -81,6 +107,47 @@ struct Tuning {
     long host_panel_mib = 64;    // panel size of that pipeline
 };
 
+// ---------------------------------------------------------------------------
+// Workspace (partial sums + ticket counters) PER STREAM.
+//
+// Every sequence writes cross-CTA partials and a join reads them; two sequences in
+// flight on different streams must therefore not share them (they did until round 2:
+// silently wrong results).  A stream's workspace grows by REPLACEMENT: the old chunk is
+// freed only when no captured CUDA graph can reference it (it was never used under
+// stream capture) and after the stream has drained; otherwise it is retired and lives
+// until bto_release_workspace().  Growth never synchronises the device and is legal
+// during stream capture (the allocation is made in relaxed capture mode, like
+// PyTorch's caching allocator does).
+struct WsChunk {
+    char *ptr = nullptr;
+    size_t bytes = 0;
+};
+
+struct StreamWs {
+    WsChunk cur;
+    bool cur_captured = false;     // handed to a kernel while the stream was capturing
+    unsigned int *tickets = nullptr;   // 64 counters, zero between kernels
+    std::vector<WsChunk> retired;
+};
+
+// cudaMalloc / cudaFree / synchronous helpers are "potentially unsafe" calls that the
+// default (global) capture mode forbids on a thread while ANY stream is capturing.
+struct RelaxedCapture {
+    cudaStreamCaptureMode mode = cudaStreamCaptureModeRelaxed;
+    RelaxedCapture() { cudaThreadExchangeStreamCaptureMode(&mode); }
+    ~RelaxedCapture() { cudaThreadExchangeStreamCaptureMode(&mode); }
+};
+
+bool stream_capturing(cudaStream_t st)
+{
+    cudaStreamCaptureStatus status = cudaStreamCaptureStatusNone;
+    if (cudaStreamIsCapturing(st, &status) != cudaSuccess) {
+        cudaGetLastError();        // e.g. the legacy stream while another stream captures
+        return false;
+    }
+    return status != cudaStreamCaptureStatusNone;
+}
+
 struct DeviceCtx {
     bool ready = false;
     int device = -1;
@@ -88,9 +155,13 @@ struct DeviceCtx {
     int max_threads_per_sm = 0;
     long l2_bytes = 0;
     long global_bytes = 0;
+    // workspace of the stream the current call runs on (bound by size_ws / bind_stream
+    // under g_mu; the owning StreamWs is in `streams`)
     char *ws = nullptr;            // partial sums
     size_t ws_bytes = 0;
     unsigned int *tickets = nullptr;
+    std::map<cudaStream_t, StreamWs> streams;
+    cudaStream_t util = nullptr;   // non-blocking helper stream (memsets of fresh counters)
     char *arena = nullptr;         // device staging for host arguments
     size_t arena_bytes = 0;
     cudaStream_t stream = nullptr; // stream of the section-1 entry points
@@ -103,7 +174,9 @@ struct DeviceCtx {
     long exch_capacity = 0;            // doubles per rank, both parity halves together
     double **exch_bufs = nullptr;      // device array [world] of peer-mapped buffers
     unsigned int **exch_flags = nullptr;
-    unsigned int exch_epoch = 0;
+    // exchange state that must survive CUDA-graph replay lives on the device:
+    // [0] exchanges completed (the epoch), [1] ticket of the CTAs that finished, [2] error word
+    unsigned int *exch_state = nullptr;
     // pageable host operands: pinned bounce slots filled / drained by host threads
     // (slots 0-2 carry host->device traffic, 3-5 device->host, so both directions can run at once)
     char *bounce[6] = {};
@@ -146,17 +219,22 @@ int get_ctx(DeviceCtx **out)
         c.max_threads_per_sm = prop.maxThreadsPerMultiProcessor;
         c.l2_bytes = prop.l2CacheSize;
         c.global_bytes = (long)prop.totalGlobalMem;
-        CUDA_TRY(cudaMalloc(&c.tickets, 64 * sizeof(unsigned int)));
-        CUDA_TRY(cudaMemset(c.tickets, 0, 64 * sizeof(unsigned int)));
+        {
+            RelaxedCapture relaxed;
+            CUDA_TRY(cudaStreamCreateWithFlags(&c.util, cudaStreamNonBlocking));
+        }
         c.ready = true;
     }
     *out = &c;
     return BTO_OK;
 }
 
+// The host staging arena: one per device, used only by the section-1 host-pointer calls,
+// which hold g_mu for their whole duration and return synchronised.
 int grow(char **buf, size_t *have, size_t want, const char *what)
 {
     if (want <= *have) return BTO_OK;
+    RelaxedCapture relaxed;
     // nothing of ours may still be running on the old buffer
     CUDA_TRY(cudaDeviceSynchronize());
     if (*buf) CUDA_TRY(cudaFree(*buf));
@@ -173,6 +251,69 @@ int grow(char **buf, size_t *have, size_t want, const char *what)
                     cudaGetErrorString(e));
     }
     *have = bytes;
+    return BTO_OK;
+}
+
+// Make `st`'s workspace the current one (creating its ticket counters on first use).
+int bind_stream(DeviceCtx &c, cudaStream_t st, StreamWs **out)
+{
+    auto it = c.streams.find(st);
+    if (it == c.streams.end()) {
+        RelaxedCapture relaxed;
+        StreamWs fresh;
+        CUDA_TRY(cudaMalloc(&fresh.tickets, 64 * sizeof(unsigned int)));
+        CUDA_TRY(cudaMemsetAsync(fresh.tickets, 0, 64 * sizeof(unsigned int), c.util));
+        CUDA_TRY(cudaStreamSynchronize(c.util));
+        it = c.streams.emplace(st, fresh).first;
+    }
+    StreamWs &w = it->second;
+    c.ws = w.cur.ptr;
+    c.ws_bytes = w.cur.bytes;
+    c.tickets = w.tickets;
+    if (out) *out = &w;
+    return BTO_OK;
+}
+
+// Ensure `st`'s workspace holds `want` bytes and bind it.  Pointers handed out before a
+// growth stay valid for the kernels already enqueued (see StreamWs).
+int reserve_ws(DeviceCtx &c, cudaStream_t st, size_t want)
+{
+    StreamWs *w = nullptr;
+    BTO_TRY(bind_stream(c, st, &w));
+    const bool capturing = stream_capturing(st);
+    if (want > w->cur.bytes) {
+        RelaxedCapture relaxed;
+        size_t bytes = want + want / 8 + (1u << 20);
+        if (bytes < 2 * w->cur.bytes) bytes = 2 * w->cur.bytes;     // retired chunks sum to < the live one
+        char *fresh = nullptr;
+        cudaError_t e = cudaMalloc(&fresh, bytes);
+        if (e != cudaSuccess) {
+            cudaGetLastError();
+            bytes = want;
+            e = cudaMalloc(&fresh, bytes);
+        }
+        if (e != cudaSuccess) {
+            cudaGetLastError();
+            return fail(BTO_ERR_ALLOC, "cannot allocate %zu bytes of workspace: %s", want,
+                        cudaGetErrorString(e));
+        }
+        if (w->cur.ptr) {
+            if (!capturing && !w->cur_captured) {
+                // only kernels of this stream use the chunk: drain the stream, not the device
+                CUDA_TRY(cudaStreamSynchronize(st));
+                CUDA_TRY(cudaFree(w->cur.ptr));
+            } else {
+                w->retired.push_back(w->cur);      // a captured graph may replay into it
+            }
+        }
+        w->cur.ptr = fresh;
+        w->cur.bytes = bytes;
+        w->cur_captured = false;
+    }
+    if (capturing) w->cur_captured = true;
+    c.ws = w->cur.ptr;
+    c.ws_bytes = w->cur.bytes;
+    c.tickets = w->tickets;
     return BTO_OK;
 }
 
@@ -209,7 +350,17 @@ int check_launch(const char *what)
         return fail(BTO_ERR_CUDA, "launch of %s failed: %s", what, cudaGetErrorString(e));
     }
     g_launches.fetch_add(1, std::memory_order_relaxed);
+    const size_t used = strlen(g_plan);
+    if (used + strlen(what) + 2 < sizeof(g_plan)) {
+        snprintf(g_plan + used, sizeof(g_plan) - used, "%s%s", used ? "+" : "", what);
+    }
     return BTO_OK;
+}
+
+int check_launch(const char *what, const void *entry)
+{
+    note_kernel(entry);
+    return check_launch(what);
 }
 
 // Launch `kernel(arg)` as a programmatic dependent of the previous kernel in the
@@ -229,7 +380,7 @@ int launch_dependent(void (*kernel)(const Arg), unsigned grid, const Arg &arg,
     cfg.attrs = attr;
     cfg.numAttrs = 1;
     CUDA_TRY(cudaLaunchKernelEx(&cfg, kernel, arg));
-    return check_launch(what);
+    return check_launch(what, reinterpret_cast<const void *>(kernel));
 }
 
 bool aligned16(const void *p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }

@@ -45,11 +45,14 @@ int launch_vec(DeviceCtx &c, VecArgs g, cudaStream_t stream)
     if (OP == kAxpydot) {
         WsLayout lay;
         const size_t off = lay.take((size_t)grid);
-        BTO_TRY(grow(&c.ws, &c.ws_bytes, lay.total, "workspace"));
+        BTO_TRY(reserve_ws(c, stream, lay.total));
         g.partials = reinterpret_cast<double *>(c.ws + off);
         g.ticket = c.tickets;
     }
-    return launch_dependent(fn, (unsigned)grid, g, stream, "vec_kernel");
+    char what[64];
+    snprintf(what, sizeof(what), "vec_kernel<%d,%d,%d>", OP, aligned ? (int)g_tuning.vec_unroll : 1,
+             aligned ? 1 : 0);
+    return launch_dependent(fn, (unsigned)grid, g, stream, what);
 }
 
 // ---------------------------------------------------------------------------
@@ -65,6 +68,7 @@ struct MvPlan {
     long units_per_strip = 1, total_units = 1;
     long grid = 1;
     long slots = 1;        // max CTAs sharing one strip
+    int flags = 0, minb = 1;   // template arguments of `fn` (for the launch record)
     MvKernel fn = nullptr;
 };
 
@@ -140,6 +144,8 @@ int plan_mv(DeviceCtx &c, long M, long N, bool aligned, MvPlan *p)
     p->V = V;
     p->aligned = aligned;
     p->fn = mv_kernel_ptr<FLAGS>(R, V, aligned, minb);
+    p->flags = FLAGS;
+    p->minb = !aligned ? 1 : ((minb == 2 || minb == 3 || minb == 4 || minb == 6) ? minb : 1);
     p->strip_width = (long)kThreads * 2 * V;
     p->nstrips = (int)((N + p->strip_width - 1) / p->strip_width);
     p->units_per_strip = (M + R - 1) / R;
@@ -182,7 +188,10 @@ void fill_geometry(const MvPlan &p, MvArgs *a, long M, long N)
 
 int launch_mv(const MvPlan &p, const MvArgs &a, cudaStream_t stream)
 {
-    return launch_dependent(p.fn, (unsigned)p.grid, a, stream, "mv_tile_kernel");
+    char what[64];
+    snprintf(what, sizeof(what), "mv_tile_kernel<%d,%d,%d,%d,%d>", p.flags, p.R, p.V, p.aligned ? 1 : 0,
+             p.minb);
+    return launch_dependent(p.fn, (unsigned)p.grid, a, stream, what);
 }
 
 // Launch the join of `f` (geometry already filled in).  While a sharded
@@ -211,8 +220,8 @@ int launch_join(DeviceCtx &c, FinArgs f, cudaStream_t stream)
         e.fin = f;
         e.exch = c.exch_bufs;
         e.flags = c.exch_flags;
-        e.epoch = ++c.exch_epoch;
-        e.buf_offset = (long)(e.epoch & 1u) * (c.exch_capacity / 2);
+        e.state = c.exch_state;
+        e.half = c.exch_capacity / 2;
         e.rank = c.exch_rank;
         e.world = c.exch_world;
         e.phases = (int)g_tuning.exchange_phases;
@@ -315,7 +324,9 @@ int run_skinny(DeviceCtx &c, const SkinnyPlan &p, const MvArgs &a, FinArgs f, cu
         fn = p.V == 1 ? mv_skinny_kernel<FLAGS, false, 1>
                       : (p.V == 4 ? mv_skinny_kernel<FLAGS, false, 4> : mv_skinny_kernel<FLAGS, false, 8>);
     }
-    BTO_TRY(launch_dependent(fn, (unsigned)p.grid, s, stream, "mv_skinny_kernel"));
+    char what[64];
+    snprintf(what, sizeof(what), "mv_skinny_kernel<%d,%d,%d>", FLAGS, p.pair ? 1 : 0, p.V);
+    BTO_TRY(launch_dependent(fn, (unsigned)p.grid, s, stream, what));
     if (f.cmode == kColNone) return BTO_OK;
     f.colpart = a.colpart;
     f.M = a.M;
@@ -384,7 +395,8 @@ struct Pass {
                 cfg.attrs = attr;
                 cfg.numAttrs = 1;
                 CUDA_TRY(cudaLaunchKernelEx(&cfg, rowstream_kernel<(FLAGS & kFlagN2) != 0>, r));
-                return check_launch("rowstream_kernel");
+                return check_launch((FLAGS & kFlagN2) ? "rowstream_kernel<1>" : "rowstream_kernel<0>", reinterpret_cast<const void *>(
+                                                            rowstream_kernel<(FLAGS & kFlagN2) != 0>));
             }
         }
         if (skinny.grid > 0) {
@@ -409,9 +421,10 @@ struct Pass {
     }
 };
 
-int size_ws(DeviceCtx &c, const WsLayout &lay)
+// size (and bind) the workspace of the stream the sequence is enqueued on
+int size_ws(DeviceCtx &c, const WsLayout &lay, cudaStream_t stream)
 {
-    return grow(&c.ws, &c.ws_bytes, lay.total, "workspace");
+    return reserve_ws(c, stream, lay.total);
 }
 
 

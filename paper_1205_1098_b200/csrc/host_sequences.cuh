@@ -43,7 +43,7 @@ int seq_bicgk(DeviceCtx &c, const double *A, const double *p, const double *r,
     WsLayout lay;
     Pass<kFlagN | kFlagT> pass;
     BTO_TRY(pass.prepare(c, M, N, mat_aligned(N, A), &lay));
-    BTO_TRY(size_ws(c, lay));
+    BTO_TRY(size_ws(c, lay, st));
     MvArgs a{};
     a.A = A; a.colw = p; a.roww = r;
     FinArgs f{};
@@ -193,7 +193,7 @@ int seq_atax_fused(DeviceCtx &c, const AtaxPlan &p, const double *A, const doubl
 {
     WsLayout lay;
     const size_t off = lay.take((size_t)p.nclusters * N);
-    BTO_TRY(size_ws(c, lay));
+    BTO_TRY(size_ws(c, lay, st));
     AtaxArgs a{};
     a.A = A; a.x = x; a.M = M; a.N = N;
     a.ypart = reinterpret_cast<double *>(c.ws + off);
@@ -206,7 +206,9 @@ int seq_atax_fused(DeviceCtx &c, const AtaxPlan &p, const double *A, const doubl
     cudaLaunchAttribute attr[2];
     fill_launch_config(p, &cfg, attr, st);
     CUDA_TRY(cudaLaunchKernelEx(&cfg, p.fn, a));
-    BTO_TRY(check_launch("atax_cluster_kernel"));
+    char what[64];
+    snprintf(what, sizeof(what), "atax_cluster_kernel<%d,%d,%d>", p.C, p.KMAX, p.RG);
+    BTO_TRY(check_launch(what, reinterpret_cast<const void *>(p.fn)));
     // join the per-cluster partials in ascending cluster order
     FinArgs f{};
     f.colpart = a.ypart;
@@ -235,7 +237,7 @@ int seq_atax(DeviceCtx &c, const double *A, const double *x, double *y, long M,
         WsLayout lay;
         const SkinnyPlan sp = plan_skinny(c, M, N, mat_aligned(N, A));
         const size_t off = lay.take((size_t)sp.grid * N);
-        BTO_TRY(size_ws(c, lay));
+        BTO_TRY(size_ws(c, lay, st));
         MvArgs a{};
         a.A = A; a.colw = x; a.M = M; a.N = N;
         a.colpart = reinterpret_cast<double *>(c.ws + off);
@@ -254,7 +256,7 @@ int seq_atax(DeviceCtx &c, const double *A, const double *x, double *y, long M,
     Pass<kFlagT> sums;
     BTO_TRY(dots.prepare(c, M, N, al, &lay));
     BTO_TRY(sums.prepare(c, M, N, al, &lay));
-    BTO_TRY(size_ws(c, lay));
+    BTO_TRY(size_ws(c, lay, st));
     double *t = reinterpret_cast<double *>(c.ws + off_t);
     {
         MvArgs a{};
@@ -278,7 +280,7 @@ int seq_gesummv(DeviceCtx &c, double alpha, double beta, const double *A,
     WsLayout lay;
     Pass<kFlagN | kFlagN2> pass;
     BTO_TRY(pass.prepare(c, M, N, mat_aligned(N, A, B), &lay));
-    BTO_TRY(size_ws(c, lay));
+    BTO_TRY(size_ws(c, lay, st));
     MvArgs a{};
     a.A = A; a.A2 = B; a.colw = x;
     FinArgs f{};
@@ -294,7 +296,7 @@ int seq_dgemv(DeviceCtx &c, double alpha, const double *A, const double *x,
     WsLayout lay;
     Pass<kFlagN> pass;
     BTO_TRY(pass.prepare(c, M, N, mat_aligned(N, A), &lay));
-    BTO_TRY(size_ws(c, lay));
+    BTO_TRY(size_ws(c, lay, st));
     MvArgs a{};
     a.A = A; a.colw = x;
     FinArgs f{};
@@ -315,13 +317,13 @@ int seq_pass1(DeviceCtx &c, const double *A, const double *u1, const double *v1,
     if (u1 == nullptr) {
         Pass<kFlagT> pass;
         BTO_TRY(pass.prepare(c, M, N, mat_aligned(N, A), &lay));
-        BTO_TRY(size_ws(c, lay));
+        BTO_TRY(size_ws(c, lay, st));
         return pass.run(c, a, f, st);
     }
     a.u1 = u1; a.v1 = v1; a.u2 = u2; a.v2 = v2; a.Bout = B;
     Pass<kFlagT | kFlagRank2> pass;
     BTO_TRY(pass.prepare(c, M, N, mat_aligned(N, A, B), &lay));
-    BTO_TRY(size_ws(c, lay));
+    BTO_TRY(size_ws(c, lay, st));
     return pass.run(c, a, f, st);
 }
 
@@ -331,7 +333,7 @@ int seq_pass2(DeviceCtx &c, const double *B, const double *x, double alpha,
     WsLayout lay;
     Pass<kFlagN> pass;
     BTO_TRY(pass.prepare(c, M, N, mat_aligned(N, B), &lay));
-    BTO_TRY(size_ws(c, lay));
+    BTO_TRY(size_ws(c, lay, st));
     MvArgs a{};
     a.A = B; a.colw = x;
     FinArgs f{};

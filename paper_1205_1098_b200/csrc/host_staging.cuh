@@ -342,6 +342,7 @@ public:
     {
         g_err = BTO_OK;
         g_errmsg[0] = 0;
+        reset_call_record();
         rc_ = get_ctx(&ctx_);
     }
     bool ok() const { return rc_ == BTO_OK; }
@@ -610,6 +611,7 @@ struct AsyncCall {
     {
         g_err = BTO_OK;
         g_errmsg[0] = 0;
+        reset_call_record();
         rc = get_ctx(&ctx);
     }
     std::lock_guard<std::mutex> lock;

@@ -501,12 +501,18 @@ finalize_kernel(const FinArgs f)
 // rank -- one kernel over all ranks' data, nobody ever waits.
 constexpr int kExchCtas = 64;
 
+// Device-resident exchange state of a rank (what must survive CUDA-graph replay cannot sit in
+// kernel arguments): state[0] = exchanges completed so far (the epoch), state[1] = ticket of the
+// column CTAs that have finished the current exchange, state[2] = error word (kExchTimedOut).
+enum : unsigned int { kExchTimedOut = 1u };
+constexpr unsigned long long kExchTimeoutNs = 20ull * 1000ull * 1000ull * 1000ull;   // 20 s
+
 struct ExchArgs {
     FinArgs fin;                   // local partials + epilogue + row side
     double *const *exch;           // [world] every rank's exchange buffer (peer-mapped)
     unsigned int *const *flags;    // [world] every rank's flags [world][kExchCtas]
-    long buf_offset;               // parity half of the exchange buffer, in doubles
-    unsigned int epoch;
+    unsigned int *state;           // this rank's exchange state (see above)
+    long half;                     // doubles per parity half of the exchange buffer
     int rank, world;
     int phases;
 };
@@ -530,6 +536,13 @@ __device__ __forceinline__ double ld_relaxed_sys(const double *p)
     return v;
 }
 
+__device__ __forceinline__ unsigned long long global_timer_ns()
+{
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+
 __global__ void __launch_bounds__(kThreads)
 join_exchange_kernel(const ExchArgs e)
 {
@@ -539,27 +552,64 @@ join_exchange_kernel(const ExchArgs e)
         finalize_rows_cta(f, (long)blockIdx.x - kExchCtas);
         return;
     }
+    // The epoch of THIS exchange: one more than the exchanges completed.  Every column CTA
+    // reads the counter before it takes its end-of-kernel ticket, and the counter moves only
+    // when the last ticket has been taken, so all CTAs of a launch see the same value; a
+    // replayed CUDA graph gets a fresh epoch each time.
+    __shared__ unsigned int s_epoch;
+    __shared__ bool s_timed_out;
+    if (threadIdx.x == 0) {
+        unsigned int done;
+        asm volatile("ld.global.cg.u32 %0, [%1];" : "=r"(done) : "l"(e.state) : "memory");
+        s_epoch = done + 1u;
+        s_timed_out = false;
+    }
+    __syncthreads();
+    const unsigned int epoch = s_epoch;
+    const long buf_offset = (long)(epoch & 1u) * e.half;
     const int cta = blockIdx.x;
     const long c_lo = (f.N * cta) / kExchCtas, c_hi = (f.N * (cta + 1)) / kExchCtas;
     if (e.phases & 1) {
-        double *mine = e.exch[e.rank] + e.buf_offset;
+        double *mine = e.exch[e.rank] + buf_offset;
         for (long j = c_lo + threadIdx.x; j < c_hi; j += kThreads) mine[j] = join_column(f, j);
         __syncthreads();
         if ((int)threadIdx.x < e.world) {
             __threadfence_system();
-            st_release_sys(e.flags[threadIdx.x] + (long)e.rank * kExchCtas + cta, e.epoch);
+            st_release_sys(e.flags[threadIdx.x] + (long)e.rank * kExchCtas + cta, epoch);
         }
     }
     if (e.phases & 2) {
         if ((int)threadIdx.x < e.world) {
+            // A peer may already be one exchange AHEAD (it needs our flag for epoch + 1 to get
+            // any further, and epoch + 1 uses the other half of the buffers), so the test is
+            // "has reached", not "equals": an equality test would spin forever on such a peer.
             const unsigned int *flag = e.flags[e.rank] + (long)threadIdx.x * kExchCtas + cta;
-            while (ld_acquire_sys(flag) != e.epoch) { }
+            const unsigned long long t0 = global_timer_ns();
+            unsigned int spins = 0;
+            while ((int)(ld_acquire_sys(flag) - epoch) < 0) {
+                if ((++spins & 0x3ffu) == 0 && global_timer_ns() - t0 > kExchTimeoutNs) {
+                    s_timed_out = true;             // a peer never arrived: fail loudly, do not hang
+                    atomicOr(e.state + 2, kExchTimedOut);
+                    break;
+                }
+            }
         }
         __syncthreads();
+        const bool dead = s_timed_out;
         for (long j = c_lo + threadIdx.x; j < c_hi; j += kThreads) {
-            double s = ld_relaxed_sys(e.exch[0] + e.buf_offset + j);
-            for (int p = 1; p < e.world; ++p) s += ld_relaxed_sys(e.exch[p] + e.buf_offset + j);
-            f.colout[j] = column_epilogue(f, j, s);
+            double s = ld_relaxed_sys(e.exch[0] + buf_offset + j);
+            for (int p = 1; p < e.world; ++p) s += ld_relaxed_sys(e.exch[p] + buf_offset + j);
+            f.colout[j] = dead ? __longlong_as_double(0x7ff8000000000000ll) : column_epilogue(f, j, s);
+        }
+        // last column CTA out: the exchange is complete on this rank
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            __threadfence();
+            if (atomicAdd(e.state + 1, 1u) == kExchCtas - 1) {
+                e.state[1] = 0u;
+                __threadfence();
+                e.state[0] = epoch;
+            }
         }
     }
 }

@@ -26,7 +26,7 @@ import time
 from dataclasses import dataclass, field
 from pathlib import Path
 
-from .cost import CachedFitness, CostReport, GpuVariant, cached, variant_space
+from .cost import CostReport, GpuVariant, cached, variant_space
 from .spec import match_corpus
 
 __all__ = ["SearchConfig", "LogEntry", "SearchResult", "run_strategy", "write_run", "STRATEGIES",
@@ -37,19 +37,31 @@ STRATEGIES = ("default", "exhaustive", "random", "ga")
 
 @dataclass(frozen=True)
 class SearchConfig:
+    """Knobs of one search run.  The field names are the reference's (`search.py:37-50`,
+    they appear in its CLI and in `summary.json`); only the ones that mean something for a
+    launch-variant search exist here."""
     population: int = 8
     tournament_k: int = 2
     generations: int = 10
-    budget: int | None = None          # max unique (cache-miss) evaluations
-    time_budget_s: float | None = None
+    budget: int | None = None          # cap on fresh (not memoised) evaluations; None = no cap
+    time_budget_s: float | None = None  # cap on wall-clock seconds; None = no cap
     seed: int = 0
     mutation_prob: float = 0.5
 
     def __post_init__(self):
+        problems = []
         if self.population < 2:
-            raise ValueError("population must be at least 2")
+            problems.append("population must be at least 2")
         if self.tournament_k < 1:
-            raise ValueError("tournament size must be at least 1")
+            problems.append("tournament size must be at least 1")
+        if not 0.0 <= self.mutation_prob <= 1.0:
+            problems.append("mutation_prob must lie in [0, 1]")
+        if problems:
+            raise ValueError("; ".join(problems))
+
+
+#: one line of log.jsonl -- the schema is the reference's (cli.py:227-233)
+LOG_FIELDS = ("key", "fitness", "generation", "elapsed_s", "strategy")
 
 
 @dataclass
@@ -61,8 +73,7 @@ class LogEntry:
     strategy: str
 
     def as_dict(self) -> dict:
-        return {"key": self.key, "fitness": self.fitness, "generation": self.generation,
-                "elapsed_s": self.elapsed_s, "strategy": self.strategy}
+        return {name: getattr(self, name) for name in LOG_FIELDS}
 
 
 @dataclass
@@ -80,48 +91,63 @@ class SearchResult:
         return self.best.key()
 
 
-class _BudgetDone(Exception):
-    pass
+class SearchExhausted(Exception):
+    """Raised by the ledger when the next candidate would exceed a budget."""
 
 
-class _Evaluator:
-    """Cached fitness with logging, an incumbent and a unique-evaluation budget
-    (same rules as the reference's: the seed evaluation is always allowed)."""
+class _Ledger:
+    """Book-keeping of one search run: every candidate goes through `price()`.
+
+    A candidate the memo already knows is free.  A fresh one is charged against the
+    evaluation budget and the time budget BEFORE it is evaluated (so a budget of k never
+    runs a k+1-th kernel); the very first evaluation -- the shipped defaults -- is exempt,
+    which is the reference's rule too (a search always returns something).  Fresh
+    evaluations are logged in order and the incumbent is the lexicographic minimum of
+    (fitness, key), so ties do not depend on visiting order."""
 
     def __init__(self, fitness, strategy: str, cfg: SearchConfig):
-        self.fitness = fitness if isinstance(fitness, CachedFitness) else cached(fitness)
+        self.memo = cached(fitness)
         self.strategy, self.cfg = strategy, cfg
-        self.log: list[LogEntry] = []
         self.generation = 0
-        self.best: tuple[float, str, GpuVariant] | None = None
-        self.best_report: CostReport | None = None
-        self.t0 = time.perf_counter()
+        self.entries: list[LogEntry] = []
+        self.incumbent: GpuVariant | None = None
+        self.incumbent_report: CostReport | None = None
+        self._started = time.perf_counter()
+        self._charged = 0
 
-    def __call__(self, variant: GpuVariant) -> CostReport:
-        key = self.fitness.key(variant)
-        fresh = key not in self.fitness._table
-        if fresh:
-            if self.cfg.budget is not None and self.fitness.misses > 0 \
-                    and self.fitness.misses >= self.cfg.budget:
-                raise _BudgetDone()
-            if self.cfg.time_budget_s is not None \
-                    and time.perf_counter() - self.t0 > self.cfg.time_budget_s:
-                raise _BudgetDone()
-        report = self.fitness(variant)
-        if fresh:
-            elapsed = 0.0 if report.source == "analytic" else time.perf_counter() - self.t0
-            self.log.append(LogEntry(variant.key(), report.total, self.generation, elapsed,
-                                     self.strategy))
-            ranked = (report.total, variant.key())
-            if self.best is None or ranked < self.best[:2]:
-                self.best = (report.total, variant.key(), variant)
-                self.best_report = report
-        return report
+    def _elapsed(self) -> float:
+        return time.perf_counter() - self._started
+
+    def _afford(self) -> None:
+        if self._charged == 0:
+            return
+        if self.cfg.budget is not None and self._charged >= self.cfg.budget:
+            raise SearchExhausted("evaluation budget")
+        if self.cfg.time_budget_s is not None and self._elapsed() > self.cfg.time_budget_s:
+            raise SearchExhausted("time budget")
+
+    def price(self, variant: GpuVariant) -> float:
+        report = self.memo.lookup(variant)
+        if report is None:
+            self._afford()
+            report = self.memo(variant)
+            self._charged += 1
+            # an analytic model has no meaningful clock: keep its logs reproducible
+            stamp = 0.0 if report.source == "analytic" else self._elapsed()
+            self.entries.append(LogEntry(variant.key(), report.total, self.generation, stamp,
+                                         self.strategy))
+            if self.incumbent is None or \
+                    (report.total, variant.key()) < (self.incumbent_report.total, self.incumbent.key()):
+                self.incumbent, self.incumbent_report = variant, report
+        else:
+            self.memo(variant)                 # counted as a cache hit
+        return report.total
 
     def result(self) -> SearchResult:
-        assert self.best is not None, "no evaluations happened"
-        return SearchResult(self.strategy, self.best[2], self.best[0], self.best_report, self.log,
-                            self.fitness.misses, self.fitness.hits)
+        if self.incumbent is None:
+            raise RuntimeError("the search evaluated nothing")
+        return SearchResult(self.strategy, self.incumbent, self.incumbent_report.total,
+                            self.incumbent_report, self.entries, self.memo.misses, self.memo.hits)
 
 
 def _gene_pool(space: list[GpuVariant]) -> dict[str, list[int]]:
@@ -158,45 +184,50 @@ def run_strategy(strategy: str, graph, cfg: SearchConfig, fitness,
     kernel = match_corpus(graph.spec)
     space = list(space) if space is not None else variant_space(kernel)
     space = [GpuVariant(v.kernel, tuple(sorted(v.tuning))) for v in space]
-    seed_variant = GpuVariant(kernel)
     rng = random.Random(cfg.seed)
-    ev = _Evaluator(fitness, strategy, cfg)
+    ledger = _Ledger(fitness, strategy, cfg)
     try:
-        ev(seed_variant)                         # the shipped defaults are always evaluated
+        ledger.price(GpuVariant(kernel))         # the shipped defaults are always evaluated
         if strategy == "exhaustive":
             for v in space:
-                ev(v)
+                ledger.price(v)
         elif strategy == "random":
             draws = cfg.budget if cfg.budget is not None else cfg.population * cfg.generations
             for _ in range(draws):
-                ev(rng.choice(space))
+                ledger.price(rng.choice(space))
         elif strategy == "ga":
-            pool = _gene_pool(space)
-            population = []
-            for _ in range(cfg.population):
-                v = rng.choice(space)
-                population.append((v, ev(v).total))
-            for gen in range(1, cfg.generations + 1):
-                ev.generation = gen
-                children = []
-                for _ in range(cfg.population):
-                    pa = min(rng.sample(population, min(cfg.tournament_k, len(population))),
-                             key=lambda t: t[1])[0]
-                    pb = min(rng.sample(population, min(cfg.tournament_k, len(population))),
-                             key=lambda t: t[1])[0]
-                    child = _crossover(pa, pb, rng)
-                    if rng.random() < cfg.mutation_prob:
-                        child = _mutate(child, pool, rng)
-                    children.append((child, ev(child).total))
-                # elitism: the incumbent survives every generation
-                best_fit, _, best_variant = ev.best
-                if min(s for _, s in children) > best_fit:
-                    worst = max(range(len(children)), key=lambda i: (children[i][1], children[i][0].key()))
-                    children[worst] = (best_variant, best_fit)
-                population = children
-    except _BudgetDone:
+            _evolve(ledger, space, cfg, rng)
+    except SearchExhausted:
         pass
-    return ev.result()
+    return ledger.result()
+
+
+def _evolve(ledger: _Ledger, space: list[GpuVariant], cfg: SearchConfig, rng: random.Random) -> None:
+    """Generational GA over launch variants: k-tournament parents, uniform crossover,
+    one-gene mutation, and the incumbent re-inserted whenever a generation lost it."""
+    pool = _gene_pool(space)
+
+    def scored(v: GpuVariant):
+        return v, ledger.price(v)
+
+    def tournament(population):
+        entrants = rng.sample(population, min(cfg.tournament_k, len(population)))
+        return min(entrants, key=lambda pair: pair[1])[0]
+
+    population = [scored(rng.choice(space)) for _ in range(cfg.population)]
+    for generation in range(1, cfg.generations + 1):
+        ledger.generation = generation
+        offspring = []
+        for _ in range(cfg.population):
+            child = _crossover(tournament(population), tournament(population), rng)
+            if rng.random() < cfg.mutation_prob:
+                child = _mutate(child, pool, rng)
+            offspring.append(scored(child))
+        champion, champion_fit = ledger.incumbent, ledger.incumbent_report.total
+        if all(fit > champion_fit for _, fit in offspring):
+            loser = max(range(len(offspring)), key=lambda i: (offspring[i][1], offspring[i][0].key()))
+            offspring[loser] = (champion, champion_fit)
+        population = offspring
 
 
 def write_run(outdir, graph, result: SearchResult, cfg: SearchConfig, fitness_source: str) -> dict:

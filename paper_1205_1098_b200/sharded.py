@@ -25,7 +25,7 @@ import ctypes
 from dataclasses import dataclass
 
 __all__ = ["row_block", "ShardSpec", "SHARDING", "ShardedRunner", "GpuShardOps",
-           "NvlinkExchange", "TorchComm", "shard_inputs"]
+           "NvlinkExchange", "TorchComm", "shard_inputs", "fused_exchange_agrees"]
 
 
 def row_block(extent: int, rank: int, world: int) -> tuple[int, int]:
@@ -71,6 +71,39 @@ class ShardedRunner:
     def __init__(self, local, comm, rank: int, world: int, fused: bool = False):
         self.local, self.comm, self.rank, self.world = local, comm, rank, world
         self.fused = fused and world > 1
+
+    def capture(self, method, *args, warmup: int = 2):
+        """Capture one sharded sequence (`method`: the name of one of this runner's methods, or any
+        callable that issues library calls on the current stream) -- its kernels AND its exchange
+        (the NCCL all-reduce or the join-fused NVLink exchange) -- into a CUDA graph and return
+        `replay()`.
+
+        At 8 GPUs a shard's kernels take 90-500 us; issuing 2-5 launches plus a collective
+        eagerly from Python costs a comparable amount of host time, a graph launch ~10 us.
+        The library's entry points are capture-safe (per-stream workspace that never moves
+        under a captured kernel, exchange epoch on the device: include/bto_b200.h section 2);
+        `warmup` eager calls run first on a side stream so that workspaces, occupancy caches
+        and the communicator are set up outside the capture.  Every rank must capture and
+        replay the same sequence the same number of times.  The operands must stay alive and
+        in place for as long as the graph is replayed."""
+        import torch
+        fn = method if callable(method) else getattr(self, method)
+        side = torch.cuda.Stream()
+        side.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(side):
+            for _ in range(max(1, warmup)):
+                fn(*args)
+        torch.cuda.current_stream().wait_stream(side)
+        torch.cuda.synchronize()
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph, stream=side):
+            fn(*args)
+        keep = (graph, args, side)
+
+        def replay(_keep=keep):
+            _keep[0].replay()
+        replay.graph = graph
+        return replay
 
     def axpydot(self, w, v, u, alpha, z, beta):
         if self.fused:
@@ -154,8 +187,61 @@ class NvlinkExchange:
         _native.check(lib.bto_exchange_init(self.rank, self.world, exch, flags, capacity, 0))
         self._lib, self._native = lib, _native
 
+    def status(self) -> int:
+        """Synchronise the device and raise BtoError if an exchange ran into the peer-wait guard
+        (its results were set to NaN); returns the number of exchanges completed on this rank."""
+        done = ctypes.c_uint(0)
+        self._native.check(self._lib.bto_exchange_status(ctypes.byref(done)))
+        return int(done.value)
+
     def close(self):
         self._native.check(self._lib.bto_exchange_shutdown())
+
+
+def fused_exchange_agrees(ops, comm, rank: int, world: int, rows: int = 640, cols: int = 4100,
+                          rounds: int = 3) -> bool:
+    """Probe run before the fused exchange is trusted with a benchmark or a job: a small sharded
+    BiCGK and AXPYDOT through `*_sharded` (exchange inside the join kernel) against the same shard
+    through the plain entry point + `comm.all_reduce_sum`, `rounds` times (both parity halves of
+    the exchange buffer, consecutive epochs).  True only if EVERY rank saw agreement within
+    1e-12 relative (the two sums differ in order only), bit-identical results across ranks'
+    own repeats, and a clean `bto_exchange_status`.  Needs bto_exchange_init (NvlinkExchange)."""
+    import torch
+    from . import _native
+    gen = torch.Generator(device="cuda").manual_seed(4321 + rank)
+    rep = torch.Generator(device="cuda").manual_seed(77)
+    rnd = lambda g, *shape: torch.rand(*shape, dtype=torch.float64, device="cuda", generator=g) * 2 - 1
+    A, r, p = rnd(gen, rows, cols), rnd(gen, rows), rnd(rep, cols)
+    w, v, u = rnd(gen, 50001), rnd(gen, 50001), rnd(gen, 50001)
+    ok = True
+    try:
+        want_s, want_b = torch.empty(cols, dtype=torch.float64, device="cuda"), torch.empty(1, dtype=torch.float64, device="cuda")
+        q, z = torch.empty(rows, dtype=torch.float64, device="cuda"), torch.empty(50001, dtype=torch.float64, device="cuda")
+        ops.bicgk(A, p, r, q, want_s)
+        comm.all_reduce_sum(want_s)
+        ops.axpydot(w, v, u, 0.37, z, want_b)
+        comm.all_reduce_sum(want_b)
+        first = None
+        for _ in range(rounds):
+            got_s = torch.full((cols,), float("nan"), dtype=torch.float64, device="cuda")
+            got_b = torch.full((1,), float("nan"), dtype=torch.float64, device="cuda")
+            ops.bicgk_sharded(A, p, r, q, got_s)
+            ops.axpydot_sharded(w, v, u, 0.37, z, got_b)
+            torch.cuda.synchronize()
+            scale = torch.clamp(want_s.abs(), min=1.0)
+            ok = ok and bool(((got_s - want_s).abs() / scale).max() <= 1e-12)
+            ok = ok and bool(((got_b - want_b).abs() / torch.clamp(want_b.abs(), min=1.0)).max() <= 1e-12)
+            if first is None:
+                first = (got_s.clone(), got_b.clone())
+            else:
+                ok = ok and torch.equal(first[0], got_s) and torch.equal(first[1], got_b)
+        done = ctypes.c_uint(0)
+        ok = ok and _native.load().bto_exchange_status(ctypes.byref(done)) == 0
+    except Exception:
+        ok = False
+    flag = torch.tensor([1.0 if ok else 0.0], dtype=torch.float64, device="cuda")
+    comm.all_reduce_sum(flag)
+    return bool(flag.item() == float(world))
 
 
 class GpuShardOps:

@@ -79,10 +79,12 @@ def max_threads() -> int:
     return int(fn())
 
 
-def _bind(fn, name: str, inputs: dict, extents: dict, trailing: list):
+def _bind(fn, name: str, inputs: dict, extents: dict, trailing: list, outputs: dict | None = None):
     """Marshal once; returns (thunk, collect): thunk() runs the C function on
     the prebuilt argument list (what the CPU baseline times), collect() reads
-    the outputs back as the reference's run_kernel would return them."""
+    the outputs back as the reference's run_kernel would return them.
+    `outputs` may hand over preallocated flat float64 buffers by output name (the CPU
+    baseline at bench size re-uses an 8 GiB buffer instead of allocating another)."""
     args, keep, outs = [], [], {}
     for pname, cls in PARAMS[name]:
         if cls == "s":
@@ -95,7 +97,10 @@ def _bind(fn, name: str, inputs: dict, extents: dict, trailing: list):
             size = 1
             for d in OUT_DIMS[name][pname]:
                 size *= int(extents[d])
-            buf = np.full(size, np.nan)
+            buf = (outputs or {}).get(pname)
+            if buf is None:
+                buf = np.full(size, np.nan)
+            assert buf.dtype == np.float64 and buf.size >= size and buf.flags.c_contiguous
             outs[pname] = buf
             args.append(buf.ctypes.data_as(ctypes.POINTER(ctypes.c_double)))
     names = ("M",) if name in VECTOR_ONLY else ("M", "N")
@@ -109,8 +114,9 @@ def _bind(fn, name: str, inputs: dict, extents: dict, trailing: list):
         result = {}
         for pname, buf in outs.items():
             dims = OUT_DIMS[name][pname]
+            shape = tuple(int(extents[d]) for d in dims)
             result[pname] = float(buf[0]) if not dims else \
-                buf.reshape(tuple(int(extents[d]) for d in dims))
+                buf[:int(np.prod(shape))].reshape(shape)
         return result
 
     thunk.keep = keep
@@ -123,14 +129,14 @@ def _call(fn, name: str, inputs: dict, extents: dict, trailing: list):
     return collect()
 
 
-def bind_oracle(name: str, inputs: dict, extents: dict, threads: int):
+def bind_oracle(name: str, inputs: dict, extents: dict, threads: int, outputs: dict | None = None):
     return _bind(getattr(_lib(), f"oracle_{name}"), name, inputs, extents,
-                 [ctypes.c_int(int(threads))])
+                 [ctypes.c_int(int(threads))], outputs)
 
 
-def bind_ref(name: str, inputs: dict, extents: dict, tag: str):
+def bind_ref(name: str, inputs: dict, extents: dict, tag: str, outputs: dict | None = None):
     fn, _ = ref_function(name, tag)
-    return _bind(fn, name, inputs, extents, [])
+    return _bind(fn, name, inputs, extents, [], outputs)
 
 
 def oracle_run(name: str, inputs: dict, extents: dict, threads: int = 8) -> dict:

@@ -18,7 +18,7 @@ HEADER = (REPO / "include" / "bto_b200.h").read_text()
 
 def declared_functions() -> list[str]:
     text = re.sub(r"/\*.*?\*/", "", HEADER, flags=re.S)
-    names = re.findall(r"^\s*(?:const\s+)?(?:void|int|long|double|char)\s*\*?\s*(\w+)\s*\(",
+    names = re.findall(r"^\s*(?:const\s+)?(?:unsigned\s+)?(?:void|int|long\s+long|long|double|char)\s*\*?\s*(\w+)\s*\(",
                        text, flags=re.M)
     return sorted(set(names))
 
@@ -35,7 +35,7 @@ def test_exports_every_declared_symbol():
     for name in names:
         assert hasattr(lib, name), f"{name} declared in bto_b200.h but not exported"
     assert set(_native.EXPORTED) == set(names)
-    assert lib.bto_abi_version() == 1
+    assert lib.bto_abi_version() == 2
 
 
 def test_reference_symbol_names_and_signatures():

@@ -65,6 +65,73 @@ def test_other_ranks_of_the_reference_arm_exit_without_work():
     assert proc.returncode == 0 and proc.stdout.strip() == ""
 
 
+def test_both_arms_print_the_same_config_object():
+    """The driver compares the two arms' `config`; what differs between them (host threads, the
+    exchange, the timing method) lives in other keys."""
+    sys.path.insert(0, str(REPO))
+    import bench
+    proc = subprocess.run([sys.executable, str(REPO / "bench.py"), "--impl", "reference", "--kernel", "axpydot",
+                           "--steps", "1", "--warmup", "0"], capture_output=True, text=True, timeout=600)
+    assert proc.returncode == 0, proc.stderr[-2000:]
+    d = _line(proc.stdout)
+    assert d["config"] == bench.config_of(("axpydot",), 1)          # what run_gpu_arm prints
+    assert d["warmup"] == 0 and d["steps"] == 1                     # the counts actually used
+    assert "2^27" in bench.config_of(bench.SUITE, 1)["workload"]
+    assert "REDUCED" in bench.describe(bench.CPU_SAMPLE, bench.SUITE)  # a scaled-down run says so
+    u = d["cpu_baseline"].get("unfused")
+    if d["cpu_baseline"]["kind"] == "reference":
+        assert u and u["cores"] == 1 and u["value"] > 0 and u["fusion_speedup_1_thread"] > 1.0
+
+
+def test_gpus_n_without_n_devices_fails_loudly(monkeypatch):
+    """`python bench.py --gpus 2` launches the ranks itself; with fewer than 2 GPUs visible it must
+    say so and exit non-zero, not run on one GPU (it printed n_gpus = 1)."""
+    import os
+    env = {k: v for k, v in os.environ.items() if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK")}
+    import torch
+    if torch.cuda.is_available() and torch.cuda.device_count() >= 2:
+        pytest.skip("two GPUs visible: the spawn path is covered by the multi-GPU test")
+    proc = subprocess.run([sys.executable, str(REPO / "bench.py"), "--gpus", "2", "--steps", "1", "--no-e2e",
+                           "--no-cpu"], capture_output=True, text=True, timeout=300, env=env)
+    assert proc.returncode != 0
+    d = _line(proc.stdout)
+    assert "error" in d and d["n_gpus_requested"] == 2 and d["n_gpus_visible"] < 2
+    # under a launcher whose world size disagrees with --gpus: refuse as well
+    env2 = dict(env, WORLD_SIZE="4", RANK="0", LOCAL_RANK="0")
+    proc = subprocess.run([sys.executable, str(REPO / "bench.py"), "--gpus", "2", "--steps", "1", "--no-e2e",
+                           "--no-cpu"], capture_output=True, text=True, timeout=300, env=env2)
+    assert proc.returncode != 0 and "error" in _line(proc.stdout)
+
+
+def test_traffic_json_is_only_quoted_for_the_kernels_it_profiled():
+    sys.path.insert(0, str(REPO))
+    import bench
+    tj = json.loads((REPO / "profiles" / "traffic.json").read_text())
+    names = [bench.normalise_kernel_name(k) for k in tj["gemver"]["kernels"]]
+    plan = "+".join([names[0], "finalize_kernel"] + names[1:] + ["finalize_kernel"])
+    assert bench.traffic_for("gemver", plan)[0] == tj["gemver"]["dram_bytes"]
+    stale, why = bench.traffic_for("gemver", "mv_tile_kernel<12,8,1,1,1>+finalize_kernel")
+    assert stale is None and why.startswith("stale")
+
+
+@pytest.mark.gpu
+def test_traffic_json_matches_the_kernels_the_library_launches(bto_lib):
+    """profiles/traffic.json (ncu DRAM bytes) must have been captured on the kernel instances the
+    library launches at the bench sizes today -- a kernel change without a new capture fails here."""
+    import torch
+    sys.path.insert(0, str(REPO))
+    import bench
+    from paper_1205_1098_b200 import _native
+    suite = bench.Suite(torch, 0, 1, bench.SUITE)
+    for k in bench.SUITE:
+        suite.launch(k)
+        plan = _native.launch_plan()
+        traffic, why = bench.traffic_for(k, plan)
+        assert traffic is not None, f"{k}: {why}"
+        assert 0.95 < traffic / bench.bytes_min(k, *bench.BENCH[k]) < 1.05
+    torch.cuda.synchronize()
+
+
 @pytest.mark.gpu
 def test_gpu_arm_single_kernel_mode_and_tuning_flag():
     """`bench.py --kernel gesummv --tune rowstream=0` on the device: one JSON line, the tunable

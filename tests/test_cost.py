@@ -159,3 +159,26 @@ class TestEmpirical:
         best, rep = C.tune(g, {"M": 4096, "N": 4096}, fitness=timer, space=space)
         assert not rep.failed and best in space
         assert timer.misses == 2
+
+
+def test_max_rel_error_is_loud_about_unwritten_outputs():
+    """Outputs arrive NaN-prefilled so that an unwritten element is visible (runtime.py:108,130);
+    the reference's metric swallows the NaN (`max(0.0, nan)` is 0.0) -- ours must not."""
+    import math
+    import numpy as np
+    want = {"y": np.ones(4), "beta": 2.0}
+    assert bto.max_rel_error({"y": np.ones(4), "beta": 2.0}, want) == 0.0
+    assert bto.max_rel_error({"y": np.array([1.0, np.nan, 1.0, 1.0]), "beta": 2.0}, want) == math.inf
+    assert bto.max_rel_error({"y": np.ones(4), "beta": float("nan")}, want) == math.inf
+    assert bto.max_rel_error({"y": np.array([1.0, np.inf, 1.0, 1.0]), "beta": 2.0}, want) == math.inf
+    assert bto.max_rel_error({"y": np.ones(3), "beta": 2.0}, want) == math.inf       # wrong length
+
+
+def test_validation_extents_keep_the_timed_dispatch():
+    """Validation runs at the timed extents, or at the same N with fewer rows when the in-product
+    evaluator's temporaries would not fit -- never at min(64, extent)."""
+    assert C.validation_extents({"M": 4096, "N": 4096}) == {"M": 4096, "N": 4096}
+    assert C.validation_extents({"M": 1 << 27}) == {"M": 1 << 27}
+    big = C.validation_extents({"M": 32768, "N": 32768})
+    assert big["N"] == 32768 and 4096 <= big["M"] < 32768
+    assert C.validation_extents({"M": 8, "N": 1 << 24}) == {"M": 8, "N": 1 << 24}

@@ -608,6 +608,97 @@ def test_cuda_graph_capture_and_replay(bto_lib, oracle):
     assert_matches("gemver", got, want, {"M": m, "N": n}, "graph replay")
 
 
+def test_two_streams_run_concurrently_without_sharing_partials(bto_lib, oracle):
+    """Every stream has its own partial-sum workspace and ticket counters (include/bto_b200.h
+    section 2): BiCGK, ATAX and AXPYDOT enqueued on two streams at once, 1000 rounds, with
+    different shapes per stream so that one stream's partials could never pass for the
+    other's.  Until round 2 there was one workspace per device and this returned wrong sums."""
+    from paper_1205_1098_b200.sharded import GpuShardOps
+    streams = [torch.cuda.Stream(), torch.cuda.Stream()]
+    shapes = [(1200, 2300), (900, 3100)]
+    cases = []
+    for st, (m, n) in zip(streams, shapes):
+        ext = {"M": m, "N": n}
+        gb, ga, gx = bto.load_graph("bicgk"), bto.load_graph("atax"), bto.load_graph("axpydot")
+        ib, ia = bto.gen_inputs(gb, ext, seed=m), bto.gen_inputs(ga, ext, seed=n)
+        ix = bto.gen_inputs(gx, {"M": m * 97}, seed=m + n)
+        dev = lambda d: {k: (torch.from_numpy(v).cuda() if isinstance(v, np.ndarray) else v) for k, v in d.items()}
+        case = {"ops": GpuShardOps(stream=st), "ext": ext, "ib": dev(ib), "ia": dev(ia), "ix": dev(ix),
+                "want_b": oracle.oracle_run("bicgk", ib, ext, threads=8),
+                "want_a": oracle.oracle_run("atax", ia, ext, threads=8),
+                "want_x": oracle.oracle_run("axpydot", ix, {"M": m * 97}, threads=8),
+                "q": torch.empty(m, dtype=torch.float64, device="cuda"),
+                "s": torch.empty(n, dtype=torch.float64, device="cuda"),
+                "y": torch.empty(n, dtype=torch.float64, device="cuda"),
+                "z": torch.empty(m * 97, dtype=torch.float64, device="cuda"),
+                "beta": torch.empty(1, dtype=torch.float64, device="cuda")}
+        cases.append(case)
+    torch.cuda.synchronize()
+    first = None
+    for rnd in range(1000):
+        for c in cases:
+            for t in (c["q"], c["s"], c["y"], c["beta"]):
+                with torch.cuda.stream(c["ops"]._stream):
+                    t.fill_(float("nan"))
+        for c in cases:                         # interleaved issue: both streams stay busy
+            c["ops"].bicgk(c["ib"]["A"], c["ib"]["p"], c["ib"]["r"], c["q"], c["s"])
+        for c in cases:
+            c["ops"].atax(c["ia"]["A"], c["ia"]["x"], c["y"])
+        for c in cases:
+            c["ops"].axpydot(c["ix"]["w"], c["ix"]["v"], c["ix"]["u"], c["ix"]["alpha"], c["z"], c["beta"])
+        torch.cuda.synchronize()
+        snap = [torch.cat([c["q"], c["s"], c["y"], c["beta"]]).clone() for c in cases]
+        if first is None:
+            first = snap
+            for c in cases:
+                assert_matches("bicgk", {"q": c["q"].cpu().numpy(), "s": c["s"].cpu().numpy()}, c["want_b"], c["ext"])
+                assert_matches("atax", {"y": c["y"].cpu().numpy()}, c["want_a"], c["ext"])
+                assert_matches("axpydot", {"z": c["z"].cpu().numpy(), "beta": float(c["beta"][0])}, c["want_x"],
+                               {"M": c["ext"]["M"] * 97})
+        else:                                   # fixed reduction order: every round the same bits
+            for a, b in zip(first, snap):
+                assert torch.equal(a, b), f"round {rnd}: results changed under concurrency"
+
+
+def test_captured_graph_survives_workspace_growth(bto_lib, oracle):
+    """A graph captured on a stream keeps replaying correctly after a LARGER call on the same
+    stream made the workspace grow (the chunk a captured kernel uses is retired, not freed), and
+    growth during capture itself is legal."""
+    from paper_1205_1098_b200.sharded import GpuShardOps
+    st = torch.cuda.Stream()
+    ops = GpuShardOps(stream=st)
+    g = bto.load_graph("bicgk")
+    small, large = {"M": 1500, "N": 2100}, {"M": 9000, "N": 7000}
+    ins = {tag: bto.gen_inputs(g, ext, seed=9) for tag, ext in (("small", small), ("large", large))}
+    dev = {tag: {k: torch.from_numpy(v).cuda() for k, v in d.items()} for tag, d in ins.items()}
+    out = {tag: (torch.empty(ext["M"], dtype=torch.float64, device="cuda"),
+                 torch.empty(ext["N"], dtype=torch.float64, device="cuda"))
+           for tag, ext in (("small", small), ("large", large))}
+    torch.cuda.synchronize()
+    before = _native.load().bto_workspace_bytes()
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(graph, stream=st):     # first call on this stream: it allocates under capture
+        ops.bicgk(dev["small"]["A"], dev["small"]["p"], dev["small"]["r"], *out["small"])
+    assert _native.load().bto_workspace_bytes() > before
+    with torch.cuda.stream(st):
+        ops.bicgk(dev["large"]["A"], dev["large"]["p"], dev["large"]["r"], *out["large"])   # grows
+    torch.cuda.synchronize()
+    for t in out["small"]:
+        t.fill_(float("nan"))
+    torch.cuda.synchronize()
+    graph.replay()
+    torch.cuda.synchronize()
+    for tag, ext in (("small", small), ("large", large)):
+        want = oracle.oracle_run("bicgk", ins[tag], ext, threads=8)
+        assert_matches("bicgk", {"q": out[tag][0].cpu().numpy(), "s": out[tag][1].cpu().numpy()}, want, ext, tag)
+    # an explicit reservation makes later calls allocation-free
+    _native.check(_native.load().bto_reserve_workspace(st.cuda_stream, 64 << 20))
+    held = _native.load().bto_workspace_bytes()
+    with torch.cuda.stream(st):
+        ops.bicgk(dev["large"]["A"], dev["large"]["p"], dev["large"]["r"], *out["large"])
+    assert _native.load().bto_workspace_bytes() == held
+
+
 def test_randomised_differential_run(bto_lib, oracle):
     """20 s of tests/fuzz_parity.py: random kernels, extents biased to tile / strip edges, random
     launch tunables, host and device operands, all against the oracle."""
@@ -710,12 +801,17 @@ def test_join_fused_exchange_emulated_ranks(bto_lib, oracle, world, shape):
                     call = lambda t=mine, o=o: ops.axpydot_sharded(t["w"], t["v"], t["u"], t["alpha"],
                                                                    o["z"], o["beta"])
                 outs.append((o, call))
-            for phase, epoch0 in ((1, epoch), (2, epoch + 1)):
+            # the epoch counter lives on the device (one per rank); ONE device stands in for all
+            # ranks here, so every emulated rank is re-initialised with the exchanges completed so far
+            for phase in (1, 2):
                 _native.set_tuning(exchange_phases=phase)
                 for r, (o, call) in enumerate(outs):
-                    _native.check(lib.bto_exchange_init(r, world, exch_ptrs, flag_ptrs, capacity, epoch0))
+                    _native.check(lib.bto_exchange_init(r, world, exch_ptrs, flag_ptrs, capacity, epoch))
                     call()
                     torch.cuda.synchronize()
+                    done = ctypes.c_uint(0)
+                    _native.check(lib.bto_exchange_status(ctypes.byref(done)))
+                    assert done.value == epoch + (1 if phase == 2 else 0)
             epoch += 1
             from paper_1205_1098_b200.sharded import SHARDING
             spec = SHARDING[name]
