@@ -556,6 +556,7 @@ static long *tuning_slot(const char *key)
     if (!strcmp(key, "exchange_phases")) return &g_tuning.exchange_phases;
     if (!strcmp(key, "skinny")) return &g_tuning.skinny;
     if (!strcmp(key, "rowstream")) return &g_tuning.rowstream;
+    if (!strcmp(key, "rowstream_min_n")) return &g_tuning.rowstream_min_n;
     if (!strcmp(key, "host_bounce")) return &g_tuning.host_bounce;
     if (!strcmp(key, "host_threads")) return &g_tuning.host_threads;
     if (!strcmp(key, "host_nt")) return &g_tuning.host_nt;
@@ -577,6 +578,7 @@ int bto_set_tuning(const char *key, long value)
     if (slot == &g_tuning.atax_fused || slot == &g_tuning.host_pipeline || slot == &g_tuning.host_bounce || slot == &g_tuning.host_nt || slot == &g_tuning.skinny) ok = value == 0 || value == 1;
     if (slot == &g_tuning.host_threads) ok = value >= 0 && value <= 64;
     if (slot == &g_tuning.rowstream) ok = value >= 0 && value <= 2;
+    if (slot == &g_tuning.rowstream_min_n) ok = value >= 1024;
     if (slot == &g_tuning.host_panel_mib) ok = value >= 1 && value <= 4096;
     if (slot == &g_tuning.exchange_phases) ok = value >= 1 && value <= 3;
     if (slot == &g_tuning.atax_cluster) ok = value == 0 || value == 1 || value == 2 || value == 4 || value == 8 || value == 16;

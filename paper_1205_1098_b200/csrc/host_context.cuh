@@ -99,6 +99,7 @@ struct Tuning {
     long debug = 0;          // print launch plans to stderr
     long exchange_phases = 3;    // bit 0 publish, bit 1 wait+reduce (tests emulate ranks with 1, 2)
     long rowstream = 1;          // GESUMMV on wide matrices streams whole rows (rowstream_kernels.cuh)
+    long rowstream_min_n = 4096; // narrowest matrix that takes the whole-row kernel
     long skinny = 1;             // N <= 256: rows shared by L threads (skinny_kernels.cuh)
     long host_bounce = 1;        // pageable operands >= 16 MiB go through pinned bounce slots
     long host_nt = 1;            // non-temporal stores in the host-side bounce copies
@@ -118,6 +119,8 @@ struct Tuning {
 // until bto_release_workspace().  Growth never synchronises the device and is legal
 // during stream capture (the allocation is made in relaxed capture mode, like
 // PyTorch's caching allocator does).
+constexpr size_t kTicketWords = 64;      // grid tickets of the vector / primitive kernels
+
 struct WsChunk {
     char *ptr = nullptr;
     size_t bytes = 0;
@@ -126,7 +129,7 @@ struct WsChunk {
 struct StreamWs {
     WsChunk cur;
     bool cur_captured = false;     // handed to a kernel while the stream was capturing
-    unsigned int *tickets = nullptr;   // 64 counters, zero between kernels
+    unsigned int *tickets = nullptr;   // kTicketWords counters, zero between kernels
     std::vector<WsChunk> retired;
 };
 
@@ -261,8 +264,8 @@ int bind_stream(DeviceCtx &c, cudaStream_t st, StreamWs **out)
     if (it == c.streams.end()) {
         RelaxedCapture relaxed;
         StreamWs fresh;
-        CUDA_TRY(cudaMalloc(&fresh.tickets, 64 * sizeof(unsigned int)));
-        CUDA_TRY(cudaMemsetAsync(fresh.tickets, 0, 64 * sizeof(unsigned int), c.util));
+        CUDA_TRY(cudaMalloc(&fresh.tickets, kTicketWords * sizeof(unsigned int)));
+        CUDA_TRY(cudaMemsetAsync(fresh.tickets, 0, kTicketWords * sizeof(unsigned int), c.util));
         CUDA_TRY(cudaStreamSynchronize(c.util));
         it = c.streams.emplace(st, fresh).first;
     }

@@ -70,6 +70,7 @@ struct MvPlan {
     long slots = 1;        // max CTAs sharing one strip
     int flags = 0, minb = 1;   // template arguments of `fn` (for the launch record)
     MvKernel fn = nullptr;
+
 };
 
 template <int FLAGS, int R, int V>
@@ -355,7 +356,7 @@ struct Pass {
         N = n;
         // two-matrix row dots of a wide matrix: stream whole rows (7.3 vs 6.9-7.07 TB/s at n = 24576)
         rowstream = (FLAGS == (kFlagN | kFlagN2) || (FLAGS == kFlagN && g_tuning.rowstream == 2)) &&
-                    aligned && g_tuning.rowstream != 0 && n >= 4096 && m >= 4L * c.sm_count;
+                    aligned && g_tuning.rowstream != 0 && n >= g_tuning.rowstream_min_n && m >= 4L * c.sm_count;
         if (rowstream) return BTO_OK;
         // (a full 512-column strip of a rank-2 pass is mv_tile_kernel's best case: 5.9 vs 4.9 TB/s)
         if (skinny_applies(N, aligned) && !((FLAGS & kFlagRank2) && N == kSkinnyMaxN)) {
@@ -411,12 +412,12 @@ struct Pass {
         a.rowpart = reinterpret_cast<double *>(c.ws + off_row);
         a.rowpart2 = reinterpret_cast<double *>(c.ws + off_row2);
         a.colpart = reinterpret_cast<double *>(c.ws + off_col);
-        BTO_TRY(launch_mv(plan, a, stream));
         f.rowpart = a.rowpart;
         f.rowpart2 = a.rowpart2;
         f.colpart = a.colpart;
         if (!(FLAGS & kFlagN)) f.rmode = kRowNone;
         if (!(FLAGS & kFlagT)) f.cmode = kColNone;
+        BTO_TRY(launch_mv(plan, a, stream));
         return launch_finalize(c, plan, f, M, N, stream);
     }
 };

@@ -190,9 +190,9 @@ __device__ __forceinline__ void mv_unit(const MvArgs &a, StripState<V> &st, long
 // MINB: minimum resident CTAs per SM the register allocator must leave room
 // for (__launch_bounds__); trades registers per thread (loads in flight per
 // thread) against warps per SM.
-template <int FLAGS, int R, int V, bool ALIGNED, int MINB>
-__global__ void __launch_bounds__(kThreads, MINB)
-mv_tile_kernel(const MvArgs a)
+// The walk of one CTA over its unit range.
+template <int FLAGS, int R, int V, bool ALIGNED>
+__device__ __forceinline__ void mv_tile_walk(const MvArgs &a)
 {
     constexpr bool kN = (FLAGS & kFlagN) != 0;
     constexpr bool kN2 = (FLAGS & kFlagN2) != 0;
@@ -309,6 +309,13 @@ mv_tile_kernel(const MvArgs a)
         }
     }
     if (kT && strip >= 0) flush_colsums();
+}
+
+template <int FLAGS, int R, int V, bool ALIGNED, int MINB>
+__global__ void __launch_bounds__(kThreads, MINB)
+mv_tile_kernel(const MvArgs a)
+{
+    mv_tile_walk<FLAGS, R, V, ALIGNED>(a);
 }
 
 // ---- finaliser: fixed-order join of the partials + the sequence's epilogue ----
@@ -478,6 +485,13 @@ finalize_kernel(const FinArgs f)
         finalize_rows_cta(f, (long)blockIdx.x - f.col_blocks);
     }
 }
+
+// (Round 2 tried folding the join into the producer for mid-size matrices -- the last CTA to arrive
+// at a strip / row unit adds its partials, ticket pattern of vec_kernels.cuh -- and measured it
+// SLOWER than this second launch: BiCGK n = 2048 16.2 us against 9.5 us, n = 4096 41.8 against
+// 29.7 (profiles/r02/midsize_join_in_producer.log).  One CTA per strip then adds ~74 partials per
+// column as a chain of L2 round trips, where finalize_kernel spreads the same loads over N/32 CTAs;
+// the launch it saves costs ~3.5 us under PDL.  Not kept.)
 
 // ---- join fused with the cross-GPU exchange (row-sharded runtime) ------------
 //
