@@ -52,9 +52,10 @@ def main(rep: str, out: str, note: str) -> None:
             continue
         entry = steps[-1].setdefault(current, {"dram_bytes": 0.0, "kernels": [], "all_kernels": []})
         entry["dram_bytes"] += to_bytes(r[ird], units[ird]) + to_bytes(r[iwr], units[iwr])
-        entry["all_kernels"].append("void " + short(r[iname]))
+        label = short(r[iname])
+        entry["all_kernels"].append(label)
         if seq is not None:
-            entry["kernels"].append("void " + short(r[iname]))
+            entry["kernels"].append(label)
     last = steps[-1]
     last["_source"] = note
     json.dump(last, open(out, "w"), indent=1)
