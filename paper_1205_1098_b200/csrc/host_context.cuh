@@ -95,6 +95,7 @@ struct Tuning {
     long atax_cluster = 0;   // cluster size of the fused ATAX (0 = auto | 1 | 2 | 4 | 8 | 16)
     long atax_stages = 0;    // TMA ring depth (0 = as many as fit, at most 8)
     long atax_rows = 0;      // 0: 16 double2 per thread per panel, 1: half-height panels
+    long direct_cols = 1;    // short-wide matrices: whole strips per CTA, column epilogue in the producer
     long pdl = 1;            // joins launched as programmatic dependents of their producer
     long debug = 0;          // print launch plans to stderr
     long exchange_phases = 3;    // bit 0 publish, bit 1 wait+reduce (tests emulate ranks with 1, 2)

@@ -59,6 +59,7 @@ int launch_vec(DeviceCtx &c, VecArgs g, cudaStream_t stream)
 // matrix kernels
 
 using MvKernel = void (*)(const MvArgs);
+using MvDirectKernel = void (*)(const MvDirectArgs);
 
 struct MvPlan {
     int R = 8, V = 1;
@@ -70,6 +71,7 @@ struct MvPlan {
     long slots = 1;        // max CTAs sharing one strip
     int flags = 0, minb = 1;   // template arguments of `fn` (for the launch record)
     MvKernel fn = nullptr;
+    MvDirectKernel direct_fn = nullptr;   // set: whole strips per CTA, columns finished in the producer
 
 };
 
@@ -130,6 +132,25 @@ constexpr MvDefault mv_default()
     return {8, 2, 8, 2};                                        // A x           7.20 TB/s
 }
 
+// The column-direct variant exists for the passes with column sums, in the tile shapes of
+// mv_shape_ok at the pass kind's default MINB.
+template <int FLAGS>
+MvDirectKernel mv_direct_kernel_ptr(int R, int V)
+{
+    if constexpr ((FLAGS & kFlagT) != 0) {
+        constexpr int minb = mv_default<FLAGS>().minb;
+        if (R == 8 && V == 1) return mv_tile_direct_kernel<FLAGS, 8, 1, minb>;
+        if (R == 16 && V == 1) return mv_tile_direct_kernel<FLAGS, 16, 1, minb>;
+        if constexpr ((FLAGS & kFlagN) == 0) {
+            if (R == 32 && V == 1) return mv_tile_direct_kernel<FLAGS, 32, 1, minb>;
+        }
+        if constexpr (FLAGS == (kFlagT | kFlagRank2) || FLAGS == (kFlagN | kFlagT)) {
+            if (R == 8 && V == 2) return mv_tile_direct_kernel<FLAGS, 8, 2, minb>;
+        }
+    }
+    return nullptr;
+}
+
 template <int FLAGS>
 int plan_mv(DeviceCtx &c, long M, long N, bool aligned, MvPlan *p)
 {
@@ -141,6 +162,10 @@ int plan_mv(DeviceCtx &c, long M, long N, bool aligned, MvPlan *p)
     // A ragged last strip takes the guarded (predicated) unit, which is slow for tall tiles; when
     // it is a large share of the matrix (N = 1000: half of it) 8-row tiles win (GEMVER 3.9 -> 5.3 TB/s)
     if (!g_tuning.mv_rows && R > 8 && N % ((long)kThreads * 2 * V) != 0 && N < 4L * kThreads * 2 * V) R = 8;
+    // fewer rows than a tall tile has: the rows beyond M would be predicated-off loads in every unit
+    if (!g_tuning.mv_rows && aligned) {
+        while (R > 8 && M <= R / 2) R /= 2;
+    }
     p->R = R;
     p->V = V;
     p->aligned = aligned;
@@ -175,6 +200,19 @@ int plan_mv(DeviceCtx &c, long M, long N, bool aligned, MvPlan *p)
         if (last - first + 1 > slots) slots = last - first + 1;
     }
     p->slots = slots;
+    // Short and very wide: at least 4 whole strips per CTA -> deal strips, finish columns in the producer
+    // (no column partials: at M = 8 they are a quarter of the matrix bytes, and their join is N / 256 CTAs)
+    p->direct_fn = nullptr;
+    if (aligned && (FLAGS & kFlagT) && g_tuning.direct_cols != 0 && !c.exch_active &&
+        p->minb == mv_default<FLAGS>().minb && (long)p->nstrips >= 4L * c.sm_count) {
+        p->direct_fn = mv_direct_kernel_ptr<FLAGS>(R, V);
+        if (p->direct_fn) {
+            long g = (long)c.sm_count * per_sm;
+            while (g > c.sm_count && (long)p->nstrips < 4 * g) g -= c.sm_count;
+            p->grid = g;
+            p->slots = 0;                  // no column partials
+        }
+    }
     return BTO_OK;
 }
 
@@ -367,7 +405,7 @@ struct Pass {
         BTO_TRY(plan_mv<FLAGS>(c, M, N, aligned, &plan));
         if (FLAGS & kFlagN) off_row = lay->take((size_t)plan.nstrips * M);
         if (FLAGS & kFlagN2) off_row2 = lay->take((size_t)plan.nstrips * M);
-        if (FLAGS & kFlagT) off_col = lay->take((size_t)plan.slots * N);
+        if ((FLAGS & kFlagT) && plan.slots > 0) off_col = lay->take((size_t)plan.slots * N);
         return BTO_OK;
     }
 
@@ -417,6 +455,22 @@ struct Pass {
         f.colpart = a.colpart;
         if (!(FLAGS & kFlagN)) f.rmode = kRowNone;
         if (!(FLAGS & kFlagT)) f.cmode = kColNone;
+        if (plan.direct_fn) {
+            MvDirectArgs d{};
+            d.mv = a;
+            d.col.out = f.colout;
+            d.col.z = f.colz;
+            d.col.scale = f.cscale;
+            d.col.mode = f.cmode;
+            d.col.vector_store = aligned16(f.colout) ? 1 : 0;
+            char what[72];
+            snprintf(what, sizeof(what), "mv_tile_direct_kernel<%d,%d,%d,%d>", plan.flags, plan.R, plan.V,
+                     plan.minb);
+            BTO_TRY(launch_dependent(plan.direct_fn, (unsigned)plan.grid, d, stream, what));
+            f.cmode = kColNone;
+            if (f.rmode == kRowNone) return BTO_OK;          // T-only pass: nothing left to join
+            return launch_finalize(c, plan, f, M, N, stream);
+        }
         BTO_TRY(launch_mv(plan, a, stream));
         return launch_finalize(c, plan, f, M, N, stream);
     }

@@ -53,6 +53,23 @@ struct MvArgs {
     int nstrips;
 };
 
+// Column epilogue of a pass (the same four cases as FinArgs::cmode below), for the kernels that
+// finish a column inside the producer (DIRECT mode of mv_tile_walk).
+struct ColEpilogue {
+    double *out;              // [N]
+    const double *z;          // mode 2: out = sum*scale + z
+    double scale;
+    int mode;                 // 1 plain, 2 axpz, 3 scale
+    int vector_store;         // out is 16-byte aligned: one 128-bit store per column pair
+};
+
+__device__ __forceinline__ double apply_col_epilogue(const ColEpilogue &e, long j, double s)
+{
+    if (e.mode == 2) return __dadd_rn(__dmul_rn(s, e.scale), e.z[j]);   // t4 = t3*beta ; x = t4 + z
+    if (e.mode == 3) return __dmul_rn(s, e.scale);                       // y = t1*beta
+    return s;
+}
+
 template <bool ALIGNED, bool BYPASS_L1>
 __device__ __forceinline__ double2 mv_load(const double *base, long row, long N,
                                            long j, bool ok0, bool ok1)
@@ -191,8 +208,11 @@ __device__ __forceinline__ void mv_unit(const MvArgs &a, StripState<V> &st, long
 // for (__launch_bounds__); trades registers per thread (loads in flight per
 // thread) against warps per SM.
 // The walk of one CTA over its unit range.
-template <int FLAGS, int R, int V, bool ALIGNED>
-__device__ __forceinline__ void mv_tile_walk(const MvArgs &a)
+// DIRECT (short, very wide matrices: thousands of strips, a handful of units each): CTAs are dealt
+// WHOLE strips, so a strip's column sums are complete when the CTA leaves it -- the column epilogue
+// is applied here and the result stored; no column partials, no column side in the join.
+template <int FLAGS, int R, int V, bool ALIGNED, bool DIRECT = false>
+__device__ __forceinline__ void mv_tile_walk(const MvArgs &a, const ColEpilogue *direct = nullptr)
 {
     constexpr bool kN = (FLAGS & kFlagN) != 0;
     constexpr bool kN2 = (FLAGS & kFlagN2) != 0;
@@ -213,8 +233,10 @@ __device__ __forceinline__ void mv_tile_walk(const MvArgs &a)
     wait_for_producer_grid();
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const long G = gridDim.x, cta = blockIdx.x;
-    const long u_begin = split_begin(a.total_units, G, cta);
-    const long u_end = split_begin(a.total_units, G, cta + 1);
+    const long u_begin = DIRECT ? split_begin(a.nstrips, G, cta) * a.units_per_strip
+                                : split_begin(a.total_units, G, cta);
+    const long u_end = DIRECT ? split_begin(a.nstrips, G, cta + 1) * a.units_per_strip
+                              : split_begin(a.total_units, G, cta + 1);
     const long M = a.M, N = a.N;
 
     long strip = -1;
@@ -230,6 +252,22 @@ __device__ __forceinline__ void mv_tile_walk(const MvArgs &a)
     int buf = 0;
 
     auto flush_colsums = [&]() {
+        if constexpr (DIRECT) {
+#pragma unroll
+            for (int v = 0; v < V; ++v) {
+                if (!ok0[v]) continue;         // (N is even on this path: ok1 == ok0)
+                double2 r;
+                r.x = apply_col_epilogue(*direct, jcol[v], csum[v].x);
+                r.y = apply_col_epilogue(*direct, jcol[v] + 1, csum[v].y);
+                if (direct->vector_store) {
+                    st_partial2(direct->out + jcol[v], r);
+                } else {                       // the caller's vector sits at an odd 8-byte offset
+                    direct->out[jcol[v]] = r.x;
+                    direct->out[jcol[v] + 1] = r.y;
+                }
+            }
+            return;
+        }
         // this CTA's slot among the CTAs that share the strip
         const long first = split_owner(a.total_units, G, strip * a.units_per_strip);
         double *dst = a.colpart + (cta - first) * N;
@@ -316,6 +354,18 @@ __global__ void __launch_bounds__(kThreads, MINB)
 mv_tile_kernel(const MvArgs a)
 {
     mv_tile_walk<FLAGS, R, V, ALIGNED>(a);
+}
+
+struct MvDirectArgs {
+    MvArgs mv;
+    ColEpilogue col;
+};
+
+template <int FLAGS, int R, int V, int MINB>
+__global__ void __launch_bounds__(kThreads, MINB)
+mv_tile_direct_kernel(const MvDirectArgs d)
+{
+    mv_tile_walk<FLAGS, R, V, true, true>(d.mv, &d.col);
 }
 
 // ---- finaliser: fixed-order join of the partials + the sequence's epilogue ----

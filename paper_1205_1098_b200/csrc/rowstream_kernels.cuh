@@ -6,7 +6,7 @@
 // across the full row -- so DRAM sees a handful of long sequential streams per CTA instead of
 // 4 KiB row segments.  The organism-driven emitter prints exactly this shape for GESUMMV and
 // measured 7.3 TB/s at n = 24576 against 6.9-7.07 for the strip-tiled pass, which is why it
-// exists here (scripts/emitted_rowstream_probe.py).  Row dots are reduced warp -> CTA in a fixed
+// exists here (profiles/r01/probes/emitted_rowstream_probe.py).  Row dots are reduced warp -> CTA in a fixed
 // order once per four rows; the row epilogue is applied in the kernel: ONE launch, no partials.
 #pragma once
 #include "mv_kernels.cuh"

@@ -405,6 +405,41 @@ def test_extreme_aspect_ratios(bto_lib, oracle, shape):
         _native.set_tuning(skinny=1)
 
 
+@pytest.mark.parametrize("shape", [(2, 2200000), (8, 700000), (64, 650000), (20, 1000002), (1, 620000),
+                                   (130, 610000)])
+def test_short_wide_matrices_finish_columns_in_the_producer(bto_lib, oracle, shape):
+    """Thousands of strips, a few units each: CTAs take whole strips and apply the column
+    epilogue themselves (mv_tile_direct_kernel) -- no column partials, no column join.  Same
+    results as the partial + join path up to the order of the row-unit sums (identical here:
+    a strip's column sum is accumulated by one thread in ascending row order either way)."""
+    m, n = shape
+    ext = {"M": m, "N": n}
+    try:
+        for name in ("bicgk", "gemver", "dgemvt", "atax", "batax"):
+            graph = bto.load_graph(name)
+            inputs = bto.gen_inputs(graph, ext, seed=m + n)
+            want = oracle.oracle_run(name, inputs, ext, threads=8)
+            if name in ("atax", "batax"):
+                # t = A x sums up to 10^6 cancelling terms; the oracle adds them one after the other
+                # (as the reference's C does) and is itself ~5e-11 off at N = 700000, the GPU's tree
+                # order ~1e-12: check these two against an extended-precision evaluation instead
+                A, x = inputs["A"].astype(np.longdouble), inputs["x"].astype(np.longdouble)
+                y = A.T @ (A @ x)
+                if name == "batax":
+                    y = y * np.longdouble(inputs["beta"])
+                assert bto.max_rel_error({"y": want["y"]}, {"y": y.astype(np.float64)}) < 1e-9   # same function
+                want = {"y": y.astype(np.float64)}
+            plans = {}
+            for direct in (1, 0):
+                _native.set_tuning(direct_cols=direct)
+                got = run_device(name, inputs, ext)
+                plans[direct] = _native.launch_plan()
+                assert_matches(name, got, want, ext, f"direct_cols={direct}")
+            assert "mv_tile_direct_kernel" in plans[1] and "direct" not in plans[0], plans
+    finally:
+        _native.set_tuning(direct_cols=1)
+
+
 @pytest.mark.parametrize("shape", [(600, 4096), (1001, 4098), (593, 6002), (2500, 9000), (4097, 4100)])
 def test_gesummv_row_streaming(bto_lib, oracle, shape):
     """Wide GESUMMV streams whole rows (rowstream_kernels.cuh) instead of column strips: one
@@ -697,6 +732,64 @@ def test_captured_graph_survives_workspace_growth(bto_lib, oracle):
     with torch.cuda.stream(st):
         ops.bicgk(dev["large"]["A"], dev["large"]["p"], dev["large"]["r"], *out["large"])
     assert _native.load().bto_workspace_bytes() == held
+
+
+@pytest.mark.parametrize("name", KERNELS)
+def test_no_write_lands_outside_the_outputs(bto_lib, oracle, name):
+    """compute-sanitizer is closed on this GPU pool (gpurun answers so), so out-of-bounds WRITES are
+    hunted with guard bands: every operand lives inside one arena, separated by canary words with
+    a recognisable bit pattern; after each call the canaries and the inputs must be bit-identical
+    and the outputs must match the oracle.  Ragged and unaligned shapes, every launch path
+    (strip tiles, shared-row kernels, whole-row streaming, cluster ATAX, the two-pass fallback)."""
+    graph = bto.load_graph(name)
+    kernel = bto.gpu_kernel(graph)
+    canary = float(np.frombuffer(np.uint64(0x7FF8DEADBEEF1234).tobytes(), dtype=np.float64)[0])
+    shapes = RAGGED + [(2048, 1024), (600, 4100), (37, 16390), (4100, 300), (5, 70001)]
+    for pad in (2, 3):                   # even / odd guard widths: 16-byte aligned and 8-byte-offset operands
+        for (m, n) in shapes:
+            ext = ext_of(name, m, n)
+            inputs = bto.gen_inputs(graph, ext, seed=m + 3 * n)
+            want = oracle.oracle_run(name, inputs, ext, threads=8)
+            sizes = []
+            for pname, decl in graph.spec.inputs + graph.spec.outputs:
+                if (pname, decl) in graph.spec.inputs and decl.kind == "scalar":
+                    continue
+                count = 1
+                for d in graph.dims[pname]:
+                    count *= int(ext[d])
+                sizes.append((pname, count))
+            total = pad + sum(c + pad for _, c in sizes)
+            arena = torch.full((total,), canary, dtype=torch.float64, device="cuda")
+            views, off = {}, pad
+            for pname, count in sizes:
+                views[pname] = arena[off:off + count]
+                off += count + pad
+            dev_in, outs = {}, {}
+            for pname, decl in graph.spec.inputs:
+                if decl.kind == "scalar":
+                    dev_in[pname] = inputs[pname]
+                else:
+                    views[pname].copy_(torch.from_numpy(np.ascontiguousarray(inputs[pname]).ravel()))
+                    dev_in[pname] = views[pname].view(tuple(int(ext[d]) for d in graph.dims[pname]))
+            for pname, decl in graph.spec.outputs:
+                views[pname].fill_(float("nan"))
+                outs[pname] = views[pname]
+            before = arena.clone()
+            bto.run_kernel_async(kernel, graph, dev_in, ext, outs)
+            torch.cuda.synchronize()
+            # everything except the outputs is bit-identical to before the call
+            mask = torch.ones(total, dtype=torch.bool, device="cuda")
+            off = pad
+            for pname, count in sizes:
+                if any(pname == o for o, _ in graph.spec.outputs):
+                    mask[off:off + count] = False
+                off += count + pad
+            same = arena.view(torch.int64)[mask] == before.view(torch.int64)[mask]
+            assert bool(same.all()), f"{name} {ext} pad {pad}: wrote outside its outputs"
+            got = {o: (float(outs[o][0]) if d.kind == "scalar" else
+                       outs[o].view(tuple(int(ext[x]) for x in graph.dims[o])).cpu().numpy())
+                   for o, d in graph.spec.outputs}
+            assert_matches(name, got, want, ext, f"guard bands, pad {pad}")
 
 
 def test_randomised_differential_run(bto_lib, oracle):
