@@ -51,7 +51,8 @@ struct AtaxArgs {
     int nclusters;
 };
 
-constexpr int kAtaxMaxCluster = 16;
+constexpr int kAtaxMaxCluster = 16;      // sizes built: 1, 2, 4, 8, 9, 16 (9: 15 clusters = 135 SMs on a
+                                         // B200 where 8 gives 15 x 8 = 120, profiles/r02/cluster_probe.log)
 constexpr int kAtaxMaxRows = 8;
 constexpr int kAtaxMaxStages = 8;
 constexpr int kAtaxSlots = 8;                      // exchange slots; phase 1 runs one panel ahead, needs > 3
@@ -164,14 +165,18 @@ __device__ __forceinline__ void cluster_wait()
     asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
 
-// fixed pairwise tree over n values (n a power of two): log2(n) dependent adds
+// fixed pairwise tree over n values: the largest power of two first, the rest added to it
+// (n = 9: ((v0+v1)+(v2+v3)) + ((v4+v5)+(v6+v7)), then + v8); ~log2(n) dependent adds
 template <int n>
 __device__ __forceinline__ double tree_sum(const double *v)
 {
     if constexpr (n == 1) {
         return v[0];
-    } else {
+    } else if constexpr ((n & (n - 1)) == 0) {
         return tree_sum<n / 2>(v) + tree_sum<n / 2>(v + n / 2);
+    } else {
+        constexpr int head = n >= 8 ? 8 : (n >= 4 ? 4 : 2);
+        return tree_sum<head>(v) + tree_sum<n - head>(v + head);
     }
 }
 

@@ -92,6 +92,7 @@ AtaxKernel atax_kernel_ptr(int c, int kmax, bool small)
         case 2: return atax_kernel_ptr<2>(kmax, small);
         case 4: return atax_kernel_ptr<4>(kmax, small);
         case 8: return atax_kernel_ptr<8>(kmax, small);
+        case 9: return atax_kernel_ptr<9>(kmax, small);
         case 16: return atax_kernel_ptr<16>(kmax, small);
     }
     return nullptr;
@@ -119,16 +120,35 @@ int fill_launch_config(const AtaxPlan &p, cudaLaunchConfig_t *cfg, cudaLaunchAtt
 // Picks cluster size, per-thread column count, ring depth and the number of
 // co-resident clusters.  Leaves p->fn == nullptr when the fused kernel does not
 // apply (odd N / unaligned operands / a row too long for 16 CTAs).
+int plan_atax_cluster(DeviceCtx &c, int C, long M, long N, AtaxPlan *p, long *max_clusters);
+
 int plan_atax(DeviceCtx &c, const double *A, const double *x, long M, long N, AtaxPlan *p)
 {
     p->fn = nullptr;
     if (!g_tuning.atax_fused || (N % 2) || !aligned16(A) || !aligned16(x)) return BTO_OK;
     int C = (int)g_tuning.atax_cluster;
-    if (C == 0) {
-        // smallest cluster whose per-CTA slice fits 8 double2 per thread (4096 columns)
-        C = 1;
-        while (C < 16 && (N + C - 1) / C > 4096) C *= 2;
+    long cover = 0;
+    if (C != 0) return plan_atax_cluster(c, C, M, N, p, &cover);
+    // smallest power-of-two cluster whose per-CTA slice fits 8 double2 per thread (4096 columns)
+    C = 1;
+    while (C < 16 && (N + C - 1) / C > 4096) C *= 2;
+    BTO_TRY(plan_atax_cluster(c, C, M, N, p, &cover));
+    if (C == 8 && p->fn) {
+        // Clusters live inside a GPC: on a B200 15 clusters of 8 fit (120 SMs) and 15 of 9 (135 SMs,
+        // profiles/r02/cluster_probe.log).  Same tile shape, an eighth more SMs pulling on HBM and
+        // an eighth more cycles per panel: take 9 when it covers more SMs.
+        AtaxPlan nine;
+        long cover9 = 0;
+        BTO_TRY(plan_atax_cluster(c, 9, M, N, &nine, &cover9));
+        if (nine.fn && nine.KMAX == p->KMAX && nine.RG == p->RG && cover9 * 9 > cover * 8) *p = nine;
     }
+    return BTO_OK;
+}
+
+// The plan for one cluster size; *max_clusters = co-resident clusters the device offers.
+int plan_atax_cluster(DeviceCtx &c, int C, long M, long N, AtaxPlan *p, long *max_clusters)
+{
+    p->fn = nullptr;
     long W = (N + C - 1) / C;
     W += W & 1;
     int kmax = 1;
@@ -181,6 +201,7 @@ int plan_atax(DeviceCtx &c, const double *A, const double *x, long M, long N, At
         it = c.max_clusters.emplace(reinterpret_cast<const void *>(fn), n).first;
     }
     long ncl = it->second;
+    *max_clusters = ncl;
     const long groups = (M + rg - 1) / rg;
     if (ncl > groups) ncl = groups;
     p->nclusters = (int)ncl;

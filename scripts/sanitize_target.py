@@ -23,7 +23,7 @@ for name in bto.CORPUS:
         bto.run_kernel(bto.library_path(), k, g, inp, ext)                       # host pointers
         dev = {a: (torch.from_numpy(v).cuda() if isinstance(v, np.ndarray) else v) for a, v in inp.items()}
         bto.run_kernel(bto.library_path(), k, g, dev, ext)                       # device pointers
-for c in (1, 2, 4, 8, 16):
+for c in (1, 2, 4, 8, 9, 16):
     _native.set_tuning(atax_cluster=c)
     g = bto.load_graph("atax")
     inp = bto.gen_inputs(g, {"M": 50, "N": 2050}, seed=2)

@@ -127,7 +127,7 @@ ATAX_SHAPES = [(2048, 1024), (8, 2), (1, 4096), (100, 514), (333, 8192), (64, 16
                (1000, 4098), (37, 32768), (5000, 1026)]
 
 
-@pytest.mark.parametrize("cluster", [0, 1, 2, 4, 8, 16])
+@pytest.mark.parametrize("cluster", [0, 1, 2, 4, 8, 9, 16])
 def test_fused_atax_every_cluster_size(bto_lib, oracle, cluster):
     """Single-pass ATAX/BATAX (cluster-resident row panels, TMA ring, st.async
     exchange): every cluster size, ring depth and panel height must
