@@ -551,9 +551,11 @@ static long *tuning_slot(const char *key)
     if (!strcmp(key, "atax_cluster")) return &g_tuning.atax_cluster;
     if (!strcmp(key, "atax_stages")) return &g_tuning.atax_stages;
     if (!strcmp(key, "atax_rows")) return &g_tuning.atax_rows;
+    if (!strcmp(key, "atax_per_sm")) return &g_tuning.atax_per_sm;
     if (!strcmp(key, "debug")) return &g_tuning.debug;
     if (!strcmp(key, "pdl")) return &g_tuning.pdl;
     if (!strcmp(key, "direct_cols")) return &g_tuning.direct_cols;
+    if (!strcmp(key, "midsize")) return &g_tuning.midsize;
     if (!strcmp(key, "exchange_phases")) return &g_tuning.exchange_phases;
     if (!strcmp(key, "skinny")) return &g_tuning.skinny;
     if (!strcmp(key, "rowstream")) return &g_tuning.rowstream;
@@ -576,7 +578,7 @@ int bto_set_tuning(const char *key, long value)
     if (slot == &g_tuning.mv_minb) ok = value == 0 || value == 1 || value == 2 || value == 3 || value == 4 || value == 6;
     if (slot == &g_tuning.mv_vec) ok = value == 0 || value == 1 || value == 2;
     if (slot == &g_tuning.vec_unroll) ok = value == 1 || value == 2 || value == 4;
-    if (slot == &g_tuning.direct_cols) ok = value == 0 || value == 1;
+    if (slot == &g_tuning.direct_cols || slot == &g_tuning.midsize) ok = value == 0 || value == 1;
     if (slot == &g_tuning.atax_fused || slot == &g_tuning.host_pipeline || slot == &g_tuning.host_bounce || slot == &g_tuning.host_nt || slot == &g_tuning.skinny) ok = value == 0 || value == 1;
     if (slot == &g_tuning.host_threads) ok = value >= 0 && value <= 64;
     if (slot == &g_tuning.rowstream) ok = value >= 0 && value <= 2;
@@ -586,6 +588,7 @@ int bto_set_tuning(const char *key, long value)
     if (slot == &g_tuning.atax_cluster) ok = value == 0 || value == 1 || value == 2 || value == 4 || value == 8 || value == 9 || value == 16;
     if (slot == &g_tuning.atax_stages) ok = value == 0 || (value >= 2 && value <= 8);
     if (slot == &g_tuning.atax_rows) ok = value == 0 || value == 1;
+    if (slot == &g_tuning.atax_per_sm) ok = value == 1 || value == 2;
     if (slot == &g_tuning.grid_per_sm || slot == &g_tuning.vec_grid_per_sm) ok = value >= 0 && value <= 64;
     if (!ok) return fail(BTO_ERR_INVALID, "tuning %s=%ld is not supported", key, value);
     *slot = value;

@@ -183,8 +183,21 @@ __device__ __forceinline__ double tree_sum(const double *v)
 // C    cluster size (1 = plain CTA, a whole row fits one CTA's slice)
 // KMAX double2 column pairs per thread: the CTA slice is at most 512*KMAX columns
 // TR   rows per panel; a panel is TR*KMAX double2 (<= 16) per thread in registers
-template <int C, int KMAX, int TR>
-__global__ void __launch_bounds__(kAtaxThreads, 1)
+// MINB CTAs per SM.  1: two register tiles, phase 2 runs one panel behind phase 1 (the exchange
+//      latency hides behind the next panel).  2: ONE tile and no software pipeline -- phase 2
+//      follows phase 1 of the same panel and the exchange latency is exposed, but the other CTA
+//      on the SM (a different cluster) works meanwhile: two independent latency chains per SM
+//      instead of one, at half the registers each.  The per-panel chain (smem reads, reduction,
+//      barrier, DSMEM round trip) is what bounds this kernel whenever the SM clock drops under the
+//      power cap (7.05 TB/s at 1965 MHz, 6.05 at ~1650, profiles/r02/atax_sustained.md).
+// What bounds the kernel (profiles/r02/atax_sustained.md, SM ~1650 MHz under the power cap): the TMA
+// stream + CTA barrier alone run at 7.25 TB/s, all the arithmetic without the cluster exchange at
+// 7.0, the whole kernel at 6.05-6.15 -- the per-panel chain (shared-memory read, dot, butterfly,
+// barrier, st.async round trip, rank-ordered sum) is ~1150 cycles + ~500 per row whatever the panel
+// height, so it follows the SM clock.  Four one-row register tiles (three panels of slack) were
+// measured at 3.9 TB/s: twice the panels, the same chain per panel.
+template <int C, int KMAX, int TR, int MINB = 1>
+__global__ void __launch_bounds__(kAtaxThreads, MINB)
 atax_cluster_kernel(const AtaxArgs a)
 {
     static_assert(TR * KMAX <= 16 && TR <= kAtaxMaxRows, "register tile too large");
@@ -284,15 +297,11 @@ atax_cluster_kernel(const AtaxArgs a)
                 }
                 d[r] = (acc0 + acc1) + (acc2 + acc3);
             }
-#pragma unroll
-            for (int off = 16; off >= 1; off >>= 1) {     // TR independent shuffle chains
-#pragma unroll
-                for (int r = 0; r < TR; ++r) d[r] += __shfl_xor_sync(kFullMask, d[r], off);
-            }
-            if (lane == 0) {
-#pragma unroll
-                for (int r = 0; r < TR; ++r) warp_part[par][r][warp] = d[r];
-            }
+            // halving butterfly: a lane hands the rows it does not keep to its partner, so TR rows
+            // cost TR - 1 + (5 - log2 TR) shuffled doubles instead of 5 TR (2 rows: 5, not 10);
+            // afterwards lane l holds the warp's sum of row l / (32 / TR) in d[0]
+            warp_transpose_sum<TR>(d, lane);
+            if ((lane % (32 / TR)) == 0) warp_part[par][lane / (32 / TR)][warp] = d[0];
             __syncthreads();
             // every warp holds its part of the tile in registers (the FMAs above
             // consumed the loads): the stage is free, refill it S panels ahead
@@ -328,15 +337,23 @@ atax_cluster_kernel(const AtaxArgs a)
             }
         };
 
-        // two register tiles, loop unrolled by two so neither is ever copied
-        double2 tile_a[TR][KMAX], tile_b[TR][KMAX];
-        if (ngroups > 0) phase1(0, tile_a);
-        for (int g = 0; g < ngroups; g += 2) {
-            if (g + 1 < ngroups) phase1(g + 1, tile_b);
-            phase2(g, tile_a);
-            if (g + 1 >= ngroups) break;
-            if (g + 2 < ngroups) phase1(g + 2, tile_a);
-            phase2(g + 1, tile_b);
+        if constexpr (MINB == 1) {
+            // two register tiles, loop unrolled by two so neither is ever copied
+            double2 tile_a[TR][KMAX], tile_b[TR][KMAX];
+            if (ngroups > 0) phase1(0, tile_a);
+            for (int g = 0; g < ngroups; g += 2) {
+                if (g + 1 < ngroups) phase1(g + 1, tile_b);
+                phase2(g, tile_a);
+                if (g + 1 >= ngroups) break;
+                if (g + 2 < ngroups) phase1(g + 2, tile_a);
+                phase2(g + 1, tile_b);
+            }
+        } else {
+            double2 tile[TR][KMAX];
+            for (int g = 0; g < ngroups; ++g) {
+                phase1(g, tile);
+                phase2(g, tile);
+            }
         }
 
         double *dst = a.ypart + cluster * N + c0;

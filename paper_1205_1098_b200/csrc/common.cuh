@@ -157,7 +157,7 @@ __device__ __forceinline__ double block_sum(double v, double *scratch)
 template <int R>
 __device__ __forceinline__ void warp_transpose_sum(double (&v)[R], int lane)
 {
-    static_assert(R == 8 || R == 16 || R == 32, "R must be 8, 16 or 32");
+    static_assert(R == 1 || R == 2 || R == 4 || R == 8 || R == 16 || R == 32, "R must be a power of two <= 32");
 #pragma unroll
     for (int s = 0; s < 5; ++s) {
         const int off = 16 >> s;

@@ -95,6 +95,9 @@ struct Tuning {
     long atax_cluster = 0;   // cluster size of the fused ATAX (0 = auto | 1 | 2 | 4 | 8 | 16)
     long atax_stages = 0;    // TMA ring depth (0 = as many as fit, at most 8)
     long atax_rows = 0;      // 0: 16 double2 per thread per panel, 1: half-height panels
+    long atax_per_sm = 1;    // 1: one CTA per SM, two register tiles (software pipeline); 2: two CTAs per SM, one tile
+    long midsize = 1;        // size-aware launch shapes (narrower strips, lower tiles, fewer CTAs, wave-exact
+                             // row blocks) below the bench sizes; 0: the bench-size shapes everywhere
     long direct_cols = 1;    // short-wide matrices: whole strips per CTA, column epilogue in the producer
     long pdl = 1;            // joins launched as programmatic dependents of their producer
     long debug = 0;          // print launch plans to stderr

@@ -166,6 +166,17 @@ int plan_mv(DeviceCtx &c, long M, long N, bool aligned, MvPlan *p)
     if (!g_tuning.mv_rows && aligned) {
         while (R > 8 && M <= R / 2) R /= 2;
     }
+    // Mid-size matrices (profiles/r02/midsize_tune_before.log): the bench-size shapes leave too few
+    // units to spread -- 1024-column strips need N > 2048 (BiCGK n = 2048: 9.4 -> 8.7 us with 512; n = 3072 is
+    // better off with three 1024-column strips),
+    // tall tiles need about eight units per resident CTA (GEMVER n = 2048: 20.0 -> 17.9 us with 8 rows)
+    if (g_tuning.midsize && aligned) {
+        if (!g_tuning.mv_vec && V == 2 && N <= 2048) V = 1;
+        if (!g_tuning.mv_rows) {
+            const long strips = (N + (long)kThreads * 2 * V - 1) / ((long)kThreads * 2 * V);
+            while (R > 8 && strips * ((M + R - 1) / R) < 16L * c.sm_count) R /= 2;
+        }
+    }
     p->R = R;
     p->V = V;
     p->aligned = aligned;
@@ -180,6 +191,14 @@ int plan_mv(DeviceCtx &c, long M, long N, bool aligned, MvPlan *p)
     BTO_TRY(occupancy_of(c, p->fn, &occ));
     long per_sm = g_tuning.grid_per_sm > 0 ? g_tuning.grid_per_sm : dflt.grid_per_sm;
     if (per_sm <= 0) per_sm = occ;
+    // More CTAs than are resident only pay (tail balance) while each still walks a few dozen units:
+    // every CTA adds a column partial per strip to the join (BiCGK n = 8192: 89.5 -> 81.4 us with
+    // the resident 2 per SM instead of 8; at n >= 16384 the sweep of round 1 stands)
+    if (g_tuning.midsize && !g_tuning.grid_per_sm && (FLAGS & kFlagT)) {
+        const long resident = occ < per_sm ? occ : per_sm;
+        while (per_sm > resident && p->total_units < 24L * c.sm_count * per_sm) per_sm /= 2;
+        if (per_sm < resident) per_sm = resident;
+    }
     long grid = (long)c.sm_count * per_sm;
     // small matrices: about 3 units or more per CTA (the prologue and the partial a CTA
     // writes per strip are fixed costs), in whole multiples of the SM count so that every
@@ -417,12 +436,30 @@ struct Pass {
             if (rowstream) {
                 RowStreamArgs r{};
                 r.A = a.A; r.A2 = a.A2; r.colw = a.colw; r.fin = f; r.M = M; r.N = N;
-                const long per_sm = g_tuning.grid_per_sm > 0 ? g_tuning.grid_per_sm : 4;
-                const long target = (long)c.sm_count * per_sm;
-                long rows = (M + target - 1) / target;
-                rows = ((rows + kRsRows - 1) / kRsRows) * kRsRows;
+                // One 512-thread CTA per SM is resident and every CTA does the same work, so the
+                // grid runs in waves of sm_count.  4 CTAs per SM unless fewer fill the last wave much
+                // better (M = 8192: 512 CTAs = 3.5 waves of 16 rows, 86 % full -> 293 CTAs of 28 rows,
+                // 99 %: 157 -> 150 us).  A small gain in fullness does not pay: M = 24576 measured
+                // 7.40 TB/s with 559 CTAs (94 %) and 7.25 with 439 (99 %) -- more CTAs in flight
+                // keep more rows streaming.
+                long rows = 0, grid = 0;
+                double best = -1.0;
+                for (long per_sm = 4; per_sm >= 2; --per_sm) {
+                    if (g_tuning.grid_per_sm > 0 && per_sm != 4) break;
+                    const long target = (long)c.sm_count * (g_tuning.grid_per_sm > 0 ? g_tuning.grid_per_sm : per_sm);
+                    long rr = (M + target - 1) / target;
+                    rr = ((rr + kRsRows - 1) / kRsRows) * kRsRows;
+                    const long gg = (M + rr - 1) / rr;
+                    const long waves = (gg + c.sm_count - 1) / c.sm_count;
+                    const double eff = (double)M / ((double)waves * (double)rr * (double)c.sm_count);
+                    if (eff > best + 0.08 || !g_tuning.midsize) {
+                        best = eff;
+                        rows = rr;
+                        grid = gg;
+                    }
+                    if (!g_tuning.midsize) break;
+                }
                 r.rows_per_cta = rows;
-                const long grid = (M + rows - 1) / rows;
                 cudaLaunchConfig_t cfg;
                 memset(&cfg, 0, sizeof(cfg));
                 cfg.gridDim = dim3((unsigned)grid, 1, 1);

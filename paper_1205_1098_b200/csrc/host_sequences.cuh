@@ -58,7 +58,7 @@ using AtaxKernel = void (*)(const AtaxArgs);
 
 struct AtaxPlan {
     AtaxKernel fn = nullptr;     // nullptr: not applicable, use the two-pass sequence
-    int C = 1, KMAX = 1, RG = 1, W = 0, S = 0;
+    int C = 1, KMAX = 1, RG = 1, W = 0, S = 0, minb = 1;
     size_t smem = 0;
     int nclusters = 0;
 };
@@ -85,8 +85,33 @@ int atax_rows_of(int kmax, bool small)
     return kmax == 1 ? 4 : full / 2;
 }
 
-AtaxKernel atax_kernel_ptr(int c, int kmax, bool small)
+// two CTAs per SM, one register tile of 8 double2 per thread (atax_cluster.cuh, MINB = 2)
+template <int C>
+AtaxKernel atax_kernel_ptr_two(int kmax)
 {
+    switch (kmax) {
+        case 1: return atax_cluster_kernel<C, 1, 8, 2>;
+        case 2: return atax_cluster_kernel<C, 2, 4, 2>;
+        case 4: return atax_cluster_kernel<C, 4, 2, 2>;
+        case 8: return atax_cluster_kernel<C, 8, 1, 2>;
+    }
+    return nullptr;
+}
+
+int atax_rows_of_two(int kmax) { return kmax >= 8 ? 1 : 8 / kmax; }
+
+AtaxKernel atax_kernel_ptr(int c, int kmax, bool small, bool two)
+{
+    if (two) {
+        switch (c) {
+            case 1: return atax_kernel_ptr_two<1>(kmax);
+            case 2: return atax_kernel_ptr_two<2>(kmax);
+            case 4: return atax_kernel_ptr_two<4>(kmax);
+            case 8: return atax_kernel_ptr_two<8>(kmax);
+            case 9: return atax_kernel_ptr_two<9>(kmax);
+        }
+        return nullptr;
+    }
     switch (c) {
         case 1: return atax_kernel_ptr<1>(kmax, small);
         case 2: return atax_kernel_ptr<2>(kmax, small);
@@ -151,14 +176,18 @@ int plan_atax_cluster(DeviceCtx &c, int C, long M, long N, AtaxPlan *p, long *ma
     p->fn = nullptr;
     long W = (N + C - 1) / C;
     W += W & 1;
+    // a slice that starts off a 128-byte line costs the TMA stream ~7 % (C = 9 at N = 32768:
+    // 3642 columns -> 6.76 TB/s for the copies alone, 3648 -> as good as C = 8)
+    if (((W + 15) / 16) * 16 * (long)(C - 1) < N) W = ((W + 15) / 16) * 16;
     int kmax = 1;
     while ((long)kmax * 2 * kThreads < W) kmax *= 2;
     if (kmax > 16) return BTO_OK;
     if ((long)(C - 1) * W >= N && C > 1) return BTO_OK;   // a CTA would own no column
     const bool small = g_tuning.atax_rows == 1;     // 1: half-height panels
-    AtaxKernel fn = atax_kernel_ptr(C, kmax, small);
+    const bool two = g_tuning.atax_per_sm == 2;     // two CTAs per SM, one register tile each
+    AtaxKernel fn = atax_kernel_ptr(C, kmax, small, two);
     if (!fn) return BTO_OK;
-    const int rg = atax_rows_of(kmax, small);
+    const int rg = two ? atax_rows_of_two(kmax) : atax_rows_of(kmax, small);
     const size_t stage = (size_t)rg * W * sizeof(double);
     auto sm = c.static_smem.find(reinterpret_cast<const void *>(fn));
     if (sm == c.static_smem.end()) {
@@ -166,8 +195,9 @@ int plan_atax_cluster(DeviceCtx &c, int C, long M, long N, AtaxPlan *p, long *ma
         CUDA_TRY(cudaFuncGetAttributes(&fattr, fn));
         sm = c.static_smem.emplace(reinterpret_cast<const void *>(fn), fattr.sharedSizeBytes).first;
     }
-    // 227 KiB per CTA on sm_100, minus the kernel's static shared memory
-    const size_t budget = ((227 * 1024 - sm->second) / 1024) * 1024;
+    // 227 KiB per CTA on sm_100 (113 KiB each for two per SM: 228 KiB per SM, 1 KiB reserved per
+    // CTA), minus the kernel's static shared memory
+    const size_t budget = (((two ? 113 : 227) * 1024 - sm->second) / 1024) * 1024;
     int S = (int)(budget / stage);
     if (S > 8) S = 8;
     if (g_tuning.atax_stages > 0 && g_tuning.atax_stages < S) S = (int)g_tuning.atax_stages;
@@ -177,6 +207,7 @@ int plan_atax_cluster(DeviceCtx &c, int C, long M, long N, AtaxPlan *p, long *ma
     p->RG = rg;
     p->W = (int)W;
     p->S = S;
+    p->minb = two ? 2 : 1;
     p->smem = stage * S;
     auto it = c.max_clusters.find(reinterpret_cast<const void *>(fn));
     if (it == c.max_clusters.end()) {
@@ -228,7 +259,7 @@ int seq_atax_fused(DeviceCtx &c, const AtaxPlan &p, const double *A, const doubl
     fill_launch_config(p, &cfg, attr, st);
     CUDA_TRY(cudaLaunchKernelEx(&cfg, p.fn, a));
     char what[64];
-    snprintf(what, sizeof(what), "atax_cluster_kernel<%d,%d,%d>", p.C, p.KMAX, p.RG);
+    snprintf(what, sizeof(what), "atax_cluster_kernel<%d,%d,%d,%d>", p.C, p.KMAX, p.RG, p.minb);
     BTO_TRY(check_launch(what, reinterpret_cast<const void *>(p.fn)));
     // join the per-cluster partials in ascending cluster order
     FinArgs f{};

@@ -140,13 +140,15 @@ def test_fused_atax_every_cluster_size(bto_lib, oracle, cluster):
                 graph = bto.load_graph(name)
                 inputs = bto.gen_inputs(graph, ext, seed=m + n)
                 want = oracle.oracle_run(name, inputs, ext, threads=8)
-                for stages, rows in ((0, 0), (2, 0), (0, 1), (4, 1)):
+                for stages, rows, per_sm in ((0, 0, 1), (2, 0, 1), (0, 1, 1), (4, 1, 1), (0, 0, 2), (2, 0, 2)):
+                    if per_sm == 2 and cluster == 16:
+                        continue                  # two CTAs per SM: clusters up to 9
                     _native.set_tuning(atax_fused=1, atax_cluster=cluster, atax_stages=stages,
-                                       atax_rows=rows)
+                                       atax_rows=rows, atax_per_sm=per_sm)
                     assert_matches(name, run_device(name, inputs, ext), want, ext,
-                                   f"C{cluster} S{stages} R{rows}")
+                                   f"C{cluster} S{stages} R{rows} per_sm{per_sm}")
     finally:
-        _native.set_tuning(atax_fused=1, atax_cluster=0, atax_stages=0, atax_rows=0)
+        _native.set_tuning(atax_fused=1, atax_cluster=0, atax_stages=0, atax_rows=0, atax_per_sm=1)
 
 
 def test_two_pass_atax_fallback(bto_lib, oracle):
