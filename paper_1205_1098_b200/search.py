@@ -317,3 +317,71 @@ class Autotuner:
                 _native.set_tuning(**saved)
 
         return scope()
+
+
+# ---------------------------------------------------------------------------
+# command line: the `--fitness` entry of the reference's `matfuse search` (cli.py:205-246)
+# for the GPU cost model and the GPU timer.  Same exit codes (cli.py:42-44), same output files.
+
+EXIT_USAGE, EXIT_KERNEL, EXIT_TOOLCHAIN = 1, 2, 3
+
+
+def main(argv=None) -> int:
+    """python -m paper_1205_1098_b200 search KERNEL [--strategy ga] [--fitness analytic|gpu]
+    [--extents M=4096,N=4096] [--out-dir DIR] [--budget K] [--seed S] [--reps R]
+
+    KERNEL is a corpus kernel name or the path of a `.bto` file with a corpus structure.
+    `--fitness analytic` prices launch variants with the HBM-bytes / occupancy model (no GPU
+    needed), `--fitness gpu` validates and times them on the current CUDA device."""
+    import argparse
+    import sys
+
+    from .cost import AnalyticGpuCost, GpuEmpiricalTimer, GpuMachineModel
+    from .runtime import load_graph
+    from .spec import infer_shapes, parse_kernel
+
+    ap = argparse.ArgumentParser(prog="python -m paper_1205_1098_b200 search", description=main.__doc__)
+    ap.add_argument("kernel")
+    ap.add_argument("--strategy", choices=STRATEGIES, default="ga")
+    ap.add_argument("--fitness", choices=("analytic", "gpu"), default="analytic")
+    ap.add_argument("--extents", default="M=4096,N=4096")
+    ap.add_argument("--out-dir", default="search-out")
+    ap.add_argument("--budget", type=int, default=None)
+    ap.add_argument("--time-budget", type=float, default=None)
+    ap.add_argument("--population", type=int, default=8)
+    ap.add_argument("--generations", type=int, default=10)
+    ap.add_argument("--seed", type=int, default=0)
+    ap.add_argument("--reps", type=int, default=5)
+    try:
+        args = ap.parse_args(argv)
+    except SystemExit as exc:
+        return EXIT_USAGE if exc.code else 0
+    try:
+        extents = {k: int(v) for k, v in (kv.split("=") for kv in args.extents.split(","))}
+        path = Path(args.kernel)
+        graph = infer_shapes(parse_kernel(path.read_text())) if path.suffix == ".bto" and path.exists() \
+            else load_graph(args.kernel)
+        match_corpus(graph.spec)
+        cfg = SearchConfig(population=args.population, generations=args.generations, budget=args.budget,
+                           time_budget_s=args.time_budget, seed=args.seed)
+    except (ValueError, KeyError, OSError, NotImplementedError) as exc:
+        print(f"error: {exc}", file=sys.stderr)
+        return EXIT_USAGE
+    if args.fitness == "gpu":
+        try:
+            import torch
+            from . import _native
+            _native.load()
+            if not torch.cuda.is_available():
+                raise RuntimeError("no CUDA device")
+        except Exception as exc:
+            print(f"error: the gpu fitness needs libbto_b200.so and a B200 ({exc})", file=sys.stderr)
+            return EXIT_TOOLCHAIN
+        fitness = cached(GpuEmpiricalTimer(graph, extents, reps=args.reps))
+    else:
+        fitness = cached(AnalyticGpuCost(graph, GpuMachineModel(extents=tuple(sorted(extents.items())))))
+    result = run_strategy(args.strategy, graph, cfg, fitness)
+    summary = write_run(args.out_dir, graph, result, cfg, args.fitness)
+    print(json.dumps(summary, indent=2))
+    return EXIT_KERNEL if result.best_report.failed else 0
+

@@ -134,3 +134,21 @@ def test_autotuner_with_the_empirical_timer(tmp_path):
         inputs = bto.gen_inputs(g, {"M": 64, "N": 64}, seed=1)
         out = bto.run_kernel(bto.library_path(), bto.gpu_kernel(g), g, inputs, {"M": 64, "N": 64})
     assert out["y"].shape == (64,)
+
+
+def test_command_line_search_with_the_analytic_fitness(tmp_path, capsys):
+    """`python -m paper_1205_1098_b200 search` -- the `--fitness` entry of the reference's CLI
+    (cli.py:205-246): same files, same exit codes."""
+    from paper_1205_1098_b200.__main__ import main
+    rc = main(["search", "gemver", "--strategy", "random", "--fitness", "analytic", "--extents",
+               "M=8192,N=8192", "--budget", "6", "--out-dir", str(tmp_path)])
+    assert rc == 0
+    summary = json.loads((tmp_path / "summary.json").read_text())
+    assert summary["kernel"] == "GEMVER" and summary["fitness_source"] == "analytic"
+    assert 1 <= summary["evaluations"] <= 6
+    assert len((tmp_path / "log.jsonl").read_text().splitlines()) == summary["evaluations"]
+    assert main(["search", "no-such-kernel"]) == S.EXIT_USAGE
+    assert main(["enumerate"]) == S.EXIT_USAGE
+    import torch
+    if not torch.cuda.is_available():
+        assert main(["search", "bicgk", "--fitness", "gpu", "--out-dir", str(tmp_path)]) == S.EXIT_TOOLCHAIN
