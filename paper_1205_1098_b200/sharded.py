@@ -257,21 +257,34 @@ class GpuShardOps:
         self.lib = _native.load()
         self._stream = stream
         self._recording = None
+        self._raw_stream = None
 
     def _st(self):
+        # the raw handle of the current stream without building a torch.cuda.Stream object
+        # (1.5 us -> 0.2 us; an eager mid-size call is bound by exactly this kind of cost)
+        if self._stream is not None:
+            return self._stream.cuda_stream
+        return self._raw_stream(self._device_index())
+
+    def _device_index(self):
         import torch
-        stream = self._stream or torch.cuda.current_stream()
-        return ctypes.c_void_p(stream.cuda_stream)
+        if self._raw_stream is None:
+            self._raw_stream = torch._C._cuda_getCurrentRawStream
+        return torch.cuda.current_device()
 
     @staticmethod
     def _p(t):
-        return ctypes.c_void_p(t.data_ptr())
+        # a plain int: ctypes converts it through the declared argtype (c_void_p), which is
+        # cheaper than constructing a c_void_p object per argument
+        return t.data_ptr()
 
     def _call(self, fn, *args):
         if self._recording is not None:          # bind(): keep the marshalled call instead of making it
             self._recording.append((fn, args))
             return
-        self._native.check(fn(*args))
+        rc = fn(*args)
+        if rc:
+            self._native.check(rc)
 
     def bind(self, method: str, *args):
         """Pre-marshal one call: `f = ops.bind("bicgk", A, p, r, q, s)`, then `f()` launches it

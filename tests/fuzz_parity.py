@@ -19,19 +19,24 @@ def extent():
     r = rng.random()
     if r < 0.25: return rng.choice([1, 2, 3, 7, 8, 9, 15, 16, 17, 31, 32, 33, 63, 64, 65])
     if r < 0.5: return max(1, rng.choice([256, 512, 1024, 1536, 2048]) + rng.randint(-3, 3))
-    if r < 0.9: return rng.randint(1, 3000)
-    return rng.randint(3000, 20000)
+    if r < 0.85: return rng.randint(1, 3000)
+    if r < 0.95: return rng.randint(3000, 20000)
+    return rng.choice([303106, 606210, 700000, 1200002])      # thousands of strips: the column-direct path
 t_end = time.time() + budget
 cases = fails = 0
 while time.time() < t_end:
     name = rng.choice(sorted(bto.CORPUS))
     g = bto.load_graph(name)
     m, n = extent(), extent()
-    if m * n > 3e7: n = max(1, int(3e7 // m))
+    if m * n > 3e7:
+        if n > 300000: m = max(1, int(3e7 // n))             # keep the very wide shapes wide
+        else: n = max(1, int(3e7 // m))
     ext = {"M": m * n} if g.extent_names == ("M",) else {"M": m, "N": n}
     tune = dict(mv_rows=rng.choice([0, 0, 8, 16, 32]), mv_vec=rng.choice([0, 0, 1, 2]),
                 grid_per_sm=rng.choice([0, 0, 1, 2, 4, 8]), mv_minb=rng.choice([0, 0, 1, 2, 4]),
-                skinny=rng.choice([1, 1, 0]), vec_unroll=rng.choice([1, 2, 4]), atax_fused=rng.choice([1, 1, 0]))
+                skinny=rng.choice([1, 1, 0]), vec_unroll=rng.choice([1, 2, 4]), atax_fused=rng.choice([1, 1, 0]),
+                direct_cols=rng.choice([1, 1, 0]), midsize=rng.choice([1, 1, 0]), atax_per_sm=rng.choice([1, 1, 2]),
+                atax_cluster=rng.choice([0, 0, 0, 1, 2, 4, 8, 9]), rowstream=rng.choice([1, 1, 0, 2]))
     _native.set_tuning(**tune)
     inputs = bto.random_inputs(g, ext, seed=cases)
     want = oracle.oracle_run(name, inputs, ext, threads=rng.choice([1, 4, 8]))
@@ -62,6 +67,7 @@ while time.time() < t_end:
         fails += 1
         print("MISMATCH", name, ext, tune, "host" if host else "device", "colmajor" if colmajor else "",
               f"err={err:.3e}", flush=True)
-_native.set_tuning(mv_rows=0, mv_vec=0, grid_per_sm=0, mv_minb=0, skinny=1, vec_unroll=2, atax_fused=1)
+_native.set_tuning(mv_rows=0, mv_vec=0, grid_per_sm=0, mv_minb=0, skinny=1, vec_unroll=2, atax_fused=1,
+                   direct_cols=1, midsize=1, atax_per_sm=1, atax_cluster=0, rowstream=1)
 print(f"{cases} cases, {fails} mismatches")
 sys.exit(1 if fails else 0)
