@@ -264,13 +264,11 @@ class GpuShardOps:
         # (1.5 us -> 0.2 us; an eager mid-size call is bound by exactly this kind of cost)
         if self._stream is not None:
             return self._stream.cuda_stream
-        return self._raw_stream(self._device_index())
-
-    def _device_index(self):
-        import torch
         if self._raw_stream is None:
+            import torch
             self._raw_stream = torch._C._cuda_getCurrentRawStream
-        return torch.cuda.current_device()
+            self._current_device = torch.cuda.current_device
+        return self._raw_stream(self._current_device())
 
     @staticmethod
     def _p(t):

@@ -11,6 +11,7 @@ sys.path.insert(0, str(REPO)); sys.path.insert(0, str(REPO / "tests"))   # test 
 import paper_1205_1098_b200 as bto
 from paper_1205_1098_b200 import _native
 import oracle_lib
+import np_interp
 budget = float(sys.argv[1]) if len(sys.argv) > 1 else 60.0
 rng = random.Random(int(sys.argv[2]) if len(sys.argv) > 2 else 0)
 oracle = oracle_lib.load_oracle() if hasattr(oracle_lib, "load_oracle") else oracle_lib
@@ -57,6 +58,14 @@ while time.time() < t_end:
                 dev[k] = shifted
         got = bto.run_kernel(bto.library_path(), bto.gpu_kernel(g), g, dev, ext)
         got = {k: (v.cpu().numpy() if hasattr(v, "cpu") else v) for k, v in got.items()}
+    if max(ext.values()) >= 100000 and g.extent_names != ("M",):
+        # sums of 10^5..10^6 cancelling terms: the oracle adds them one after the other (like the
+        # reference's C) and is itself several 1e-11 off; judge the GPU against an extended-precision
+        # evaluation, and the oracle too (loosely: it must still be the same function)
+        exact = np_interp.evaluate(bto.load_graph(name).spec, inputs, dtype=np.longdouble)
+        assert bto.max_rel_error(want, exact) < 1e-9, (name, ext)
+        reductions = {k: v for k, v in exact.items() if k not in ELEMENTWISE.get(name, ())}
+        want = dict(want, **reductions)
     err = bto.max_rel_error(got, want)
     tol = 1e-12 * max(1.0, math.log2(max(ext.values())))
     bad = not (err <= tol) or any(np.any(np.isnan(np.asarray(got[o]))) for o in want)
