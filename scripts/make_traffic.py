@@ -56,7 +56,9 @@ def main(rep: str, out: str, note: str) -> None:
         entry["all_kernels"].append(label)
         if seq is not None:
             entry["kernels"].append(label)
-    last = steps[-1]
+    # the capture window may end inside a step: take the last step that holds all five sequences
+    whole = [s for s in steps if len(s) == len({seq for _, seq in MAIN})]
+    last = whole[-1] if whole else steps[-1]
     last["_source"] = note
     json.dump(last, open(out, "w"), indent=1)
     for k, v in last.items():
