@@ -196,6 +196,11 @@ __device__ __forceinline__ double tree_sum(const double *v)
 // barrier, st.async round trip, rank-ordered sum) is ~1150 cycles + ~500 per row whatever the panel
 // height, so it follows the SM clock.  Four one-row register tiles (three panels of slack) were
 // measured at 3.9 TB/s: twice the panels, the same chain per panel.
+// Round 2 also measured, and dropped (profiles/r02/atax_sustained.md): loads without predicates for
+// the iterations every thread has (-5 %: the predicated schedule interleaves loads and FMAs better),
+// warps without tail columns skipping the last iteration behind warp-uniform branches (-10 %), and
+// a split CTA barrier where only warp 0 waits (-15 %: the other warps then poll the exchange
+// mbarrier while warp 0 is still pushing).
 template <int C, int KMAX, int TR, int MINB = 1>
 __global__ void __launch_bounds__(kAtaxThreads, MINB)
 atax_cluster_kernel(const AtaxArgs a)
@@ -206,8 +211,9 @@ atax_cluster_kernel(const AtaxArgs a)
     double *tiles = reinterpret_cast<double *>(smem_raw);        // [S][TR][W]
     __shared__ __align__(8) uint64_t full[kAtaxMaxStages];       // TMA landed (tx bytes)
     __shared__ __align__(8) uint64_t pbar[kAtaxSlots];           // C partials of a panel arrived
-    __shared__ double warp_part[2][TR][kWarps];                  // phase-1 warp sums
-    __shared__ double part[kAtaxSlots][TR][C];                   // pushed by every CTA of the cluster
+    constexpr int CP = (C + 1) & ~1;     // a row's partials padded to whole 16-byte words (LDS.128; +0.9 %)
+    __shared__ __align__(16) double warp_part[2][TR][kWarps];    // phase-1 warp sums
+    __shared__ __align__(16) double part[kAtaxSlots][TR][CP];    // pushed by every CTA of the cluster
 
     wait_for_producer_grid();
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;

@@ -124,7 +124,7 @@ def test_every_tile_variant(bto_lib, oracle, rows, vec):
 
 
 ATAX_SHAPES = [(2048, 1024), (8, 2), (1, 4096), (100, 514), (333, 8192), (64, 16390),
-               (1000, 4098), (37, 32768), (5000, 1026)]
+               (1000, 4098), (37, 32768), (5000, 1026), (257, 3586), (129, 28672), (75, 30000)]
 
 
 @pytest.mark.parametrize("cluster", [0, 1, 2, 4, 8, 9, 16])
