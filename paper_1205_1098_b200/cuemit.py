@@ -179,6 +179,50 @@ __device__ __forceinline__ void cta_allreduce_n(double (&v)[R], double *scratch)
         v[r] = total;
     }
 }
+
+// Cluster mode (a region whose CTAs split the strided axis between the C CTAs of a cluster): a sum
+// that leaves the axis is completed across the cluster.  Warp sums go to shared memory as in
+// cta_allreduce_n; thread c < C then adds them (the CTA's total, warps in ascending order) and PUSHES
+// it into CTA c's exchange buffer through distributed shared memory; ONE cluster barrier; every
+// thread adds the C totals it finds in its own shared memory in rank order -- the same bits in
+// every CTA.  Two buffers alternate (`par`): a peer overwrites a buffer only after the barrier of
+// the exchange in between, which this CTA reaches after it has read it.
+template <int R, int C>
+__device__ __forceinline__ void cluster_allreduce_n(double (&v)[R], double *scratch, double *gather, int &par)
+{
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = (blockDim.x + 31) >> 5;
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+#pragma unroll
+        for (int off = 16; off >= 1; off >>= 1) v[r] += __shfl_xor_sync(0xffffffffu, v[r], off);
+    }
+    if (lane == 0) {
+#pragma unroll
+        for (int r = 0; r < R; ++r) scratch[warp * R + r] = v[r];
+    }
+    __syncthreads();
+    if (threadIdx.x < C) {
+        unsigned rank, dst;
+        asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(rank));
+        asm volatile("mapa.shared::cluster.u32 %0, %1, %2;"
+                     : "=r"(dst) : "r"((unsigned)__cvta_generic_to_shared(gather + rank * R)), "r"(threadIdx.x));
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+            double total = scratch[r];
+            for (int w = 1; w < nwarps; ++w) total += scratch[w * R + r];
+            asm volatile("st.shared::cluster.f64 [%0], %1;" ::"r"(dst + 8u * r), "d"(total) : "memory");
+        }
+    }
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+        double total = gather[r];
+#pragma unroll
+        for (int c = 1; c < C; ++c) total += gather[c * R + r];
+        v[r] = total;
+    }
+    par ^= 1;
+}
 }  // namespace
 """
 
@@ -194,7 +238,8 @@ JOIN_COLS = 32                # columns per CTA of a join kernel
 class _Emitter:
     def __init__(self, ir: dict, blocks: int, optimize: bool = True, jam: int = JAM,
                  unroll: int = 4, threads: int = CTA_THREADS, minb: int = 2, bypass_l1: int = 1,
-                 sync: int = 0, auto: int = 1):
+                 sync: int = 0, auto: int = 1, cluster: int = 8, cluster_min_bytes: int | None = None,
+                 cluster_jam: int = 0, cluster_minb: int = 0, cluster_threads: int = 0):
         self.jam, self.unroll, self.threads, self.minb = int(jam), int(unroll), int(threads), int(minb)
         self.bypass_l1 = bool(bypass_l1)
         self.sync = bool(sync)
@@ -223,6 +268,12 @@ class _Emitter:
         self.strip_axis = None         # set while a region is emitted with a 2-D (block x column strip) grid
         self.row_accs: dict = {}       # row accumulator -> its per-strip partial buffer (strip mode)
         self.tile_axis = None          # set while a region's own slices are dealt out tile by tile
+        self.cluster = 0               # cluster size while a region is emitted in cluster mode (else 0)
+        self.cluster_size = int(cluster)
+        self.cluster_min_bytes = self.CLUSTER_MIN_BYTES if cluster_min_bytes is None else int(cluster_min_bytes)
+        self.cluster_jam = int(cluster_jam)      # rows per batch in cluster mode (0: CLUSTER_SHAPE's)
+        self.cluster_minb = int(cluster_minb)    # CTAs per SM the registers are sized for (0: CLUSTER_SHAPE's)
+        self.cluster_threads = int(cluster_threads)
 
     # -- names and references (cemit.py:54-110) ----------------------------------
     def index(self, s: dict, block: str | None = None) -> str:
@@ -444,6 +495,82 @@ class _Emitter:
                 else:
                     yield from self._lane_loops(it["body"])
 
+    # Launch shape of the same kind of region in CLUSTER mode (below): CTA c of a cluster of C does
+    # strip c of the strided axis, a batch of `jam` row slices is read from HBM once and a second
+    # time from L1 (jam x N / C doubles per CTA), column accumulators are N / C doubles of shared
+    # memory whatever N is.
+    # B200 sweep at n = 32768 (scripts/emit_cluster_sweep.py, profiles/r02/emit_cluster_sweep.log):
+    # ATAX 2.3 -> 5.2 TB/s (0.33 -> 0.73 of the hand-written cluster kernel).
+    CLUSTER_SHAPE = {"jam": 4, "unroll": 4, "threads": 256, "minb": 3, "bypass_l1": False, "per_sm": 3}
+    # Which variant runs is decided per call from the row length (profiles/r02/emit_cluster_sizes.log,
+    # emitted ATAX against the plain mapping): below 80 KiB the plain mapping (0.80-0.87 of the
+    # hand-written kernel at n <= 8192), then the smallest cluster whose slice per CTA is at most
+    # 40 KiB -- C = 4 at n = 12288 / 16384 (0.88 / 0.79 against 0.76 / 0.62 plain), C = 8 from
+    # n = 24576 on (0.94, 0.73 at 32768 against 0.70, 0.33).
+    CLUSTER_MIN_BYTES = 80 * 1024
+    CLUSTER_SLICE_BYTES = 40 * 1024
+
+    def cluster_mappable(self, root: dict):
+        """A region that reads a row twice (`rereads`) needs the whole row between the two reads
+        and one accumulator per column: beyond ~16 K columns neither L2 (rows in flight) nor shared
+        memory (accumulators) holds that per CTA, and the plain mapping falls to a third of the
+        hand-written kernel.  When every strided loop of the region runs over ONE full-extent axis
+        other than the partition axis, the C CTAs of a thread-block cluster can split that axis:
+        element-wise targets stay owned by one thread of one CTA, sums that leave the axis are
+        completed through distributed shared memory (`cluster_allreduce_n`), statements with a
+        memory target outside the strided loops are executed by one thread of the cluster.
+        Returns the strided axis or None."""
+        if not self.optimize or self.conservative or not 2 <= self.cluster_size <= 8:
+            return None                                   # (portable cluster sizes only)
+        axes = set()
+
+        def walk(its) -> bool:
+            for it in its:
+                if it["t"] == "stmt":
+                    # uniform statement: must not touch anything indexed by a strided axis (checked
+                    # once the axis is known, below)
+                    continue
+                if it["t"] != "loop":
+                    return False
+                if self.is_innermost(it):
+                    if it["sliced"]:
+                        return False
+                    axes.add(it["axis"])
+                    for st in it["body"]:
+                        name = st["target"] if st["role"] == "init" else \
+                            self.target_name(self.ops[str(st["op"])], True)
+                        if it["axis"] in self.st[name]["labels"] and self.st[name]["cls"] != "contracted":
+                            continue                      # element-wise in the strided axis
+                        if st["role"] != "compute" or not self.ops[str(st["op"])]["reduction"]:
+                            return False                  # a plain store that does not move with the axis
+                elif not walk(it["body"]):
+                    return False
+            return True
+
+        if not walk(root["body"]) or len(axes) != 1:
+            return None
+        v = next(iter(axes))
+        if v == root["axis"]:
+            return None
+        for it in self._all_stmts(root["body"]):
+            pass
+        # uniform statements (outside strided loops) must not read or write v-indexed storage
+        def uniform_ok(its, in_lane) -> bool:
+            for it in its:
+                if it["t"] == "loop":
+                    if not uniform_ok(it["body"], in_lane or self.is_innermost(it)):
+                        return False
+                    continue
+                if in_lane:
+                    continue
+                names = [it["target"]] if it["role"] == "init" else \
+                    list(self.ops[str(it["op"])]["operands"]) + [self.target_name(self.ops[str(it["op"])], True)]
+                if any(self.indexed_by(n, v) for n in names):
+                    return False
+            return True
+
+        return v if uniform_ok(root["body"], False) else None
+
     def strip_width(self) -> int:
         return self.threads * self.unroll
 
@@ -540,6 +667,11 @@ class _Emitter:
         return any(self.st[n]["cls"] != "contracted" and self.written(n) and not self.lane_private(n, key)
                    for n in names)
 
+    def t0(self) -> str:
+        """Guard of a statement with a memory target outside the strided loops: one thread of the
+        block -- in cluster mode one thread of the cluster (every CTA holds the same value)."""
+        return "threadIdx.x == 0 && c_ == 0" if self.cluster else "threadIdx.x == 0"
+
     # -- plain emission ------------------------------------------------------------------
     def emit_uniform_stmt(self, stmt: dict, block: str | None, in_region: bool, barrier: bool = True):
         """A statement outside any strided loop: same value in every thread."""
@@ -552,7 +684,7 @@ class _Emitter:
             if self.st[name]["cls"] == "contracted":
                 w.put(f"{self.scalar_names[name]} = 0.0;")
                 return
-            w.put(f"if (threadIdx.x == 0) {self.init_lvalue(name, block)} = 0.0;")
+            w.put(f"if ({self.t0()}) {self.init_lvalue(name, block)} = 0.0;")
             if barrier:
                 w.put("__syncthreads();")
             return
@@ -562,7 +694,7 @@ class _Emitter:
         if self.st[sname]["cls"] == "contracted":
             w.put(f"{lhs} {assign} {self.expr(op)};")
         else:
-            w.put(f"if (threadIdx.x == 0) {lhs} {assign} {self.expr(op)};")
+            w.put(f"if ({self.t0()}) {lhs} {assign} {self.expr(op)};")
             if barrier:
                 w.put("__syncthreads();")
 
@@ -747,15 +879,22 @@ class _Emitter:
                 w.put(f"if ((threadIdx.x & 31) == 0) {lhs} = {acc};")
                 close_rows()
                 continue
+            xbuf = f"xch_ + xpar_ * {self.cluster * self.jam}"
             if rows:
-                w.put(f"cta_allreduce_n<{R}>({acc}_a, scratch_);")
+                if self.cluster:
+                    w.put(f"cluster_allreduce_n<{R}, {self.cluster}>({acc}_a, scratch_, {xbuf}, xpar_);")
+                else:
+                    w.put(f"cta_allreduce_n<{R}>({acc}_a, scratch_);")
                 open_rows()
+            elif self.cluster:
+                w.put(f"{{ double one_[1] = {{{acc}}}; cluster_allreduce_n<1, {self.cluster}>(one_, scratch_, {xbuf}, xpar_); "
+                      f"{acc} = one_[0]; }}")
             else:
                 w.put(f"{acc} = cta_allreduce({acc}, scratch_);")
             if self.st[sname]["cls"] == "contracted":
                 w.put(f"{lhs} += {acc};")
             else:
-                w.put(f"if (threadIdx.x == 0) {lhs} += {acc};")
+                w.put(f"if ({self.t0()}) {lhs} += {acc};")
             close_rows()
         if self.loop_needs_barrier(loop, in_region):
             w.put("__syncthreads();")
@@ -820,7 +959,6 @@ class _Emitter:
         w.open(f"for (; {a}_b_ + {self.jam} <= {hi}; {a}_b_ += {self.jam})")
         for name in scalars:
             w.put(f"double {self.scalar_names[name]}_a[{self.jam}];")
-
         def rows(extra_alias=()):
             """open the per-row loop: row index and the row's private scalars under their usual names"""
             w.put("#pragma unroll")
@@ -979,128 +1117,223 @@ class _Emitter:
             flush_serial()
             org_t = int(ir["threads"][root["slot"]])
             t = max(org_t, self.blocks)
-            fname = f"{kname}_region{regions}"
+            base_name = f"{kname}_region{regions}"
             nb = f"nb{regions}_"
             regions += 1
-            saved = (self.jam, self.unroll, self.threads, self.minb, self.bypass_l1)
-            shape = self.region_shape(root)
-            if shape:
-                self.jam, self.unroll, self.threads = shape["jam"], shape["unroll"], shape["threads"]
-                self.minb, self.bypass_l1 = shape["minb"], shape["bypass_l1"]
-            self.begin_launch(root["body"], True)
-            # When the strided (innermost) loops run over the block's own slice, a
-            # slice narrower than the CTA leaves threads idle: cap the block count
-            # so every CTA gets at least a CTA-width of the axis (never below the
-            # organism's own count).  Any count is legal for the block formula.
-            tiles = self.tile_mappable(root)
-            if tiles:
-                # interleaved tiles: as many blocks as there are tiles at most
-                tile = self.unroll * self.threads
-                launches.append(f"long {nb} = ({root['extent']} + {tile - 1}) / {tile}; "
-                                f"if ({nb} < {org_t}) {nb} = {org_t}; if ({nb} > {t}) {nb} = {t};")
-            elif self.has_sliced_lane_loop(root["body"]):
-                launches.append(f"long {nb} = {root['extent']} / {self.threads}; "
-                                f"if ({nb} < {org_t}) {nb} = {org_t}; if ({nb} > {t}) {nb} = {t};")
-            else:
-                launches.append(f"long {nb} = {t};")
-            if shape:
-                uses_smem = True                     # (sms_ is read from the device below)
-                launches.append(f"{{ long cap_ = (long)sms_ * {shape['per_sm']}; if (cap_ < {org_t}) cap_ = {org_t}; "
-                                f"if ({nb} > cap_) {nb} = cap_; }}")
             ax, ext = root["axis"], root["extent"]
-            smem_args = ""
-            strip = self.strip_mappable(root["body"], root["axis"])
-            strip_ext = None
-            if strip is not None:
-                # 2-D grid: blockIdx.x = block of the partition, blockIdx.y = column strip
-                strip_ext = next(l["extent"] for l in self._lane_loops(root["body"]))
-                sw = self.strip_width()
-                launches.append(f"const long strips{regions}_ = ({strip_ext} + {sw - 1}) / {sw};")
-                launches.append(f"{{ long want_ = ((long)sms_ * 8 + strips{regions}_ - 1) / strips{regions}_; "
-                                f"if (want_ < {org_t}) want_ = {org_t}; if ({nb} > want_) {nb} = want_; }}")
-                uses_smem = True                     # (sms_ is read from the device below)
-                for name, sp in self.row_accs.items():
-                    e0 = self.st[name]["extents"][0]
-                    launches.append(f"cudaMallocAsync(&{sp}, sizeof(double) * (size_t)strips{regions}_ * {self.threads // 32} * (size_t){e0}, 0);")
-            if self.promoted and strip is not None:
-                total = len(self.promoted) * self.strip_width()
-                launches.append(f"const size_t smb{regions}_ = sizeof(double) * {total};")
-                launches.append(f"const int sm_ok{regions}_ = 1;")
-                smem_args = f", sm_ok{regions}_"
-            elif self.promoted:
-                # block partials indexed by the strided axis only: each thread owns its
-                # elements for the whole launch, so they accumulate in shared memory and
-                # reach the partial buffer once, at the end (when they fit; else in place)
-                uses_smem = True
-                total = " + ".join(f"(size_t){e}" for e in self.promoted.values())
-                launches.append(f"const size_t smb{regions}_ = sizeof(double) * ({total});")
-                launches.append(f"const int sm_ok{regions}_ = smb{regions}_ <= {SMEM_ACC_BYTES};")
-                launches.append(f"if (sm_ok{regions}_) {{ long fit_ = (long)sms_ * (long)((227 * 1024) / (smb{regions}_ + 2048)); "
-                                f"if (fit_ < {org_t}) fit_ = {org_t}; if ({nb} > fit_) {nb} = fit_; }}")
-                launches.append(f"static bool attr{regions}_ = false; if (!attr{regions}_) {{ cudaFuncSetAttribute({fname}, "
-                                f"cudaFuncAttributeMaxDynamicSharedMemorySize, {SMEM_ACC_BYTES}); attr{regions}_ = true; }}")
-                smem_args = f", sm_ok{regions}_"
-            # min-blocks in the launch bounds: without it ptxas aims for full occupancy, keeps the
-            # register count low and sinks every batched load down to its use
-            bounds = f"{self.threads}, {self.minb}" if self.optimize else f"{self.threads}"
-            w.open(f"__global__ void __launch_bounds__({bounds}) {fname}({decl}, long nblocks_"
-                   + (", int sm_ok_" if self.promoted else "") + ")")
-            scalars_decl()
-            w.put("const long p_ = blockIdx.x;")
-            w.put(f"const long {ax}_lo = ({ext} * p_) / nblocks_;")
-            w.put(f"const long {ax}_hi = ({ext} * (p_ + 1)) / nblocks_;")
-            w.put(f"(void){ax}_lo; (void){ax}_hi;")
-            self.tile_axis = root["axis"] if tiles else None
-            if strip is not None:
-                sw = self.strip_width()
-                w.put(f"const long {strip}_s0_ = (long)blockIdx.y * {sw};")
-                w.put(f"const long {strip}_s1_ = {strip}_s0_ + {sw} < {strip_ext} ? {strip}_s0_ + {sw} : {strip_ext};")
-                self.strip_axis = strip
-            if self.promoted:
-                w.put("extern __shared__ double dyn_[];")
-                offset = "0"
-                for name, e in self.promoted.items():
-                    size = self.st[name]["extents"][0]
-                    if strip is not None:          # X_l[j] is valid for the strip's j
-                        w.put(f"double *{name}_l = dyn_ + ({offset}) - {strip}_s0_; (void)sm_ok_;")
-                        offset += f" + {self.strip_width()}"
-                    else:
-                        w.put(f"double *{name}_l = sm_ok_ ? dyn_ + ({offset}) : {name} + p_ * ({size});")
-                        offset += f" + {e}"
-            self.emit_items(root["body"], "p_", True)
-            if self.promoted:
-                w.open("if (sm_ok_)")
-                for name in self.promoted:
-                    s = self.st[name]
-                    lab, size = s["labels"][0], s["extents"][0]
-                    lo, hi = (f"{strip}_s0_", f"{strip}_s1_") if strip is not None else ("0", size)
-                    w.put(f"for (long {lab} = {lo} + threadIdx.x; {lab} < {hi}; {lab} += blockDim.x) "
-                          f"{name}[p_ * ({size}) + {lab}] = {name}_l[{lab}];")
-                w.close()
-            self.strip_axis = None
-            self.tile_axis = None
-            w.close()
-            w.put()
-            dyn = f"sm_ok{regions}_ ? smb{regions}_ : 0" if self.promoted else "0"
-            grid = f"dim3((unsigned){nb}, (unsigned)strips{regions}_)" if strip is not None else f"(unsigned){nb}"
-            launches.append(f"{fname}<<<{grid}, {self.threads}, {dyn}, 0>>>({call}, {nb}{smem_args});")
-            for name, sp in (self.row_accs.items() if strip is not None else ()):
-                # ascending (strip, warp) partials, a thread per row
-                e0, lab = self.st[name]["extents"][0], self.st[name]["labels"][0]
-                jname = f"{kname}_rows{regions}_{name}"
-                w.open(f"__global__ void __launch_bounds__(256) {jname}({decl}, long strips_)")
-                w.put(f"const long {lab} = (long)blockIdx.x * 256 + threadIdx.x;")
-                w.open(f"if ({lab} < {e0})")
-                w.put(f"double acc = {sp}[{lab}];")
-                w.put(f"for (long c = 1; c < strips_; ++c) acc += {sp}[c * ({e0}) + {lab}];")
-                w.put(f"{self.ref(name)} = acc;")
-                w.close()
+            saved = (self.jam, self.unroll, self.threads, self.minb, self.bypass_l1)
+            launches.append(f"long {nb} = 0;")
+
+            def variant(cluster_axis, C=0):
+                """One kernel for the region (plain / strips, or cluster mode) and the host statements
+                that size and launch it; `nb` receives its block count."""
+                nonlocal uses_smem
+                out = []
+                fname = base_name + (f"c{C}" if cluster_axis else "")
+                shape = dict(self.CLUSTER_SHAPE) if cluster_axis else self.region_shape(root)
+                if cluster_axis and self.cluster_jam:
+                    shape["jam"] = self.cluster_jam
+                if cluster_axis and self.cluster_minb:
+                    shape["minb"] = self.cluster_minb
+                if cluster_axis and self.cluster_threads:
+                    shape["threads"] = self.cluster_threads
+                if shape:
+                    self.jam, self.unroll, self.threads = shape["jam"], shape["unroll"], shape["threads"]
+                    self.minb, self.bypass_l1 = shape["minb"], shape["bypass_l1"]
+                self.begin_launch(root["body"], True)
+                # When the strided (innermost) loops run over the block's own slice, a
+                # slice narrower than the CTA leaves threads idle: cap the block count
+                # so every CTA gets at least a CTA-width of the axis (never below the
+                # organism's own count).  Any count is legal for the block formula.
+                tiles = self.tile_mappable(root) and not cluster_axis
+                if tiles:
+                    # interleaved tiles: as many blocks as there are tiles at most
+                    tile = self.unroll * self.threads
+                    out.append(f"{nb} = ({root['extent']} + {tile - 1}) / {tile}; "
+                               f"if ({nb} < {org_t}) {nb} = {org_t}; if ({nb} > {t}) {nb} = {t};")
+                elif self.has_sliced_lane_loop(root["body"]):
+                    out.append(f"{nb} = {root['extent']} / {self.threads}; "
+                               f"if ({nb} < {org_t}) {nb} = {org_t}; if ({nb} > {t}) {nb} = {t};")
+                else:
+                    out.append(f"{nb} = {t};")
+                if shape and not C:
+                    uses_smem = True                     # (sms_ is read from the device below)
+                    out.append(f"{{ long cap_ = (long)sms_ * {shape['per_sm']}; if (cap_ < {org_t}) cap_ = {org_t}; "
+                               f"if ({nb} > cap_) {nb} = cap_; }}")
+                smem_args = ""
+                strip = None if cluster_axis else self.strip_mappable(root["body"], root["axis"])
+                strip_ext = None
+                if strip is not None:
+                    # 2-D grid: blockIdx.x = block of the partition, blockIdx.y = column strip
+                    strip_ext = next(l["extent"] for l in self._lane_loops(root["body"]))
+                    sw = self.strip_width()
+                    out.append(f"const long strips{regions}_ = ({strip_ext} + {sw - 1}) / {sw};")
+                    out.append(f"{{ long want_ = ((long)sms_ * 8 + strips{regions}_ - 1) / strips{regions}_; "
+                               f"if (want_ < {org_t}) want_ = {org_t}; if ({nb} > want_) {nb} = want_; }}")
+                    uses_smem = True                     # (sms_ is read from the device below)
+                    for name, sp in self.row_accs.items():
+                        e0 = self.st[name]["extents"][0]
+                        out.append(f"cudaMallocAsync(&{sp}, sizeof(double) * (size_t)strips{regions}_ * {self.threads // 32} * (size_t){e0}, 0);")
+                if cluster_axis:
+                    # the cluster's C CTAs split the strided axis: strip c = [c sw, (c + 1) sw)
+                    strip_ext = next(l["extent"] for l in self._lane_loops(root["body"]))
+                    out.append(f"const long csw{regions}_ = ((({strip_ext} + {C - 1}) / {C}) + 1) & ~1L;")
+                if self.promoted and strip is not None:
+                    total = len(self.promoted) * self.strip_width()
+                    out.append(f"const size_t smb{regions}_ = sizeof(double) * {total};")
+                    out.append(f"const int sm_ok{regions}_ = 1;")
+                    smem_args = f", sm_ok{regions}_"
+                elif self.promoted and cluster_axis:
+                    out.append(f"const size_t smb{regions}_ = sizeof(double) * {len(self.promoted)} * (size_t)csw{regions}_;")
+                    out.append(f"const int sm_ok{regions}_ = smb{regions}_ <= {SMEM_ACC_BYTES // 2};")
+                    out.append(f"static bool attr{regions}_ = false; if (!attr{regions}_) {{ cudaFuncSetAttribute({fname}, "
+                               f"cudaFuncAttributeMaxDynamicSharedMemorySize, {SMEM_ACC_BYTES // 2}); attr{regions}_ = true; }}")
+                    smem_args = f", sm_ok{regions}_"
+                elif self.promoted:
+                    # block partials indexed by the strided axis only: each thread owns its
+                    # elements for the whole launch, so they accumulate in shared memory and
+                    # reach the partial buffer once, at the end (when they fit; else in place)
+                    uses_smem = True
+                    total = " + ".join(f"(size_t){e}" for e in self.promoted.values())
+                    out.append(f"const size_t smb{regions}_ = sizeof(double) * ({total});")
+                    out.append(f"const int sm_ok{regions}_ = smb{regions}_ <= {SMEM_ACC_BYTES};")
+                    out.append(f"if (sm_ok{regions}_) {{ long fit_ = (long)sms_ * (long)((227 * 1024) / (smb{regions}_ + 2048)); "
+                               f"if (fit_ < {org_t}) fit_ = {org_t}; if ({nb} > fit_) {nb} = fit_; }}")
+                    out.append(f"static bool attr{regions}_ = false; if (!attr{regions}_) {{ cudaFuncSetAttribute({fname}, "
+                               f"cudaFuncAttributeMaxDynamicSharedMemorySize, {SMEM_ACC_BYTES}); attr{regions}_ = true; }}")
+                    smem_args = f", sm_ok{regions}_"
+                if cluster_axis:
+                    # one wave: as many clusters as the device holds at once (clusters live inside a
+                    # GPC, so this is less than SMs x CTAs per SM / C), asked once per footprint
+                    dynb = f"(sm_ok{regions}_ ? smb{regions}_ : 0)" if self.promoted else "0"
+                    out.append("cudaLaunchConfig_t cfg_ = {}; cudaLaunchAttribute cattr_;")
+                    out.append(f"cattr_.id = cudaLaunchAttributeClusterDimension; cattr_.val.clusterDim.x = {C}; "
+                               "cattr_.val.clusterDim.y = 1; cattr_.val.clusterDim.z = 1;")
+                    out.append(f"cfg_.blockDim = dim3({self.threads}); cfg_.dynamicSmemBytes = {dynb}; cfg_.stream = 0; "
+                               "cfg_.attrs = &cattr_; cfg_.numAttrs = 1;")
+                    out.append(f"static size_t occ_for{regions}_ = ~(size_t)0; static int occ{regions}_ = 0;")
+                    out.append(f"if (occ_for{regions}_ != cfg_.dynamicSmemBytes) {{ cfg_.gridDim = dim3({C} * 64); "
+                               f"if (cudaOccupancyMaxActiveClusters(&occ{regions}_, {fname}, &cfg_) != cudaSuccess || occ{regions}_ < 1) "
+                               f"occ{regions}_ = 1; occ_for{regions}_ = cfg_.dynamicSmemBytes; }}")
+                    out.append(f"{{ long cap_ = occ{regions}_; if (cap_ < {org_t}) cap_ = {org_t}; if ({nb} > cap_) {nb} = cap_; }}")
+                # min-blocks in the launch bounds: without it ptxas aims for full occupancy, keeps the
+                # register count low and sinks every batched load down to its use
+                bounds = f"{self.threads}, {self.minb}" if self.optimize else f"{self.threads}"
+                w.open(f"__global__ void __launch_bounds__({bounds}) {fname}({decl}, long nblocks_"
+                       + (", int sm_ok_" if self.promoted else "") + (", long csw_" if C else "") + ")")
+                scalars_decl()
+                if C:
+                    w.put(f"__shared__ double xch_[{2 * C * max(self.jam, 1)}];")
+                    w.put("int xpar_ = 0; (void)xpar_;")
+                    w.put(f"const long p_ = blockIdx.x / {C};")
+                    w.put(f"const long c_ = blockIdx.x % {C}; (void)c_;")
+                else:
+                    w.put("const long p_ = blockIdx.x;")
+                w.put(f"const long {ax}_lo = ({ext} * p_) / nblocks_;")
+                w.put(f"const long {ax}_hi = ({ext} * (p_ + 1)) / nblocks_;")
+                w.put(f"(void){ax}_lo; (void){ax}_hi;")
+                self.tile_axis = root["axis"] if tiles else None
+                if strip is not None:
+                    sw = self.strip_width()
+                    w.put(f"const long {strip}_s0_ = (long)blockIdx.y * {sw};")
+                    w.put(f"const long {strip}_s1_ = {strip}_s0_ + {sw} < {strip_ext} ? {strip}_s0_ + {sw} : {strip_ext};")
+                    self.strip_axis = strip
+                if cluster_axis:
+                    cv = cluster_axis
+                    w.put(f"const long {cv}_s0_ = c_ * csw_ < {strip_ext} ? c_ * csw_ : {strip_ext};")
+                    w.put(f"const long {cv}_s1_ = {cv}_s0_ + csw_ < {strip_ext} ? {cv}_s0_ + csw_ : {strip_ext};")
+                    self.strip_axis = cv
+                    self.cluster = C
+                if self.promoted:
+                    w.put("extern __shared__ double dyn_[];")
+                    offset = "0"
+                    for name, e in self.promoted.items():
+                        size = self.st[name]["extents"][0]
+                        if strip is not None:          # X_l[j] is valid for the strip's j
+                            w.put(f"double *{name}_l = dyn_ + ({offset}) - {strip}_s0_; (void)sm_ok_;")
+                            offset += f" + {self.strip_width()}"
+                        elif cluster_axis:
+                            w.put(f"double *{name}_l = sm_ok_ ? dyn_ + ({offset}) - {cluster_axis}_s0_ : {name} + p_ * ({size});")
+                            offset += " + csw_"
+                        else:
+                            w.put(f"double *{name}_l = sm_ok_ ? dyn_ + ({offset}) : {name} + p_ * ({size});")
+                            offset += f" + {e}"
+                self.emit_items(root["body"], "p_", True)
+                if self.promoted:
+                    w.open("if (sm_ok_)")
+                    for name in self.promoted:
+                        s = self.st[name]
+                        lab, size = s["labels"][0], s["extents"][0]
+                        sa = strip if strip is not None else cluster_axis
+                        lo, hi = (f"{sa}_s0_", f"{sa}_s1_") if sa is not None else ("0", size)
+                        w.put(f"for (long {lab} = {lo} + threadIdx.x; {lab} < {hi}; {lab} += blockDim.x) "
+                              f"{name}[p_ * ({size}) + {lab}] = {name}_l[{lab}];")
+                    w.close()
+                if C:
+                    # nobody leaves while a peer may still read its exchange buffer
+                    w.put('asm volatile("barrier.cluster.arrive.release.aligned;\\n\\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");')
+                self.strip_axis = None
+                self.tile_axis = None
+                self.cluster = 0
                 w.close()
                 w.put()
-                launches.append(f"{jname}<<<(unsigned)(({e0} + 255) / 256), 256, 0, 0>>>({call}, strips{regions}_ * {self.threads // 32});")
-                launches.append(f"cudaFreeAsync({sp}, 0);")
-            self.row_accs = {}
-            self.promoted = {}
+                dyn = f"sm_ok{regions}_ ? smb{regions}_ : 0" if self.promoted else "0"
+                if strip is not None:
+                    grid = f"dim3((unsigned){nb}, (unsigned)strips{regions}_)"
+                elif C:
+                    grid = f"(unsigned)({nb} * {C})"
+                else:
+                    grid = f"(unsigned){nb}"
+                if C:
+                    out.append(f"cfg_.gridDim = dim3({grid});")
+                    out.append(f"cudaLaunchKernelEx(&cfg_, {fname}, {call}, {nb}{smem_args}, csw{regions}_);")
+                else:
+                    out.append(f"{fname}<<<{grid}, {self.threads}, {dyn}, 0>>>({call}, {nb}{smem_args});")
+                for name, sp in (self.row_accs.items() if strip is not None else ()):
+                    # ascending (strip, warp) partials, a thread per row
+                    e0, lab = self.st[name]["extents"][0], self.st[name]["labels"][0]
+                    jname = f"{kname}_rows{regions}_{name}"
+                    w.open(f"__global__ void __launch_bounds__(256) {jname}({decl}, long strips_)")
+                    w.put(f"const long {lab} = (long)blockIdx.x * 256 + threadIdx.x;")
+                    w.open(f"if ({lab} < {e0})")
+                    w.put(f"double acc = {sp}[{lab}];")
+                    w.put(f"for (long c = 1; c < strips_; ++c) acc += {sp}[c * ({e0}) + {lab}];")
+                    w.put(f"{self.ref(name)} = acc;")
+                    w.close()
+                    w.close()
+                    w.put()
+                    out.append(f"{jname}<<<(unsigned)(({e0} + 255) / 256), 256, 0, 0>>>({call}, strips{regions}_ * {self.threads // 32});")
+                    out.append(f"cudaFreeAsync({sp}, 0);")
+                self.row_accs = {}
+                self.promoted = {}
+                self.jam, self.unroll, self.threads, self.minb, self.bypass_l1 = saved
+                return out
+
+            cl_axis = None
+            if self.optimize and self.auto and self.cluster_size and self.rereads(root["body"]):
+                self.begin_launch(root["body"], True)
+                # (a region that can be cut into independent column strips -- the two reads of a row do
+                #  not depend on each other, BiCGK's two products -- is better off that way: measured)
+                if self.strip_mappable(root["body"], root["axis"]) is None:
+                    cl_axis = self.cluster_mappable(root)
+                self.row_accs = {}
+            plain = variant(None)
+            if cl_axis is not None:
+                sizes = [c for c in (4, 8) if c <= self.cluster_size] or [self.cluster_size]
+                row_ext = next(l["extent"] for l in self._lane_loops(root["body"]))
+                launches.append(f"const size_t row{regions}_ = (size_t){row_ext} * sizeof(double);")
+                for k, C in enumerate(sizes):
+                    cond = f"row{regions}_ >= {self.cluster_min_bytes}"
+                    if k + 1 < len(sizes):
+                        cond += f" && row{regions}_ <= {C * self.CLUSTER_SLICE_BYTES}"
+                    clustered = variant(cl_axis, C)
+                    launches.append(("if" if k == 0 else "} else if") + f" ({cond}) {{")
+                    launches.extend("    " + st for st in clustered)
+                launches.append("} else {")
+                launches.extend("    " + st for st in plain)
+                launches.append("}")
+            else:
+                launches.extend(plain)
             for result in root["partials"]:
                 pname = self.partial_for(result)
                 jname = f"{kname}_join{regions}_{result}"
@@ -1170,7 +1403,9 @@ def emit_cuda(ir: dict, blocks: int = DEFAULT_BLOCKS, optimize: bool = True, **t
     `optimize=False` prints the plain mapping only (every barrier, no unroll-and-jam, block
     partials accumulated in global memory).  `tune`: jam (rows per batch), unroll (of the
     strided loop under a batch), threads (per CTA of a parallel region), minb (CTAs per SM the
-    register budget is sized for), sync (1: cudaStreamSynchronize before returning), bypass_l1 (0: 2-D operands are loaded L1-allocating; ATAX-like
+    register budget is sized for), sync (1: cudaStreamSynchronize before returning), cluster (CTAs per
+    cluster of the cluster-mode variant of regions that read a row twice, 0: none), cluster_min_bytes
+    (row length from which that variant runs; 0 forces it), cluster_jam, bypass_l1 (0: 2-D operands are loaded L1-allocating; ATAX-like
     bodies that read a row twice gain 10 %)."""
     em = _Emitter(ir, int(blocks), bool(optimize), **tune)
     source = em.emit()
@@ -1494,11 +1729,15 @@ def estimate_cost_ir(ir: dict, extents: dict, model: EmitModel | None = None,
     def has_loop(items):
         return any(it["t"] == "loop" for it in items)
 
-    strip = {"axis": None, "count": 1.0}          # 2-D (block x column strip) mapping of the launch
+    # 2-D (block x column strip) mapping of the launch; `width` = columns of a strip.  (The cluster
+    # variants the emitter adds for rows of 80 KiB and more are not modelled: the coefficients are
+    # fitted at n <= 4096, where they never run.)
+    strip = {"axis": None, "count": 1.0, "width": 0.0, "reread_free": False}
 
-    def walk(items, trips, nb, threads, acc, in_region, batch):
+    def walk(items, trips, nb, threads, acc, in_region, batch, seen=None):
         """acc: dict(bytes=, steps=) for one launch; `trips` executions per block, `batch`
         rows handled per execution (1 unless the enclosing loop is jammed)."""
+        seen = set() if seen is None else seen
         for it in items:
             if it["t"] == "stmt":
                 target = it["target"] if it["role"] == "init" else ops[str(it["op"])]["result"]
@@ -1508,12 +1747,12 @@ def estimate_cost_ir(ir: dict, extents: dict, model: EmitModel | None = None,
             rng = ext[it["extent"]] / nb if it["sliced"] else ext[it["extent"]]
             if has_loop(it["body"]):
                 jam = em.jam if em.jam_legal(it, in_region) else 1
-                walk(it["body"], trips * max(rng / jam, 1.0), nb, threads, acc, in_region, jam)
+                walk(it["body"], trips * max(rng / jam, 1.0), nb, threads, acc, in_region, jam, set())
                 continue
             # strided (innermost) loop
             ctas = nb
             if strip["axis"] == it["axis"] and not it["sliced"]:
-                rng = min(rng, float(em.strip_width()))        # a CTA walks one strip of it
+                rng = min(rng, strip["width"])                 # a CTA walks one strip of it
                 ctas = nb * strip["count"]
             per_thread = max(1.0, rng / threads)
             mats, vecs, rmw = set(), set(), False
@@ -1530,6 +1769,8 @@ def estimate_cost_ir(ir: dict, extents: dict, model: EmitModel | None = None,
                         continue
                     (mats if len(s_["labels"]) == 2 else vecs).add(n)
             rmw = em.is_global_rmw(it, accs, in_region)
+            if strip["reread_free"]:
+                mats, _ = mats - seen, seen.update(mats)
             acc["bytes"] += 8.0 * len(mats) * rng * trips * batch * ctas + 8.0 * len(vecs) * rng * ctas
             ends_in_sync = bool(accs) or em.loop_needs_barrier(it, in_region)
             trip = m.rmw_trip_us if rmw else (m.jam_trip_us if batch > 1 else m.trip_us)
@@ -1569,7 +1810,7 @@ def estimate_cost_ir(ir: dict, extents: dict, model: EmitModel | None = None,
             nb = min(nb, max(org_t, float(int(ext[root["extent"]]) // em.threads)))
         axis = em.strip_mappable(root["body"], root["axis"])
         row_joins = len(em.row_accs)
-        strip["axis"], strip["count"] = axis, 1.0
+        strip["axis"], strip["count"], strip["width"], strip["reread_free"] = axis, 1.0, float(em.strip_width()), False
         if axis is not None:
             width = ext[next(l["extent"] for l in em._lane_loops(root["body"]))]
             strip["count"] = float(-(-int(width) // em.strip_width()))
@@ -1588,7 +1829,7 @@ def estimate_cost_ir(ir: dict, extents: dict, model: EmitModel | None = None,
             per_launch.append((m.launch_us + 8.0 * ext[root["extent"]] * (strip["count"] + 1)
                                / (m.peak_gbs * 1e9) * 1e6) * 1e-6)
             launches += 1
-        strip["axis"], strip["count"] = None, 1.0
+        strip.update(axis=None, count=1.0, reread_free=False)
         em.row_accs = {}
         em.jam, em.unroll, em.threads, em.minb, em.bypass_l1 = saved
         launches += 1

@@ -50,7 +50,7 @@ def test_structure_of_the_bicgk_max_fuse_kernel():
     assert "lacc1 += __dmul_rn(A[i * N + j], p[j]);" in src            # row dot -> thread accumulator
     assert "s_part[p_ * (N) + j] += __dmul_rn(A[i * N + j], r[i]);" in src   # column sums: own j
     assert "cta_allreduce(lacc1, scratch_)" in src
-    assert "long nb0_ = 64;" in src and "bicgk_region0<<<(unsigned)nb0_, 256, 0, 0>>>" in src
+    assert "nb0_ = 64;" in src and "bicgk_region0<<<(unsigned)nb0_, 256, 0, 0>>>" in src
     assert "bicgk_join1_s" in src
     # optimised: rows four at a time, one batched reduction, explicit load / compute batches with
     # a literal stride, and -- q being a pure row dot -- a 2-D grid of column strips: the column
@@ -81,6 +81,25 @@ def test_structure_of_the_bicgk_max_fuse_kernel():
     assert "double t0_s_a[4];" in cuemit.emit_cuda(IRS["atax"][0], auto=0).source
     assert "double *y_part_l = sm_ok_ ? dyn_ + (0) : y_part + p_ * (N);" in atax
     assert "y_part[p_ * (N) + j] = y_part_l[j];" in atax and "blockIdx.y" not in atax
+    # ... and for rows of 80 KiB and more two more kernels in CLUSTER mode, chosen at run time: the 4
+    # or 8 CTAs of a cluster split the columns (accumulators: N / C doubles of shared memory
+    # whatever N is, a batch of four row slices read from HBM once and from L1 the second time), the
+    # row dot is completed through distributed shared memory, one wave of clusters
+    assert "const size_t row1_ = (size_t)N * sizeof(double);" in atax
+    assert "if (row1_ >= 81920 && row1_ <= 163840) {" in atax and "} else if (row1_ >= 81920) {" in atax
+    assert "__launch_bounds__(256, 3) atax_region0c4(" in atax
+    assert "__launch_bounds__(256, 3) atax_region0c8(" in atax and "long csw_)" in atax
+    assert "const long p_ = blockIdx.x / 8;" in atax and "const long c_ = blockIdx.x % 8;" in atax
+    assert "const long j_s0_ = c_ * csw_ < N ? c_ * csw_ : N;" in atax
+    assert "double *y_part_l = sm_ok_ ? dyn_ + (0) - j_s0_ : y_part + p_ * (N);" in atax
+    assert "cluster_allreduce_n<4, 4>(lacc3_a, scratch_, xch_ + xpar_ * 16, xpar_);" in atax
+    assert "cluster_allreduce_n<4, 8>(lacc5_a, scratch_, xch_ + xpar_ * 32, xpar_);" in atax
+    assert "cudaOccupancyMaxActiveClusters(&occ1_, atax_region0c8, &cfg_)" in atax
+    assert "cudaLaunchKernelEx(&cfg_, atax_region0c8, A, x, y, y_part, M, N, nb0_, sm_ok1_, csw1_);" in atax
+    assert "atax_region0c" not in cuemit.emit_cuda(IRS["atax"][0], cluster=0).source
+    # BiCGK's two reads of a row do not depend on each other: column strips, no cluster variant
+    bic = cuemit.emit_cuda(next(i for i in IRS["bicgk"] if i["organism"].startswith("{_{p(i)}{_i{_j 1}{_j 2}}}"))).source
+    assert "bicgk_region0c" not in bic and "blockIdx.y" in bic
     # a region whose statements are all element-wise in the strided axis needs no row join at all
     best = json.loads((Path(__file__).parent.parent / "profiles" / "r01" / "ga_best_irs.json").read_text())
     gem2 = cuemit.emit_cuda(best["gemver"]["alternatives"][1]["ir"]).source
@@ -89,21 +108,21 @@ def test_structure_of_the_bicgk_max_fuse_kernel():
     # a pure vector region deals its own axis out in interleaved tiles (all CTAs sweep together)
     axp = cuemit.emit_cuda(IRS["axpydot"][0]).source
     assert "for (long t_ = p_; t_ * 1024 < M; t_ += nblocks_)" in axp and "const long k_t0_ = t_ * 1024;" in axp
-    assert "long nb0_ = (M + 1023) / 1024;" in axp
+    assert "nb0_ = (M + 1023) / 1024;" in axp
     # a value written by thread 0 and read by every thread keeps all barriers and is not jammed
     plain = cuemit.emit_cuda(next(i for i in IRS["gesummv"] if i["organism"].startswith("{_i{_j 1}}{_i 2}"))).source
     assert "cta_allreduce_n<" not in plain and "__syncthreads();" in plain
     # a region whose strided loops run over its own slice gets at least a CTA-width per block
     gem = cuemit.emit_cuda(IRS["gemver"][0], blocks=592).source
-    assert "long nb0_ = N / 256; if (nb0_ < 8) nb0_ = 8; if (nb0_ > 592) nb0_ = 592;" in gem
+    assert "nb0_ = N / 256; if (nb0_ < 8) nb0_ = 8; if (nb0_ > 592) nb0_ = 592;" in gem
 
 
-def _compile_all(irs, workdir, blocks=cuemit.DEFAULT_BLOCKS, optimize=True):
+def _compile_all(irs, workdir, blocks=cuemit.DEFAULT_BLOCKS, optimize=True, **tune):
     tc = cuemit.NvccToolchain()
 
     def job(args):
         idx, ir = args
-        k = cuemit.emit_cuda(ir, blocks=blocks, optimize=optimize)
+        k = cuemit.emit_cuda(ir, blocks=blocks, optimize=optimize, **tune)
         return idx, k, tc.compile(k.source, workdir, name=f"{ir['name'].lower()}_{idx}")
 
     with ThreadPoolExecutor(max_workers=8) as pool:
@@ -166,6 +185,37 @@ def test_every_organism_matches_the_oracle(bto_lib, oracle, tmp_path, name, opti
             for out in ELEMENTWISE.get(name, ()):
                 assert np.array_equal(np.asarray(got[out]), np.asarray(want[out])), (name, ir["organism"], out)
     assert worst < 1e-10          # the reference's own gate
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("cluster,jam", [(8, 0), (4, 2), (2, 1)])
+def test_cluster_mode_matches_the_oracle(bto_lib, oracle, tmp_path, cluster, jam):
+    """Regions that read a row twice, emitted in cluster mode and FORCED at every size
+    (`cluster_min_bytes=0`): the CTAs of a cluster split the columns, row dots are completed
+    through distributed shared memory.  Shapes: fewer columns than CTAs in the cluster (empty
+    strips), odd column counts, rows that do not fill a batch, more clusters than rows, and a
+    row too long for the accumulators of a small cluster to fit shared memory."""
+    picked = [(name, idx, ir) for name in ("atax", "batax") for idx, ir in enumerate(IRS[name])
+              if "{_i{_j 1}{_j 2}}" in ir["organism"] and ir["organism"].startswith("{_{p(i)}")]
+    assert {n for n, _, _ in picked} == {"atax", "batax"}
+    sizes = [(1, 1), (3, 5), (7, 50), (200, 201), (513, 1030), (41, 4099), (6, 24700)]
+    for name, idx, ir in picked:
+        typed = bto.load_graph(name)
+        kernel = cuemit.emit_cuda(ir, blocks=37, cluster=cluster, cluster_min_bytes=0, cluster_jam=jam)
+        assert f"{name}_region0c{cluster}(" in kernel.source
+        path = cuemit.NvccToolchain().compile(kernel.source, tmp_path, name=f"{name}_{idx}_c{cluster}")
+        for (m, n) in sizes:
+            ext = {"M": m, "N": n}
+            inputs = bto.random_inputs(typed, ext, seed=idx + m)
+            want = oracle.oracle_run(name, inputs, ext, threads=8)
+            got = cuemit.run_emitted(path, kernel, ir, inputs, ext)
+            for out in want:
+                assert not np.any(np.isnan(np.asarray(got[out]))), (name, ir["organism"], ext, out)
+            err = bto.max_rel_error(got, want)
+            assert err <= 1e-12 * max(1.0, math.log2(max(ext.values()))), (name, ir["organism"], ext, err)
+            again = cuemit.run_emitted(path, kernel, ir, inputs, ext)      # fixed order: bit-stable
+            for out in want:
+                assert np.array_equal(np.asarray(got[out]), np.asarray(again[out])), (name, ext, out)
 
 
 @pytest.mark.gpu
