@@ -585,7 +585,7 @@ int bto_set_tuning(const char *key, long value)
     if (slot == &g_tuning.rowstream_min_n) ok = value >= 1024;
     if (slot == &g_tuning.host_panel_mib) ok = value >= 1 && value <= 4096;
     if (slot == &g_tuning.exchange_phases) ok = value >= 1 && value <= 3;
-    if (slot == &g_tuning.atax_cluster) ok = value == 0 || value == 1 || value == 2 || value == 4 || value == 8 || value == 9 || value == 16;
+    if (slot == &g_tuning.atax_cluster) ok = (value >= 0 && value <= 10) || value == 16;
     if (slot == &g_tuning.atax_stages) ok = value == 0 || (value >= 2 && value <= 8);
     if (slot == &g_tuning.atax_rows) ok = value == 0 || value == 1;
     if (slot == &g_tuning.atax_per_sm) ok = value == 1 || value == 2;

@@ -63,24 +63,49 @@ struct AtaxPlan {
     int nclusters = 0;
 };
 
-// TR (rows per panel) is 16 / KMAX capped at 8: a panel is 16 double2 per thread.
-// `small` halves it (fewer registers per tile, more panels per byte).
+// TR (rows per panel): the largest power of two with TR * KMAX <= 16, capped at 8 -- a panel is at
+// most 16 double2 per thread.  `small` halves it (fewer registers per tile, more panels per byte).
+// KMAX need not be a power of two: a slice of 3072 columns (N = 24576 over 8 CTAs) in a KMAX = 8
+// kernel runs 8 iterations for 6 of data, and the per-panel chain is what bounds the kernel --
+// 5.4 TB/s where KMAX = 6 gives 7 (profiles/r02/atax_kmax.log).
+constexpr int atax_tr(int kmax) { return kmax <= 2 ? 8 : kmax <= 4 ? 4 : kmax <= 8 ? 2 : 1; }
+
 template <int C>
 AtaxKernel atax_kernel_ptr(int kmax, bool small)
 {
     switch (kmax) {
         case 1: return small ? atax_cluster_kernel<C, 1, 4> : atax_cluster_kernel<C, 1, 8>;
         case 2: return small ? atax_cluster_kernel<C, 2, 4> : atax_cluster_kernel<C, 2, 8>;
+        case 3: return small ? atax_cluster_kernel<C, 3, 2> : atax_cluster_kernel<C, 3, 4>;
         case 4: return small ? atax_cluster_kernel<C, 4, 2> : atax_cluster_kernel<C, 4, 4>;
+        case 5: return small ? atax_cluster_kernel<C, 5, 1> : atax_cluster_kernel<C, 5, 2>;
+        case 6: return small ? atax_cluster_kernel<C, 6, 1> : atax_cluster_kernel<C, 6, 2>;
+        case 7: return small ? atax_cluster_kernel<C, 7, 1> : atax_cluster_kernel<C, 7, 2>;
         case 8: return small ? atax_cluster_kernel<C, 8, 1> : atax_cluster_kernel<C, 8, 2>;
         case 16: return atax_cluster_kernel<C, 16, 1>;
     }
     return nullptr;
 }
 
+// Cluster sizes that exist only to give mid-size matrices full-width slices (N = 24576 over 6 CTAs
+// = 4096 columns each, where 8 or 9 CTAs hold 3072 / 2736 and the panels get too small for their
+// fixed cost): whole panels, one CTA per SM, slices of 5 .. 8 iterations.
+template <int C>
+AtaxKernel atax_kernel_ptr_wide(int kmax, bool small)
+{
+    if (small) return nullptr;
+    switch (kmax) {
+        case 5: return atax_cluster_kernel<C, 5, 2>;
+        case 6: return atax_cluster_kernel<C, 6, 2>;
+        case 7: return atax_cluster_kernel<C, 7, 2>;
+        case 8: return atax_cluster_kernel<C, 8, 2>;
+    }
+    return nullptr;
+}
+
 int atax_rows_of(int kmax, bool small)
 {
-    const int full = (16 / kmax) < kAtaxMaxRows ? (16 / kmax) : kAtaxMaxRows;
+    const int full = atax_tr(kmax);
     if (!small || kmax == 16) return full;
     return kmax == 1 ? 4 : full / 2;
 }
@@ -115,9 +140,14 @@ AtaxKernel atax_kernel_ptr(int c, int kmax, bool small, bool two)
     switch (c) {
         case 1: return atax_kernel_ptr<1>(kmax, small);
         case 2: return atax_kernel_ptr<2>(kmax, small);
+        case 3: return atax_kernel_ptr_wide<3>(kmax, small);
         case 4: return atax_kernel_ptr<4>(kmax, small);
+        case 5: return atax_kernel_ptr_wide<5>(kmax, small);
+        case 6: return atax_kernel_ptr_wide<6>(kmax, small);
+        case 7: return atax_kernel_ptr_wide<7>(kmax, small);
         case 8: return atax_kernel_ptr<8>(kmax, small);
         case 9: return atax_kernel_ptr<9>(kmax, small);
+        case 10: return atax_kernel_ptr_wide<10>(kmax, small);
         case 16: return atax_kernel_ptr<16>(kmax, small);
     }
     return nullptr;
@@ -154,18 +184,28 @@ int plan_atax(DeviceCtx &c, const double *A, const double *x, long M, long N, At
     int C = (int)g_tuning.atax_cluster;
     long cover = 0;
     if (C != 0) return plan_atax_cluster(c, C, M, N, p, &cover);
-    // smallest power-of-two cluster whose per-CTA slice fits 8 double2 per thread (4096 columns)
-    C = 1;
-    while (C < 16 && (N + C - 1) / C > 4096) C *= 2;
-    BTO_TRY(plan_atax_cluster(c, C, M, N, p, &cover));
-    if (C == 8 && p->fn) {
-        // Clusters live inside a GPC: on a B200 15 clusters of 8 fit (120 SMs) and 15 of 9 (135 SMs,
-        // profiles/r02/cluster_probe.log).  Same tile shape, an eighth more SMs pulling on HBM and
-        // an eighth more cycles per panel: take 9 when it covers more SMs.
-        AtaxPlan nine;
-        long cover9 = 0;
-        BTO_TRY(plan_atax_cluster(c, 9, M, N, &nine, &cover9));
-        if (nine.fn && nine.KMAX == p->KMAX && nine.RG == p->RG && cover9 * 9 > cover * 8) *p = nine;
+    // Every cluster size that is built, priced by what bounds the kernel (profiles/r02/atax_sustained.md):
+    // a panel of TR rows costs a fixed ~1150 cycles (the exchange chain) + ~62 per row and
+    // 512-column iteration, and a cluster works through M / clusters rows.  Slices close to the
+    // 4096-column maximum amortise the fixed part; clusters live inside a GPC, so their number
+    // depends on the size (profiles/r02/cluster_probe.log: 74 x 2, 45 x 3, 33 x 4, 26 x 5, 22 x 6,
+    // 15 x 7 / 8 / 9, 11 x 10, 7 x 16).  N = 24576: 6 CTAs x 4096 columns on 22 clusters instead of 9 x 2736
+    // on 15; N = 32768 stays at 9 (profiles/r02/atax_csize.log).
+    static const int kSizes[] = {1, 2, 3, 4, 5, 6, 7, 8, 9, 10, 16};
+    double best = 0.0;
+    for (int C : kSizes) {
+        AtaxPlan q;
+        long cover = 0;
+        BTO_TRY(plan_atax_cluster(c, C, M, N, &q, &cover));
+        if (!q.fn) continue;
+        if (q.KMAX == 16 && C < 16) continue;       // 8192-column slices: one-row panels and no registers to spare
+        const double panel = 1150.0 / q.RG + 62.5 * q.KMAX;            // cycles per row
+        const double cost = panel / (double)q.nclusters;
+        // (ties: more SMs pulling on HBM)
+        if (!p->fn || cost < best * 0.999 || (cost < best * 1.001 && q.nclusters * q.C > p->nclusters * p->C)) {
+            *p = q;
+            best = cost;
+        }
     }
     return BTO_OK;
 }
@@ -179,8 +219,13 @@ int plan_atax_cluster(DeviceCtx &c, int C, long M, long N, AtaxPlan *p, long *ma
     // a slice that starts off a 128-byte line costs the TMA stream ~7 % (C = 9 at N = 32768:
     // 3642 columns -> 6.76 TB/s for the copies alone, 3648 -> as good as C = 8)
     if (((W + 15) / 16) * 16 * (long)(C - 1) < N) W = ((W + 15) / 16) * 16;
-    int kmax = 1;
-    while ((long)kmax * 2 * kThreads < W) kmax *= 2;
+    int kmax = (int)((W + 2 * kThreads - 1) / (2 * kThreads));      // iterations of 512 columns a slice needs
+    const bool two_per_sm = g_tuning.atax_per_sm == 2;
+    if (kmax > 8 || two_per_sm) {                                   // 9 .. 16 and the two-per-SM variants: powers of two
+        int p2 = 1;
+        while (p2 < kmax) p2 *= 2;
+        kmax = p2;
+    }
     if (kmax > 16) return BTO_OK;
     if ((long)(C - 1) * W >= N && C > 1) return BTO_OK;   // a CTA would own no column
     const bool small = g_tuning.atax_rows == 1;     // 1: half-height panels

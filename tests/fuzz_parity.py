@@ -37,7 +37,7 @@ while time.time() < t_end:
                 grid_per_sm=rng.choice([0, 0, 1, 2, 4, 8]), mv_minb=rng.choice([0, 0, 1, 2, 4]),
                 skinny=rng.choice([1, 1, 0]), vec_unroll=rng.choice([1, 2, 4]), atax_fused=rng.choice([1, 1, 0]),
                 direct_cols=rng.choice([1, 1, 0]), midsize=rng.choice([1, 1, 0]), atax_per_sm=rng.choice([1, 1, 2]),
-                atax_cluster=rng.choice([0, 0, 0, 1, 2, 4, 8, 9]), rowstream=rng.choice([1, 1, 0, 2]))
+                atax_cluster=rng.choice([0, 0, 0, 1, 2, 3, 4, 5, 6, 7, 8, 9]), rowstream=rng.choice([1, 1, 0, 2]))
     _native.set_tuning(**tune)
     inputs = bto.random_inputs(g, ext, seed=cases)
     want = oracle.oracle_run(name, inputs, ext, threads=rng.choice([1, 4, 8]))

@@ -124,10 +124,11 @@ def test_every_tile_variant(bto_lib, oracle, rows, vec):
 
 
 ATAX_SHAPES = [(2048, 1024), (8, 2), (1, 4096), (100, 514), (333, 8192), (64, 16390),
-               (1000, 4098), (37, 32768), (5000, 1026), (257, 3586), (129, 28672), (75, 30000)]
+               (1000, 4098), (37, 32768), (5000, 1026), (257, 3586), (129, 28672), (75, 30000),
+               (50, 24576), (40, 12288), (33, 20480), (65, 1536), (70, 2600), (21, 40960), (19, 36000)]
 
 
-@pytest.mark.parametrize("cluster", [0, 1, 2, 4, 8, 9, 16])
+@pytest.mark.parametrize("cluster", [0, 1, 2, 3, 4, 5, 6, 7, 8, 9, 10, 16])
 def test_fused_atax_every_cluster_size(bto_lib, oracle, cluster):
     """Single-pass ATAX/BATAX (cluster-resident row panels, TMA ring, st.async
     exchange): every cluster size, ring depth and panel height must
