@@ -46,7 +46,7 @@ from pathlib import Path
 
 from .runtime import GeneratedKernel, ToolchainError
 
-__all__ = ["ir_from_matfuse", "emit_cuda", "NvccToolchain", "run_emitted", "DEFAULT_BLOCKS",
+__all__ = ["ir_from_matfuse", "emit_cuda", "emitted_kernel_for", "emitted_entry", "ir_for_spec", "NvccToolchain", "run_emitted", "DEFAULT_BLOCKS",
            "EMIT_VARIANTS", "time_emitted", "measure_empirical_ir", "OrganismTimer", "EmitModel", "estimate_cost_ir",
            "AnalyticOrganismCost"]
 
@@ -1577,6 +1577,75 @@ def time_emitted(binary, kernel: GeneratedKernel, ir: dict, dev_inputs: dict, ex
     if getattr(lib, kernel.kernel_name + "_last_cuda_error")():
         raise ToolchainError("emitted kernel failed while being timed")
     return best
+
+
+# ---------------------------------------------------------------------------
+# fused execution of specs outside the hand-written set (mixed orientations, non-corpus kernels)
+
+_EMITTED: dict = {}           # GeneratedKernel.source -> (shared object, emitted kernel, IR)
+NOMINAL_EXTENT = 4096         # organisms are ranked by the analytic model at this size (where it is fitted)
+
+
+def ir_for_spec(ref_graph, extents: dict | None = None, generations: int = 20, seed: int = 0) -> dict:
+    """Loop IR of the organism the REFERENCE's own search (MFGA, search.py:834) finds best for
+    `ref_graph` under the organism-level GPU cost model (`AnalyticOrganismCost`), max-fuse being one
+    of the candidates.  Needs the reference importable (it is, where this package is a drop-in)."""
+    from matfuse import SearchConfig, cached, contract_arrays, lower, max_fuse, run_strategy
+    names = tuple(ref_graph.extent_names)
+    # (a kernel of vectors only is priced at the element count of a NOMINAL_EXTENT-square matrix)
+    ext = extents or {e: (NOMINAL_EXTENT * NOMINAL_EXTENT if len(names) == 1 else NOMINAL_EXTENT) for e in names}
+    fitness = cached(AnalyticOrganismCost(ref_graph, ext))
+    best = max_fuse(ref_graph, 8)
+    best_cost = fitness(best).total
+    try:
+        res = run_strategy("mfga", ref_graph, SearchConfig(core_count=8, generations=generations, seed=seed), fitness)
+        if res.best is not None and res.best_fitness < best_cost:
+            best = res.best
+    except Exception:                               # a search that fails leaves max-fuse
+        pass
+    return ir_from_matfuse(contract_arrays(lower(best, ref_graph)))
+
+
+def emitted_kernel_for(graph, toolchain: "NvccToolchain | None" = None, ir: dict | None = None):
+    """A FUSED kernel for a spec the hand-written sequences do not cover: the reference lowers the
+    organism its search picks (`ir_for_spec`), `emit_cuda` prints it, nvcc compiles it once (cached
+    by source hash).  `graph`: this package's TypedSpec / KernelSpec or the reference's
+    DataflowGraph.  Returns a GeneratedKernel whose `source` is "emitted:<shared object>", or None
+    when the reference or nvcc is not available (the caller falls back to the unfused executor).
+    `ir`: a stored snapshot instead of the search (machines without the reference)."""
+    import tempfile
+    tc = toolchain or NvccToolchain(cache_dir=os.environ.get("BTO_NVCC_CACHE") or
+                                    str(Path(tempfile.gettempdir()) / "bto_b200_emit"))
+    if not tc.available:
+        return None
+    if ir is None:
+        try:
+            import matfuse                              # noqa: F401
+            from matfuse.graph import build_dataflow, infer_types
+        except ImportError:
+            return None
+        if hasattr(graph, "data") and hasattr(graph, "ops"):
+            ref_graph = graph                           # the reference's own DataflowGraph
+        else:
+            from .spec import format_kernel
+            spec = graph.spec if hasattr(graph, "spec") else graph
+            ref_graph = infer_types(build_dataflow(matfuse.parse_kernel(format_kernel(spec))))
+        ir = ir_for_spec(ref_graph)
+    kernel = emit_cuda(ir)
+    work = Path(tempfile.mkdtemp(prefix="bto-emit-"))
+    path = tc.compile(kernel.source, work, name=kernel.kernel_name)
+    handle = GeneratedKernel(source=f"emitted:{path}", kernel_name=kernel.kernel_name, params=kernel.params,
+                             organism_key=kernel.organism_key, threads=kernel.threads)
+    _EMITTED[handle.source] = (path, kernel, ir)
+    return handle
+
+
+def emitted_entry(source: str):
+    """(shared object, emitted kernel, IR) behind an "emitted:..." handle."""
+    try:
+        return _EMITTED[source]
+    except KeyError:
+        raise ToolchainError(f"{source} was not produced by emitted_kernel_for in this process") from None
 
 
 # ---------------------------------------------------------------------------

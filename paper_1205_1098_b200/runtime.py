@@ -97,12 +97,15 @@ def _c_params(inputs, outputs, extent_names) -> tuple[tuple[str, str], ...]:
     return tuple(out)
 
 
-def gpu_kernel(graph, allow_generic: bool = True) -> GeneratedKernel:
+def gpu_kernel(graph, allow_generic: bool = True, allow_emitted: bool = True) -> GeneratedKernel:
     """The kernel handle for `graph`'s spec: the hand-written fused sm_100a
-    sequence when the spec is one of the corpus structures, otherwise (unless
-    `allow_generic=False`, which raises UnsupportedKernelError) the generic
-    unfused executor of generic.py -- the analogue of the reference compiling
-    ANY valid spec, with the unfused organism."""
+    sequence when the spec is one of the corpus structures (row-major, or all
+    column-major); otherwise -- mixed orientations, kernels outside the corpus --
+    FUSED CUDA emitted for the organism the reference's search picks under the
+    GPU cost model (`cuemit.emitted_kernel_for`: needs the reference and nvcc,
+    i.e. the drop-in setting; the reference emits fused C for any spec,
+    cemit.py:54-72); failing that (unless `allow_generic=False`, which raises
+    UnsupportedKernelError) the generic unfused executor of generic.py."""
     from .spec import UnsupportedKernelError
     typed = _as_typed(graph) if not hasattr(graph, "data") else None
     spec = typed.spec if typed is not None else graph.spec
@@ -117,6 +120,14 @@ def gpu_kernel(graph, allow_generic: bool = True) -> GeneratedKernel:
                     source=f"libbto_b200:colmajor:{cm}", kernel_name=spec.name.lower(),
                     params=_c_params(spec.inputs, spec.outputs, typed.extent_names),
                     organism_key="colmajor " + _SEQUENCES[cm])
+            if allow_emitted:
+                from .cuemit import emitted_kernel_for
+                try:
+                    emitted = emitted_kernel_for(typed)
+                except ToolchainError:
+                    emitted = None
+                if emitted is not None:
+                    return emitted
             if not allow_generic:
                 raise
             return GeneratedKernel(
@@ -267,6 +278,10 @@ def run_kernel(binary, kernel: GeneratedKernel, graph, inputs: dict,
     if kernel.source.endswith(":generic"):
         from .generic import run_generic
         return run_generic(_as_typed(graph), inputs, extents)
+    if kernel.source.startswith("emitted:"):
+        from .cuemit import emitted_entry, run_emitted
+        path, emitted, ir = emitted_entry(kernel.source)
+        return run_emitted(path, emitted, ir, inputs, extents)
     if ":colmajor:" in kernel.source:
         from .colmajor import run_colmajor
         return run_colmajor(kernel.source.rsplit(":", 1)[1], _as_typed(graph), inputs, extents)

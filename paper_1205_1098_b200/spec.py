@@ -212,6 +212,24 @@ def _names_in(expr) -> list[str]:
     return _names_in(expr[1]) + _names_in(expr[2])
 
 
+def format_expr(e) -> str:
+    if e[0] == "var":
+        return e[1]
+    if e[0] == "t":
+        inner = format_expr(e[1])
+        return f"{inner}'" if e[1][0] == "var" else f"({inner})'"
+    return f"({format_expr(e[1])} {e[0]} {format_expr(e[2])})"
+
+
+def format_kernel(spec: KernelSpec) -> str:
+    """`.bto` text of a spec (fully parenthesised): `parse_kernel(format_kernel(s)) == s`, and the
+    reference's parser reads it too (lang.py:337)."""
+    ins = ", ".join(f"{n} : {d}" for n, d in spec.inputs)
+    outs = ", ".join(f"{n} : {d}" for n, d in spec.outputs)
+    body = "  ".join(f"{t} = {format_expr(e)}" for t, e in spec.statements)
+    return f"{spec.name} in: {ins} out: {outs} {{ {body} }}"
+
+
 def parse_kernel(text: str) -> KernelSpec:
     """Parse `.bto` text; same accept/reject behaviour as lang.py:337-344."""
     spec = _Reader(text).kernel()

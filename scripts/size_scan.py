@@ -17,15 +17,16 @@ torch.cuda.set_device(0)
 lib = _native.load()
 ops = GpuShardOps()
 rows = []
-for n in (512, 1024, 2048, 4096, 8192, 16384):
+SIZES = tuple(int(a) for a in sys.argv[1:]) or (512, 1024, 2048, 4096, 8192, 16384)
+for n in SIZES:
     A = torch.rand(n, n, dtype=torch.float64, device="cuda")
     B = torch.rand(n, n, dtype=torch.float64, device="cuda")
     v = [torch.rand(n, dtype=torch.float64, device="cuda") for _ in range(8)]
     o = [torch.empty(n, dtype=torch.float64, device="cuda") for _ in range(3)]
-    big = torch.rand(4, n * n, dtype=torch.float64, device="cuda")
+    big = torch.rand(4, min(n * n, 1 << 27), dtype=torch.float64, device="cuda")
     beta = torch.empty(1, dtype=torch.float64, device="cuda")
     calls = {
-        "axpydot": (lambda: ops.axpydot(big[0], big[1], big[2], 0.3, big[3], beta), 32.0 * n * n),
+        "axpydot": (lambda: ops.axpydot(big[0], big[1], big[2], 0.3, big[3], beta), 32.0 * big.shape[1]),
         "bicgk": (lambda: ops.bicgk(A, v[0], v[1], o[0], o[1]), 8.0 * n * n),
         "atax": (lambda: ops.atax(A, v[0], o[0]), 8.0 * n * n),
         "gesummv": (lambda: ops.gesummv(0.5, 0.25, A, B, v[0], o[0]), 16.0 * n * n),
