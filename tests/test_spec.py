@@ -55,8 +55,8 @@ def test_unknown_structure_gets_the_generic_executor_or_a_loud_error():
     text = "T in: a : vector(column), b : vector(column) out: c : vector(column) { c = a - b }"
     typed = S.infer_shapes(S.parse_kernel(text))
     with pytest.raises(S.UnsupportedKernelError):
-        bto.gpu_kernel(typed, allow_generic=False)
-    k = bto.gpu_kernel(typed)
+        bto.gpu_kernel(typed, allow_generic=False, allow_emitted=False)
+    k = bto.gpu_kernel(typed, allow_emitted=False)      # (with the reference + nvcc: fused emitted code)
     assert k.source == "libbto_b200:generic" and k.kernel_name == "t"
     assert k.organism_key == "gpu-unfused{1}"
 
