@@ -552,8 +552,6 @@ class _Emitter:
         v = next(iter(axes))
         if v == root["axis"]:
             return None
-        for it in self._all_stmts(root["body"]):
-            pass
         # uniform statements (outside strided loops) must not read or write v-indexed storage
         def uniform_ok(its, in_lane) -> bool:
             for it in its:
