@@ -22,7 +22,7 @@
 //            order (t_i, identical bits in all CTAs), then y[j] += A[i,j] * t_i
 //            from the tile it still holds in REGISTERS; column sums live in
 //            registers for the whole kernel.
-// Thread 0 issues the TMA copies: phase 1 ends with a CTA barrier after every
+// One thread (of warp 1) issues the TMA copies: phase 1 ends with a CTA barrier after every
 // warp has its part of the tile in registers, so right after that barrier the
 // stage is free and is refilled with the panel S steps ahead (no "empty"
 // mbarrier, and no extra warp -- a ninth warp would cap the kernel at 168
@@ -57,7 +57,8 @@ constexpr int kAtaxMaxCluster = 16;      // sizes built: 1 .. 9 and 16 (9: 15 cl
 constexpr int kAtaxMaxRows = 8;
 constexpr int kAtaxMaxStages = 8;
 constexpr int kAtaxSlots = 8;                      // exchange slots; phase 1 runs one panel ahead, needs > 3
-constexpr int kAtaxThreads = kThreads;             // 8 warps; thread 0 also issues the TMA copies
+constexpr int kAtaxThreads = kThreads;             // 8 warps; one thread of warp 1 also issues the TMA copies
+constexpr int kIssuer = 32;                        // ... this one (warp 0 pushes the exchange partials)
 
 __device__ __forceinline__ uint32_t smem_u32(const void *p)
 {
@@ -142,6 +143,14 @@ __device__ __forceinline__ void st_async_cluster(double *local, uint64_t *local_
                  : "memory");
 }
 
+// the same with the remote addresses already mapped (mapa once per kernel, not once per store)
+__device__ __forceinline__ void st_async_remote(uint32_t raddr, uint32_t rbar, double v)
+{
+    asm volatile("st.async.weak.shared::cluster.mbarrier::complete_tx::bytes.f64 [%0], %1, [%2];"
+                 ::"r"(raddr), "d"(v), "r"(rbar)
+                 : "memory");
+}
+
 __device__ __forceinline__ uint32_t cluster_rank()
 {
     uint32_t r;
@@ -201,7 +210,11 @@ __device__ __forceinline__ double tree_sum(const double *v)
 // the iterations every thread has (-5 %: the predicated schedule interleaves loads and FMAs better),
 // warps without tail columns skipping the last iteration behind warp-uniform branches (-10 %), and
 // a split CTA barrier where only warp 0 waits (-15 %: the other warps then poll the exchange
-// mbarrier while warp 0 is still pushing).
+// mbarrier while warp 0 is still pushing).  What did help (+4 % alone, +6.7 % in the power-capped
+// suite: 6.74 -> 7.19 TB/s): issuing the refill copies from warp 1 -- the stall samples sit on
+// the waits for the PEERS' partials (14 % vs 2 % on the waits for the copies), and warp 0's pushes
+// used to queue behind thread 0's refill code.  One lane per (row, peer) instead of one per peer
+// with a loop over the rows: no further change.
 template <int C, int KMAX, int TR, int MINB = 1>
 __global__ void __launch_bounds__(kAtaxThreads, MINB)
 atax_cluster_kernel(const AtaxArgs a)
@@ -241,7 +254,7 @@ atax_cluster_kernel(const AtaxArgs a)
         cluster_wait();
     }
 
-    // thread 0: fill stage g % S with panel g
+    // the issuer thread: fill stage g % S with panel g
     auto issue = [&](int g) {
         if (wlen <= 0) return;
         const int s = g % S;
@@ -254,8 +267,16 @@ atax_cluster_kernel(const AtaxArgs a)
             bulk_load(dst + (size_t)r * W, a.A + (r0 + r) * N + c0, seg, &full[s]);
         }
     };
-    if (tid == 0) {
+    if (tid == kIssuer) {
         for (int g = 0; g < S && g < ngroups; ++g) issue(g);
+    }
+    // where thread p < C pushes: this CTA's column of CTA p's `part`, and CTA p's exchange barriers
+    uint32_t peer_part = 0, peer_bar = 0;
+    if (C > 1 && tid < C) {
+        asm volatile("mapa.shared::cluster.u32 %0, %1, %2;"
+                     : "=r"(peer_part) : "r"(smem_u32(&part[0][0][rank])), "r"((uint32_t)tid));
+        asm volatile("mapa.shared::cluster.u32 %0, %1, %2;"
+                     : "=r"(peer_bar) : "r"(smem_u32(&pbar[0])), "r"((uint32_t)tid));
     }
 
     {
@@ -311,8 +332,10 @@ atax_cluster_kernel(const AtaxArgs a)
             if ((lane % (32 / TR)) == 0) warp_part[par][lane / (32 / TR)][warp] = d[0];
             __syncthreads();
             // every warp holds its part of the tile in registers (the FMAs above
-            // consumed the loads): the stage is free, refill it S panels ahead
-            if (tid == 0 && g + S < ngroups) issue(g + S);
+            // consumed the loads): the stage is free, refill it S panels ahead.  The copies are
+            // issued from warp 1 so that warp 0's pushes -- which every CTA of the cluster is
+            // waiting for -- do not queue behind the address arithmetic of the refill.
+            if (tid == kIssuer && g + S < ngroups) issue(g + S);
             if (tid < C) {
                 // thread p serves peer p: the same 8-warp sum in every thread (same bits)
                 if (C > 1 && tid == 0) mbar_expect_tx(&pbar[slot], (uint32_t)(C * nr * 8));
@@ -320,8 +343,12 @@ atax_cluster_kernel(const AtaxArgs a)
                     const double *wp = warp_part[par][r];      // fixed pairwise tree
                     const double sum = ((wp[0] + wp[1]) + (wp[2] + wp[3])) +
                                        ((wp[4] + wp[5]) + (wp[6] + wp[7]));
-                    if (C > 1) st_async_cluster(&part[slot][r][rank], &pbar[slot], (uint32_t)tid, sum);
-                    else part[slot][r][0] = sum;
+                    if (C > 1) {
+                        st_async_remote(peer_part + (uint32_t)((slot * TR + r) * CP * 8),
+                                        peer_bar + (uint32_t)(slot * 8), sum);
+                    } else {
+                        part[slot][r][0] = sum;
+                    }
                 }
                 if (C == 1) mbar_arrive(&pbar[slot]);
             }
