@@ -60,16 +60,7 @@ constexpr int kAtaxSlots = 8;                      // exchange slots; phase 1 ru
 constexpr int kAtaxThreads = kThreads;             // 8 warps; one thread of warp 1 also issues the TMA copies
 constexpr int kIssuer = 32;                        // ... this one (warp 0 pushes the exchange partials)
 
-__device__ __forceinline__ uint32_t smem_u32(const void *p)
-{
-    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
-}
 
-__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count)
-{
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count)
-                 : "memory");
-}
 
 __device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes)
 {
@@ -78,20 +69,6 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes)
                  : "memory");
 }
 
-__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity)
-{
-    asm volatile(
-        "{\n"
-        ".reg .pred p;\n"
-        "WAIT_%=:\n"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
-        "@p bra DONE_%=;\n"
-        "bra WAIT_%=;\n"
-        "DONE_%=:\n"
-        "}\n" ::"r"(smem_u32(bar)),
-        "r"(parity)
-        : "memory");
-}
 
 // TMA 1-D bulk copy global -> shared, completion counted in bytes on `bar`
 // BTO_TMA_POLICY: 0 = no L2 hint, 1 = evict_first, 2 = evict_last, 3 = evict_normal (explicit)
@@ -122,10 +99,6 @@ __device__ __forceinline__ void bulk_load(void *dst, const void *src, uint32_t b
 #endif
 }
 
-__device__ __forceinline__ void mbar_arrive(uint64_t *bar)
-{
-    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
-}
 
 // Asynchronous remote store: write `v` into the same-named shared variable of
 // CTA `rank` and count 8 bytes on that CTA's mbarrier when the data has landed.
