@@ -1171,7 +1171,9 @@ class _Emitter:
                     uses_smem = True                     # (sms_ is read from the device below)
                     for name, sp in self.row_accs.items():
                         e0 = self.st[name]["extents"][0]
-                        out.append(f"cudaMallocAsync(&{sp}, sizeof(double) * (size_t)strips{regions}_ * {self.threads // 32} * (size_t){e0}, 0);")
+                        out.append(f"{{ const size_t need_ = sizeof(double) * (size_t)strips{regions}_ * {self.threads // 32} * (size_t){e0}; "
+                                   f"if (need_ > {sp}_n_) {{ if ({sp}_c_) cudaFreeAsync({sp}_c_, 0); cudaMallocAsync(&{sp}_c_, need_, 0); {sp}_n_ = need_; }} "
+                                   f"{sp} = {sp}_c_; }}")
                 if cluster_axis:
                     # the cluster's C CTAs split the strided axis: strip c = [c sw, (c + 1) sw)
                     strip_ext = next(l["extent"] for l in self._lane_loops(root["body"]))
@@ -1301,7 +1303,6 @@ class _Emitter:
                     w.close()
                     w.put()
                     out.append(f"{jname}<<<(unsigned)(({e0} + 255) / 256), 256, 0, 0>>>({call}, strips{regions}_ * {self.threads // 32});")
-                    out.append(f"cudaFreeAsync({sp}, 0);")
                 self.row_accs = {}
                 self.promoted = {}
                 self.jam, self.unroll, self.threads, self.minb, self.bypass_l1 = saved
@@ -1374,15 +1375,35 @@ class _Emitter:
             w.put("cudaMemPoolSetAttribute(pool_, cudaMemPoolAttrReleaseThreshold, &keep_);")
             w.put("pool_ready_ = true;")
             w.close()
+        cached = self.optimize and (temps or sp_buffers)
+        if cached:
+            # Temporaries and partial buffers are kept from call to call, per HOST THREAD and device,
+            # and only ever grow: no allocation on the steady-state path (the reference mallocs and
+            # frees per call, cemit.py:183-202; two calls from two threads still get buffers of their
+            # own, so "thread-safe per output buffer", holds).  Launches are on stream 0,
+            # so the next call's kernels are ordered after this call's.
+            w.put("static thread_local int cache_dev_ = -1;")
+            w.put("int dev_now_ = 0; cudaGetDevice(&dev_now_);")
+            names = [n for n, _ in temps] + list(sp_buffers)
+            for n in names:
+                w.put(f"static thread_local double *{n}_c_ = nullptr; static thread_local size_t {n}_n_ = 0;")
+            w.put("if (dev_now_ != cache_dev_) { " + " ".join(f"{n}_c_ = nullptr; {n}_n_ = 0;" for n in names)
+                  + " cache_dev_ = dev_now_; }")
         for name, size in temps:
-            w.put(f"double *{name} = nullptr;")
-            w.put(f"cudaMallocAsync(&{name}, sizeof(double) * ({size}), 0);")
+            if cached:
+                w.put(f"{{ const size_t need_ = sizeof(double) * ({size}); if (need_ > {name}_n_) {{ "
+                      f"if ({name}_c_) cudaFreeAsync({name}_c_, 0); cudaMallocAsync(&{name}_c_, need_, 0); {name}_n_ = need_; }} }}")
+                w.put(f"double *{name} = {name}_c_;")
+            else:
+                w.put(f"double *{name} = nullptr;")
+                w.put(f"cudaMallocAsync(&{name}, sizeof(double) * ({size}), 0);")
         for sp in sp_buffers:
             w.put(f"double *{sp} = nullptr;")
         for stmt in launches:
             w.put(stmt)
-        for name, _ in temps:      # stream-ordered pool: no device-wide sync per temporary
-            w.put(f"cudaFreeAsync({name}, 0);")
+        if not cached:
+            for name, _ in temps:      # stream-ordered pool: no device-wide sync per temporary
+                w.put(f"cudaFreeAsync({name}, 0);")
         if self.sync or not self.optimize:
             w.put("cudaStreamSynchronize(0);")       # the reference's protocol: results ready on return
         # (default: stream-ordered like the library's own device-pointer entry points -- operands
