@@ -345,7 +345,9 @@ __device__ __forceinline__ void mv_tile_walk(const MvArgs &a, const ColEpilogue 
             // its __syncthreads orders this unit's reads before buf is reused.
             // (Round 2 replaced this barrier by an mbarrier hand-off -- producers arrive, only the
             //  consumer warp waits, the rest go on to the next unit's loads: BiCGK 7.07 -> 6.96 TB/s,
-            //  GEMVER 6.61 -> 6.58, profiles/r02/ab/ab_mv_handoff.log.  The barrier stays.)
+            //  GEMVER 6.61 -> 6.58, profiles/r02/ab/ab_mv_handoff.log.  The barrier stays.  Dealing the
+            //  8-warp sums to all warps instead of warp 0's first threads: BiCGK 7.07 -> 7.00,
+            //  ab_mv_spread.log.)
             buf ^= 1;
         }
     }
