@@ -1602,6 +1602,7 @@ def time_emitted(binary, kernel: GeneratedKernel, ir: dict, dev_inputs: dict, ex
 # fused execution of specs outside the hand-written set (mixed orientations, non-corpus kernels)
 
 _EMITTED: dict = {}           # GeneratedKernel.source -> (shared object, emitted kernel, IR)
+_EMITTED_BY_SPEC: dict = {}   # .bto text -> handle (the search and the compile run once per spec and process)
 NOMINAL_EXTENT = 4096         # organisms are ranked by the analytic model at this size (where it is fitted)
 
 
@@ -1637,6 +1638,12 @@ def emitted_kernel_for(graph, toolchain: "NvccToolchain | None" = None, ir: dict
                                     str(Path(tempfile.gettempdir()) / "bto_b200_emit"))
     if not tc.available:
         return None
+    memo_key = None
+    if ir is None and toolchain is None and not (hasattr(graph, "data") and hasattr(graph, "ops")):
+        from .spec import format_kernel
+        memo_key = format_kernel(graph.spec if hasattr(graph, "spec") else graph)
+        if memo_key in _EMITTED_BY_SPEC:
+            return _EMITTED_BY_SPEC[memo_key]
     if ir is None:
         try:
             import matfuse                              # noqa: F401
@@ -1656,6 +1663,8 @@ def emitted_kernel_for(graph, toolchain: "NvccToolchain | None" = None, ir: dict
     handle = GeneratedKernel(source=f"emitted:{path}", kernel_name=kernel.kernel_name, params=kernel.params,
                              organism_key=kernel.organism_key, threads=kernel.threads)
     _EMITTED[handle.source] = (path, kernel, ir)
+    if memo_key is not None:
+        _EMITTED_BY_SPEC[memo_key] = handle
     return handle
 
 
