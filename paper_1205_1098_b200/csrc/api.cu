@@ -678,6 +678,32 @@ int bto_reserve_workspace(bto_stream_t stream, long bytes)
     return reserve_ws(*ac.ctx, st, (size_t)bytes);
 }
 
+// Testing hook: every SM's shared memory := the all-ones pattern (a NaN as a double, -1 as an int).
+// A kernel that reads a shared-memory word nobody wrote in ITS launch -- and multiplies it by a zero
+// it took for harmless -- then fails loudly instead of depending on what ran before it.
+__global__ void __launch_bounds__(1024) poison_shared_kernel(int words)
+{
+    extern __shared__ unsigned long long poison_words[];
+    for (int i = threadIdx.x; i < words; i += blockDim.x) poison_words[i] = ~0ULL;
+    __syncthreads();
+    if (poison_words[(threadIdx.x * 2654435761u) % (unsigned)words] != ~0ULL) __trap();   // keeps the stores alive
+}
+
+int bto_debug_poison_shared_memory(bto_stream_t stream)
+{
+    ASYNC_PROLOGUE();
+    static bool configured = false;
+    const int bytes = 227 * 1024;
+    if (!configured) {
+        CUDA_TRY(cudaFuncSetAttribute(poison_shared_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+        configured = true;
+    }
+    // one CTA owns a whole SM's shared memory; several waves so that every SM gets (at least) one
+    poison_shared_kernel<<<ac.ctx->sm_count * 4, 1024, bytes, st>>>(bytes / 8);
+    CUDA_TRY(cudaGetLastError());
+    return BTO_OK;
+}
+
 int bto_fill_host(double *host_dst, long count, double value)
 {
     if (count < 0 || (count > 0 && !host_dst)) return fail(BTO_ERR_INVALID, "fill_host: bad argument");

@@ -310,9 +310,16 @@ atax_cluster_kernel(const AtaxArgs a)
             // waiting for -- do not queue behind the address arithmetic of the refill.
             if (tid == kIssuer && g + S < ngroups) issue(g + S);
             if (tid < C) {
-                // thread p serves peer p: the same 8-warp sum in every thread (same bits)
-                if (C > 1 && tid == 0) mbar_expect_tx(&pbar[slot], (uint32_t)(C * nr * 8));
-                for (int r = 0; r < nr; ++r) {
+                // thread p serves peer p: the same 8-warp sum in every thread (same bits).
+                // ALL TR rows are pushed, also those past the end of the row range (their tiles are
+                // zeros, so their sums are exact zeros): phase 2 multiplies every row's t with its
+                // tile, and 0 x t is only 0 if t is a number -- an entry of `part` that nobody wrote
+                // in this launch is whatever the previous kernel left in shared memory, NaN bit
+                // patterns included (round-2 fuzz: one BATAX result in 37 000 with 960 NaN columns,
+                // the slice of one CTA; scripts/batax_rare_probe.py).
+                if (C > 1 && tid == 0) mbar_expect_tx(&pbar[slot], (uint32_t)(C * TR * 8));
+#pragma unroll
+                for (int r = 0; r < TR; ++r) {
                     const double *wp = warp_part[par][r];      // fixed pairwise tree
                     const double sum = ((wp[0] + wp[1]) + (wp[2] + wp[3])) +
                                        ((wp[4] + wp[5]) + (wp[6] + wp[7]));

@@ -16,7 +16,7 @@ import numpy as np
 import pytest
 
 import paper_1205_1098_b200 as bto
-from paper_1205_1098_b200 import cuemit
+from paper_1205_1098_b200 import _native, cuemit
 
 IRS = json.loads((Path(__file__).parent / "golden" / "organisms.json").read_text())
 ELEMENTWISE = {"axpydot": ("z",), "gemver": ("B",), "vadd": ("x",), "waxpby": ("w",)}
@@ -176,6 +176,7 @@ def test_every_organism_matches_the_oracle(bto_lib, oracle, tmp_path, name, opti
             ext = {"M": m * n} if typed.extent_names == ("M",) else {"M": m, "N": n}
             inputs = bto.random_inputs(typed, ext, seed=idx)
             want = oracle.oracle_run(name, inputs, ext, threads=8)
+            _native.poison_shared_memory()      # emitted kernels too must write what they read
             got = cuemit.run_emitted(path, kernel, ir, inputs, ext)
             for out in want:
                 assert not np.any(np.isnan(np.asarray(got[out]))), (name, ir["organism"], ext, out)
@@ -208,6 +209,7 @@ def test_cluster_mode_matches_the_oracle(bto_lib, oracle, tmp_path, cluster, jam
             ext = {"M": m, "N": n}
             inputs = bto.random_inputs(typed, ext, seed=idx + m)
             want = oracle.oracle_run(name, inputs, ext, threads=8)
+            _native.poison_shared_memory()
             got = cuemit.run_emitted(path, kernel, ir, inputs, ext)
             for out in want:
                 assert not np.any(np.isnan(np.asarray(got[out]))), (name, ir["organism"], ext, out)

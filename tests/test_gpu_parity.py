@@ -152,6 +152,56 @@ def test_fused_atax_every_cluster_size(bto_lib, oracle, cluster):
         _native.set_tuning(atax_fused=1, atax_cluster=0, atax_stages=0, atax_rows=0, atax_per_sm=1)
 
 
+def test_no_kernel_depends_on_shared_memory_it_did_not_write(bto_lib, oracle):
+    """Shared memory keeps what the previous kernel left in it.  Before every call here all of it is
+    filled with NaN bit patterns (`bto_debug_poison_shared_memory`); ragged shapes -- row counts
+    that leave the last panel / unit / tile short, column counts that leave slices and strips
+    short -- must still give the oracle's result.  (Round 2: the single-pass ATAX multiplied the
+    zero tile of a missing row with an exchange partial nobody had pushed: 0 x NaN, one result in
+    37 000 fuzz cases; it now pushes all rows of a panel.)"""
+    shapes = [(633, 8502), (21, 8502), (5, 4098), (1, 16390), (1031, 514), (37, 2050), (7, 50), (3, 70000),
+              (257, 3586), (9, 24578), (13, 1026)]
+    try:
+        for name in KERNELS:
+            graph = bto.load_graph(name)
+            for (m, n) in shapes:
+                ext = {"M": m * 3 + 1} if graph.extent_names == ("M",) else {"M": m, "N": n}
+                inputs = bto.gen_inputs(graph, ext, seed=m + n)
+                want = oracle.oracle_run(name, inputs, ext, threads=8)
+                variants = [dict()]
+                if name in ("atax", "batax"):
+                    variants = [dict(atax_cluster=c, atax_per_sm=p, atax_rows=r)
+                                for c in (0, 1, 2, 4, 8, 9, 16) for p in (1, 2) for r in (0, 1) if not (p == 2 and (c == 16 or r == 1))]
+                for tune in variants:
+                    _native.set_tuning(**tune)
+                    _native.poison_shared_memory()
+                    assert_matches(name, run_device(name, inputs, ext), want, ext, f"poisoned {tune}")
+    finally:
+        _native.set_tuning(atax_cluster=0, atax_per_sm=1, atax_rows=0)
+
+
+def test_atax_cluster_size_follows_the_slice_width(bto_lib):
+    """The plan prices every built cluster size by the per-panel chain (host_sequences.cuh::plan_atax):
+    rows whose length divides into full 4096-column slices get the cluster that makes them --
+    24576 = 6 x 4096, 20480 = 5 x 4096, 40960 = 10 x 4096 -- and the bench size keeps 9; results
+    are checked against cuBLAS-free closed forms (a rank-1 matrix)."""
+    import torch
+    for n, want in ((32768, "atax_cluster_kernel<9,8,2,1>"), (24576, "atax_cluster_kernel<6,8,2,1>"),
+                    (20480, "atax_cluster_kernel<5,8,2,1>"), (40960, "atax_cluster_kernel<10,8,2,1>"),
+                    (12288, "atax_cluster_kernel<3,8,2,1>"), (8192, "atax_cluster_kernel<2,8,2,1>")):
+        m = 600
+        u = torch.linspace(0.5, 1.5, m, dtype=torch.float64, device="cuda")
+        v = torch.linspace(-1.0, 1.0, n, dtype=torch.float64, device="cuda")
+        A = torch.outer(u, v).contiguous()                         # A = u v'
+        x = torch.full((n,), 0.25, dtype=torch.float64, device="cuda")
+        got = bto.run_kernel(bto.library_path(), bto.gpu_kernel(bto.load_graph("atax")), bto.load_graph("atax"),
+                             {"A": A, "x": x}, {"M": m, "N": n})["y"]
+        plan = _native.launch_plan()
+        assert plan.startswith(want), (n, plan)
+        expect = v * (float(u @ u) * float(v @ x))                 # A'(A x) = v (u'u)(v'x)
+        assert float((got - expect).abs().max()) <= 1e-12 * math.log2(n) * max(1.0, float(expect.abs().max())), n
+
+
 def test_two_pass_atax_fallback(bto_lib, oracle):
     """Odd N (rows not 16-byte aligned) and atax_fused=0 take the two-pass path."""
     try:
