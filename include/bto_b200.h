@@ -275,6 +275,9 @@ int   bto_copy_to_host(void *host_dst, const void *device_src, long bytes);
  * `stream`.  The library's kernels must not depend on shared memory they did not write in their own
  * launch; the GPU tests call this before ragged-shape runs to make such a read loud.            */
 int   bto_debug_poison_shared_memory(bto_stream_t stream);
+/* Testing hook: `stream`'s partial-sum workspace := NaN patterns (stream-ordered), so that a join
+ * reading a partial nobody produced in the same call is loud.                                    */
+int   bto_debug_poison_workspace(bto_stream_t stream);
 /* host_dst[0 .. count) = value with the copy threads (first touch of fresh pages in
  * parallel: the NaN prefill of a large output, runtime.py:99-150, at 30+ GB/s).   */
 int   bto_fill_host(double *host_dst, long count, double value);

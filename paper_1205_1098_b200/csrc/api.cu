@@ -704,6 +704,18 @@ int bto_debug_poison_shared_memory(bto_stream_t stream)
     return BTO_OK;
 }
 
+// Testing hook: `stream`'s partial-sum workspace := NaN patterns (stream-ordered).  A join that
+// reads a partial no producer wrote in the same call then fails loudly instead of meeting the
+// finite leftovers of an earlier call.  (The ticket counters are left alone: they are zero between kernels.)
+int bto_debug_poison_workspace(bto_stream_t stream)
+{
+    ASYNC_PROLOGUE();
+    StreamWs *w = nullptr;
+    BTO_TRY(bind_stream(*ac.ctx, st, &w));
+    if (w->cur.ptr && w->cur.bytes) CUDA_TRY(cudaMemsetAsync(w->cur.ptr, 0xFF, w->cur.bytes, st));
+    return BTO_OK;
+}
+
 int bto_fill_host(double *host_dst, long count, double value)
 {
     if (count < 0 || (count > 0 && !host_dst)) return fail(BTO_ERR_INVALID, "fill_host: bad argument");

@@ -45,6 +45,7 @@ while time.time() < t_end:
     _native.set_tuning(**tune)
     if rng.random() < 0.5:
         _native.poison_shared_memory()      # NaN patterns in every SM's shared memory before the call
+        _native.poison_workspace()          # ... and in the partial-sum workspace
     inputs = bto.random_inputs(g, ext, seed=cases)
     want = oracle.oracle_run(name, inputs, ext, threads=rng.choice([1, 4, 8]))
     host = rng.random() < 0.3

@@ -160,7 +160,7 @@ def test_no_kernel_depends_on_shared_memory_it_did_not_write(bto_lib, oracle):
     zero tile of a missing row with an exchange partial nobody had pushed: 0 x NaN, one result in
     37 000 fuzz cases; it now pushes all rows of a panel.)"""
     shapes = [(633, 8502), (21, 8502), (5, 4098), (1, 16390), (1031, 514), (37, 2050), (7, 50), (3, 70000),
-              (257, 3586), (9, 24578), (13, 1026)]
+              (257, 3586), (9, 24578), (13, 1026), (1001, 33), (77, 300), (600, 5000)]
     try:
         for name in KERNELS:
             graph = bto.load_graph(name)
@@ -175,6 +175,7 @@ def test_no_kernel_depends_on_shared_memory_it_did_not_write(bto_lib, oracle):
                 for tune in variants:
                     _native.set_tuning(**tune)
                     _native.poison_shared_memory()
+                    _native.poison_workspace()      # ... nor on partials no producer wrote in this call
                     assert_matches(name, run_device(name, inputs, ext), want, ext, f"poisoned {tune}")
     finally:
         _native.set_tuning(atax_cluster=0, atax_per_sm=1, atax_rows=0)
