@@ -954,6 +954,8 @@ def test_join_fused_exchange_emulated_ranks(bto_lib, oracle, world, shape):
                 _native.set_tuning(exchange_phases=phase)
                 for r, (o, call) in enumerate(outs):
                     _native.check(lib.bto_exchange_init(r, world, exch_ptrs, flag_ptrs, capacity, epoch))
+                    _native.poison_shared_memory()      # (a rank's kernels read only what they wrote)
+                    _native.poison_workspace()
                     call()
                     torch.cuda.synchronize()
                     done = ctypes.c_uint(0)
