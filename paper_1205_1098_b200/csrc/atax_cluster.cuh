@@ -51,9 +51,9 @@ struct AtaxArgs {
     int nclusters;
 };
 
-constexpr int kAtaxMaxCluster = 16;      // sizes built: 1 .. 9 and 16 (9: 15 clusters = 135 SMs on a B200
+constexpr int kAtaxMaxCluster = 16;      // sizes built: 1 .. 10 and 16 (9: 15 clusters = 135 SMs on a B200
                                          // where 8 gives 15 x 8 = 120; 3, 5, 6, 7: full-width slices for
-                                         // mid-size matrices, profiles/r02/cluster_probe.log)
+                                         // mid-size matrices, 10 for rows of 36865 .. 40960 columns; profiles/r02/cluster_probe.log)
 constexpr int kAtaxMaxRows = 8;
 constexpr int kAtaxMaxStages = 8;
 constexpr int kAtaxSlots = 8;                      // exchange slots; phase 1 runs one panel ahead, needs > 3
