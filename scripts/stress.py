@@ -23,8 +23,8 @@ for name in ("bicgk", "gesummv", "gemver", "atax", "batax", "dgemvt", "axpydot")
     for (m, n) in [(4096, 4096), (1000, 8192), (8192, 1026), (333, 32768),
                    (100000, 32), (40000, 100), (20000, 256), (9000, 500), (9, 300000), (5000, 1000)]:
         cases.append((name, m, n, {}))
-for c in (1, 2, 4, 8, 16):
-    for (m, n) in [(2048, 4096), (777, 16384), (5000, 2050)]:
+for c in (1, 2, 3, 4, 5, 6, 7, 8, 9, 10, 16):
+    for (m, n) in [(2048, 4096), (777, 16384), (5000, 2050), (633, 8502), (301, 24576), (450, 40960)]:
         for rows in (0, 1):
             cases.append(("atax", m, n, {"atax_cluster": c, "atax_rows": rows}))
 for name, m, n, tune in cases:
