@@ -278,6 +278,9 @@ int   bto_debug_poison_shared_memory(bto_stream_t stream);
 /* Testing hook: `stream`'s partial-sum workspace := NaN patterns (stream-ordered), so that a join
  * reading a partial nobody produced in the same call is loud.                                    */
 int   bto_debug_poison_workspace(bto_stream_t stream);
+/* Both of the above for the host-pointer entry points of section 1: shared memory on the library's
+ * own stream, and the workspace of every stream the library has seen.                            */
+int   bto_debug_poison_all(void);
 /* host_dst[0 .. count) = value with the copy threads (first touch of fresh pages in
  * parallel: the NaN prefill of a large output, runtime.py:99-150, at 30+ GB/s).   */
 int   bto_fill_host(double *host_dst, long count, double value);

@@ -60,7 +60,7 @@ EXPORTED = tuple(SIGNATURES) + tuple(f"bto_{k}_async" for k in SIGNATURES) + (
     "bto_abi_version", "bto_set_stream", "bto_set_tuning", "bto_get_tuning",
     "bto_kernel_launches", "bto_last_launch_signature", "bto_last_launch_plan", "bto_bytes_min", "bto_device_info",
     "bto_workspace_bytes", "bto_release_workspace", "bto_reserve_workspace", "bto_copy_to_device", "bto_copy_to_host", "bto_fill_host",
-    "bto_debug_poison_shared_memory", "bto_debug_poison_workspace",
+    "bto_debug_poison_shared_memory", "bto_debug_poison_workspace", "bto_debug_poison_all",
 )
 
 _lib = None
@@ -147,6 +147,8 @@ def load() -> ctypes.CDLL:
     lib.bto_copy_to_host.argtypes = [_P, _P, _L]
     lib.bto_debug_poison_shared_memory.restype = c_int
     lib.bto_debug_poison_shared_memory.argtypes = [_S]
+    lib.bto_debug_poison_all.restype = c_int
+    lib.bto_debug_poison_all.argtypes = []
     lib.bto_debug_poison_workspace.restype = c_int
     lib.bto_debug_poison_workspace.argtypes = [_S]
     lib.bto_fill_host.restype = c_int
@@ -187,6 +189,12 @@ def poison_shared_memory() -> None:
     """Testing hook: every SM's shared memory := NaN bit patterns, on torch's current stream."""
     import torch
     check(load().bto_debug_poison_shared_memory(ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)))
+
+
+def poison_all() -> None:
+    """Testing hook: shared memory on the library's stream and every stream's workspace := NaN patterns
+    (what the host-pointer entry points run on)."""
+    check(load().bto_debug_poison_all())
 
 
 def poison_workspace() -> None:

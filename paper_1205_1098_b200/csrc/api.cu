@@ -716,6 +716,28 @@ int bto_debug_poison_workspace(bto_stream_t stream)
     return BTO_OK;
 }
 
+// Testing hook for the host-pointer entry points (they run on the library's stream): shared memory
+// on that stream and EVERY stream's workspace := NaN patterns.
+int bto_debug_poison_all(void)
+{
+    AsyncCall ac;
+    if (ac.rc != BTO_OK) return ac.rc;
+    for (auto &entry : ac.ctx->streams) {
+        if (entry.second.cur.ptr && entry.second.cur.bytes) {
+            CUDA_TRY(cudaMemsetAsync(entry.second.cur.ptr, 0xFF, entry.second.cur.bytes, entry.first));
+        }
+    }
+    static bool configured = false;
+    const int bytes = 227 * 1024;
+    if (!configured) {
+        CUDA_TRY(cudaFuncSetAttribute(poison_shared_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+        configured = true;
+    }
+    poison_shared_kernel<<<ac.ctx->sm_count * 4, 1024, bytes, ac.ctx->stream>>>(bytes / 8);
+    CUDA_TRY(cudaGetLastError());
+    return BTO_OK;
+}
+
 int bto_fill_host(double *host_dst, long count, double value)
 {
     if (count < 0 || (count > 0 && !host_dst)) return fail(BTO_ERR_INVALID, "fill_host: bad argument");

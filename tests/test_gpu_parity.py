@@ -177,6 +177,9 @@ def test_no_kernel_depends_on_shared_memory_it_did_not_write(bto_lib, oracle):
                     _native.poison_shared_memory()
                     _native.poison_workspace()      # ... nor on partials no producer wrote in this call
                     assert_matches(name, run_device(name, inputs, ext), want, ext, f"poisoned {tune}")
+                if (m + n) % 3 == 0:          # and through the host-pointer entry points (library stream)
+                    _native.poison_all()
+                    assert_matches(name, run_host(name, inputs, ext), want, ext, "poisoned, host operands")
     finally:
         _native.set_tuning(atax_cluster=0, atax_per_sm=1, atax_rows=0)
 
