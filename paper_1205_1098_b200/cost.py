@@ -145,6 +145,40 @@ def _pass_geometry(kind: str, variant: GpuVariant, machine: GpuMachineModel, M: 
     return nstrips, slots, inflight
 
 
+# Co-resident clusters of the single-pass ATAX kernel on a 148-SM B200 (clusters live inside a GPC;
+# profiles/r02/cluster_probe.log) -- what cudaOccupancyMaxActiveClusters answers the library.
+ATAX_CLUSTERS_148 = {1: 148, 2: 74, 3: 45, 4: 33, 5: 26, 6: 22, 7: 15, 8: 15, 9: 15, 10: 11, 16: 7}
+
+
+def atax_cluster_choice(N: int, sm_count: int = 148) -> tuple[int, int, int, int]:
+    """(cluster size, KMAX, rows per panel, co-resident clusters) the library picks for a row of N
+    columns: the restatement of csrc/host_sequences.cuh::plan_atax -- every built size priced as
+    (1150 / TR + 62.5 KMAX) / clusters, ties to the larger SM coverage."""
+    best = None
+    for c, ncl148 in ATAX_CLUSTERS_148.items():
+        w = -(-N // c)
+        w += w & 1
+        if -(-w // 16) * 16 * (c - 1) < N:
+            w = -(-w // 16) * 16
+        if c > 1 and (c - 1) * w >= N:
+            continue
+        kmax = -(-w // 512)
+        if kmax > 8:
+            kmax = 1 << (kmax - 1).bit_length()
+        if kmax > 16 or (kmax == 16 and c < 16):
+            continue
+        if c in (3, 5, 6, 7, 10) and not 5 <= kmax <= 8:
+            continue                                  # the wide-slice sizes are built for 5..8 iterations
+        tr = 8 if kmax <= 2 else 4 if kmax <= 4 else 2 if kmax <= 8 else 1
+        ncl = max(1, ncl148 * sm_count // 148)
+        cost = (1150.0 / tr + 62.5 * kmax) / ncl
+        if best is None or cost < best[0] * 0.999 or (cost < best[0] * 1.001 and ncl * c > best[4] * best[1]):
+            best = (cost, c, kmax, tr, ncl)
+    if best is None:
+        raise ValueError(f"no cluster size holds a row of {N} columns")
+    return best[1], best[2], best[3], best[4]
+
+
 def hbm_traffic(kernel: str, M: int, N: int, variant: GpuVariant | None = None,
                 machine: GpuMachineModel | None = None) -> Traffic:
     """Bytes crossing HBM for one call of `kernel` under `variant`."""
@@ -168,9 +202,11 @@ def hbm_traffic(kernel: str, M: int, N: int, variant: GpuVariant | None = None,
         return Traffic(algo, 0.0, 2 * 8.0 * grid * N, 2, (("N", 8.0 * M * N, 0.0, 128 * 1024),))
     for idx, (kind, reads, writes) in enumerate(_SEQUENCE[seq]):
         if kind == "ATAX":
-            c = variant.get("atax_cluster") or next(c for c in (1, 2, 4, 8, 16)
-                                                    if -(-N // c) <= 4096 or c == 16)
-            clusters = max(1, (machine.sm_count // c) * 13 // 16 if c > 1 else machine.sm_count)
+            c = variant.get("atax_cluster")
+            if c:
+                clusters = max(1, ATAX_CLUSTERS_148.get(c, machine.sm_count // c) * machine.sm_count // 148)
+            else:
+                c, _, _, clusters = atax_cluster_choice(N, machine.sm_count)
             partials += 2 * 8.0 * clusters * N
             passes.append((kind, 8.0 * M * N, 0.0, 64 * 1024))
             continue
@@ -476,7 +512,7 @@ def variant_space(kernel: str) -> list[GpuVariant]:
     out = []
     if kernel in ("atax", "batax"):
         out += [GpuVariant(kernel, (("atax_fused", 1), ("atax_cluster", c), ("atax_rows", r)))
-                for c in (0, 4, 8) for r in (0, 1)]
+                for c in (0, 4, 8, 9) for r in (0, 1)]
         out.append(GpuVariant(kernel, (("atax_fused", 0),)))
         return out
     for rows, vec in ((8, 1), (16, 1), (8, 2)):

@@ -46,6 +46,17 @@ class TestTraffic:
         assert t.passes[1][1] == 8 * N * N
 
 
+def test_atax_cluster_choice_restates_the_library_plan():
+    """cost.atax_cluster_choice is the Python restatement of plan_atax (host_sequences.cuh); the GPU
+    test test_atax_cluster_size_follows_the_slice_width holds the library to the same picks."""
+    picks = {n: C.atax_cluster_choice(n)[:3] for n in (8192, 12288, 20480, 24576, 32768, 40960, 2048, 20000)}
+    assert picks[8192] == (2, 8, 2) and picks[12288] == (3, 8, 2) and picks[20480] == (5, 8, 2)
+    assert picks[24576] == (6, 8, 2) and picks[32768] == (9, 8, 2) and picks[40960] == (10, 8, 2)
+    assert picks[2048][0] == 1 and picks[20000][0] in (5, 9)
+    with pytest.raises(ValueError):
+        C.atax_cluster_choice(16 * 8192 + 2)
+
+
 class TestAnalytic:
     def test_fused_atax_beats_two_pass(self):
         g = bto.load_graph("atax")
