@@ -71,6 +71,22 @@ _SEQUENCES = {
 }
 
 
+def _is_reference_graph(graph) -> bool:
+    """matfuse's DataflowGraph (graph.py): carries `.data` (name -> typed node) and `.spec`."""
+    return hasattr(graph, "data") and hasattr(graph, "spec") and not isinstance(graph, TypedSpec)
+
+
+def _spec_from_reference(graph) -> KernelSpec:
+    """The reference's parsed spec (lang.py dataclasses) as this package's KernelSpec."""
+    from .spec import Decl
+    spec = graph.spec
+    return KernelSpec(
+        spec.name,
+        tuple((n, Decl(d.kind, d.orientation)) for n, d in spec.inputs),
+        tuple((n, Decl(d.kind, d.orientation)) for n, d in spec.outputs),
+        tuple((s.target, _convert_expr(s.value)) for s in spec.statements))
+
+
 def _as_typed(graph) -> TypedSpec:
     if isinstance(graph, TypedSpec):
         return graph
@@ -78,6 +94,8 @@ def _as_typed(graph) -> TypedSpec:
         return infer_shapes(graph)
     if isinstance(graph, str):
         return infer_shapes(parse_kernel(graph))
+    if _is_reference_graph(graph):
+        return infer_shapes(_spec_from_reference(graph))
     raise TypeError(f"cannot interpret {type(graph).__name__} as a kernel spec")
 
 
@@ -107,47 +125,33 @@ def gpu_kernel(graph, allow_generic: bool = True, allow_emitted: bool = True) ->
     cemit.py:54-72); failing that (unless `allow_generic=False`, which raises
     UnsupportedKernelError) the generic unfused executor of generic.py."""
     from .spec import UnsupportedKernelError
-    typed = _as_typed(graph) if not hasattr(graph, "data") else None
-    spec = typed.spec if typed is not None else graph.spec
-    if typed is not None:
-        try:
-            name = match_corpus(spec)
-        except UnsupportedKernelError:
-            from .colmajor import column_major_variant
-            cm = column_major_variant(spec)
-            if cm is not None:      # a corpus kernel on column-major matrices: fused, roles swapped
-                return GeneratedKernel(
-                    source=f"libbto_b200:colmajor:{cm}", kernel_name=spec.name.lower(),
-                    params=_c_params(spec.inputs, spec.outputs, typed.extent_names),
-                    organism_key="colmajor " + _SEQUENCES[cm])
-            if allow_emitted:
-                from .cuemit import emitted_kernel_for
-                try:
-                    emitted = emitted_kernel_for(typed)
-                except ToolchainError:
-                    emitted = None
-                if emitted is not None:
-                    return emitted
-            if not allow_generic:
-                raise
+    typed = _as_typed(graph)          # (the reference's own DataflowGraph is converted)
+    spec = typed.spec
+    params = _c_params(spec.inputs, spec.outputs, typed.extent_names)
+    try:
+        name = match_corpus(spec)
+    except UnsupportedKernelError:
+        from .colmajor import column_major_variant
+        cm = column_major_variant(spec)
+        if cm is not None:      # a corpus kernel on column-major matrices: fused, roles swapped
             return GeneratedKernel(
-                source="libbto_b200:generic", kernel_name=spec.name.lower(),
-                params=_c_params(spec.inputs, spec.outputs, typed.extent_names),
-                organism_key="gpu-unfused{" + " ".join(str(i + 1) for i in range(len(spec.statements))) + "}")
-        extent_names = typed.extent_names
-    else:
-        # the reference's DataflowGraph: re-parse its printed spec with our parser
-        from .spec import Decl
-        ours = KernelSpec(
-            spec.name,
-            tuple((n, Decl(d.kind, d.orientation)) for n, d in spec.inputs),
-            tuple((n, Decl(d.kind, d.orientation)) for n, d in spec.outputs),
-            tuple((s.target, _convert_expr(s.value)) for s in spec.statements))
-        name = match_corpus(ours)
-        extent_names = tuple(graph.extent_names)
+                source=f"libbto_b200:colmajor:{cm}", kernel_name=spec.name.lower(), params=params,
+                organism_key="colmajor " + _SEQUENCES[cm])
+        if allow_emitted:
+            from .cuemit import emitted_kernel_for
+            try:
+                emitted = emitted_kernel_for(graph if _is_reference_graph(graph) else typed)
+            except ToolchainError:
+                emitted = None
+            if emitted is not None:
+                return emitted
+        if not allow_generic:
+            raise
+        return GeneratedKernel(
+            source="libbto_b200:generic", kernel_name=spec.name.lower(), params=params,
+            organism_key="gpu-unfused{" + " ".join(str(i + 1) for i in range(len(spec.statements))) + "}")
     return GeneratedKernel(
-        source=f"libbto_b200:{name}", kernel_name=name,
-        params=_c_params(spec.inputs, spec.outputs, extent_names),
+        source=f"libbto_b200:{name}", kernel_name=name, params=params,
         organism_key=_SEQUENCES[name])
 
 

@@ -89,6 +89,16 @@ def test_specs_outside_the_hand_written_set_get_fused_emitted_code(tmp_path, mon
         assert [n for _, n in kernel.params] == [n for n, _ in typed.spec.inputs + typed.spec.outputs] + list(typed.extent_names)
         _, emitted, ir = cuemit.emitted_entry(kernel.source)
         assert ir == stored[key]["ir"] and "_region0" in emitted.source
+    # the reference's own DataflowGraph is accepted in place of a TypedSpec: corpus kernels get the
+    # hand-written sequence, anything else the same emitted code
+    import matfuse
+    from matfuse.corpus import load_graph as ref_load
+    from matfuse.graph import build_dataflow, infer_types
+    assert bto.gpu_kernel(ref_load("gemver")).source == "libbto_b200:gemver"
+    ref_mixed = infer_types(build_dataflow(matfuse.parse_kernel(S.format_kernel(S.parse_kernel(SPECS["mixed"])))))
+    k = bto.gpu_kernel(ref_mixed)
+    assert k.source.startswith("emitted:") and k.organism_key == stored["mixed"]["ir"]["organism"]
+    assert bto.gpu_kernel(ref_mixed, allow_emitted=False).source == "libbto_b200:generic"
     # without the toolchain the unfused executor answers
     monkeypatch.setattr(cuemit.NvccToolchain, "available", property(lambda self: False))
     assert bto.gpu_kernel(S.infer_shapes(S.parse_kernel(SPECS["mixed"]))).source.endswith(":generic")
