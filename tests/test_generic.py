@@ -12,6 +12,7 @@ import torch
 import golden_util as G
 import np_interp
 import paper_1205_1098_b200 as bto
+from paper_1205_1098_b200 import _native
 from paper_1205_1098_b200 import spec as S
 
 
@@ -121,6 +122,7 @@ def test_emitted_fused_code_for_specs_outside_the_hand_written_set(bto_lib, tmp_
         inputs = bto.random_inputs(typed, ext, seed=case["seed"])
         want = np_interp.evaluate(typed.spec, inputs)
         tol = 1e-12 * max(1.0, math.log2(max(ext.values())))
+        _native.poison_shared_memory()
         got = bto.run_kernel(bto.library_path(), kernel, typed, inputs, ext)
         assert bto.max_rel_error(got, want) <= tol, (key, ext)
         for name, head in case["out"].items():          # the reference's own O1 values
