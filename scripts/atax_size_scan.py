@@ -18,6 +18,8 @@ ops = GpuShardOps()
 shapes = [(8192, 8192), (10240, 10240), (12288, 12288), (16384, 16384), (20480, 20480), (24576, 24576),
           (28672, 28672), (32768, 32768), (30000, 30000), (20000, 18000), (50000, 6000), (16384, 2560),
           (65536, 1536), (12000, 40960)]
+if len(sys.argv) > 1:          # atax_size_scan.py 4096x65536 2048x131072 ...
+    shapes = [tuple(int(v) for v in a.split("x")) for a in sys.argv[1:]]
 for (m, n) in shapes:
     A = torch.rand(m, n, dtype=torch.float64, device="cuda")
     x = torch.rand(n, dtype=torch.float64, device="cuda")
