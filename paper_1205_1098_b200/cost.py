@@ -216,7 +216,7 @@ def hbm_traffic(kernel: str, M: int, N: int, variant: GpuVariant | None = None,
             if "T" in kind:
                 partials += 2 * 8.0 * machine.sm_count * (variant.get("grid_per_sm") or 4) * N
                 joins += 1
-        elif kind == "NN" and N >= 4096 and M >= 4 * machine.sm_count and variant.get("rowstream", 1):
+        elif kind == "NN" and (N >= 4096 or N <= 2048) and M >= 4 * machine.sm_count and variant.get("rowstream", 1):
             pass                        # whole-row streaming (csrc/rowstream_kernels.cuh): no partials, no join
         else:
             if "N" in kind:

@@ -412,8 +412,12 @@ struct Pass {
         M = m;
         N = n;
         // two-matrix row dots of a wide matrix: stream whole rows (7.3 vs 6.9-7.07 TB/s at n = 24576)
+        // ... and of a narrow one: one launch and no partials beat the strips up to N = 2048 (graph
+        // replay, profiles/r02/gesummv_rowstream_mid.log: n = 2000 -- the reference's acceptance size --
+        // 15.2 -> 12.3 us, 1536 9.2 -> 8.1, 2048 13.1 -> 12.0; at 2500 / 3072 the strips win, 22.0 vs 24.6 us)
+        const bool wide_or_narrow = n >= g_tuning.rowstream_min_n || (g_tuning.midsize && n <= 2048);
         rowstream = (FLAGS == (kFlagN | kFlagN2) || (FLAGS == kFlagN && g_tuning.rowstream == 2)) &&
-                    aligned && g_tuning.rowstream != 0 && n >= g_tuning.rowstream_min_n && m >= 4L * c.sm_count;
+                    aligned && g_tuning.rowstream != 0 && wide_or_narrow && m >= 4L * c.sm_count;
         if (rowstream) return BTO_OK;
         // (a full 512-column strip of a rank-2 pass is mv_tile_kernel's best case: 5.9 vs 4.9 TB/s)
         if (skinny_applies(N, aligned) && !((FLAGS & kFlagRank2) && N == kSkinnyMaxN)) {
