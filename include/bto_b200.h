@@ -231,9 +231,11 @@ int   bto_set_stream(bto_stream_t stream);      /* stream for section-1 calls */
 /* Tunables of the launch heuristics (what the GPU variant search explores):
  * "mv_rows" (8|16|32 rows per unit), "mv_vec" (1|2 double2 per thread per row),
  * "grid_per_sm" (0 = default), "mv_minb", "vec_unroll" (1|2|4), "atax_fused",
- * "atax_cluster", "atax_rows", "atax_stages", "host_pipeline", "host_panel_mib",
- * "rowstream" (0|1|2: wide GESUMMV streams whole rows, rowstream_kernels.cuh; 2 also the
- * single-matrix A x pass -- measured: no gain),
+ * "atax_cluster" (0 = chosen by the cost model of host_sequences.cuh::plan_atax, or 1..10 | 16 CTAs
+ * per cluster), "atax_rows", "atax_stages", "atax_per_sm" (1|2), "host_pipeline", "host_panel_mib",
+ * "rowstream" (0|1|2: GESUMMV streams whole rows, rowstream_kernels.cuh, for N >= 4096 and -- with
+ * "midsize" -- for N <= 2048; 2 also the single-matrix A x pass -- measured: no gain),
+ * "midsize" (0|1: size-aware launch shapes below the bench sizes), "direct_cols" (0|1),
  * "skinny" (0|1: N <= 512 takes the shared-row kernels of skinny_kernels.cuh),
  * "host_bounce" (0|1: pageable host operands of 16 MiB and more go through pinned
  * bounce slots), "host_threads" (host threads filling the slots, 0 = auto),
